@@ -1,0 +1,97 @@
+"""Traffic and time bounds of the ring allreduce (and App. A planner values).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+P:78 (§5.1 Overhead Analysis): "a ReduceScatter retains only a 1/n shard and
+must send (n-1)/n D_total; an AllGather must receive the same amount ... The
+NCCL's ring algorithm realizes these lower bounds."  P:121: "The time for a
+ring AllReduce is given by 2(ng-1)/(ng) x D/B."  P:122-136 and App. A
+(P:358-447): T1, T2, T3, T(Y), Y*, threshold.  nccl-tests bus bandwidth
+(the paper's tool): busbw = algbw * 2(n-1)/n.
+"""
+from __future__ import annotations
+
+
+def ring_allreduce_time(n: int, g: int, D: float, B: float) -> float:
+    """2(ng-1)/(ng) * D/B."""
+    ng = n * g
+    return 2 * (ng - 1) / ng * D / B
+
+
+def busbw(S_bytes: float, seconds: float, n: int) -> float:
+    """nccl-tests bus bandwidth (bytes/s)."""
+    return S_bytes / seconds * 2 * (n - 1) / n if n > 1 else 0.0
+
+
+def nvlink_bytes_per_gpu(S: float, n: int) -> float:
+    """Bytes each GPU sends (= receives) in a push ring allreduce: 2(n-1)/n S."""
+    return 2 * (n - 1) / n * S
+
+
+def hbm_bytes_per_gpu(S: float, n: int) -> float:
+    """Algorithmic HBM bytes per GPU (push ring, registered recv, fused final
+    add): reads (3n-3)/n S + writes (2n-1)/n S = (5n-4)/n S.
+
+    RS steps 0..n-2: read x slice (n-1 times), read scratch (n-2 times),
+    write peer scratch lands in the peer's HBM (counted at the receiver:
+    n-1 writes).  Final add: read scratch + x, write own recv (1 + 1 reads,
+    1 write), the peer's recv write lands remotely.  AG: n-2 forwards read own
+    recv; every shard except the own one lands in recv from the peer (n-1
+    writes).  Per shard unit (S/n): reads (n-1)+(n-2)+2+(n-2) = 3n-3,
+    writes (n-1)+1+(n-1) = 2n-1.
+    """
+    return (5 * n - 4) / n * S
+
+
+def hbm_bytes_sim(S: float, k: int) -> float:
+    """1-GPU simulated-rank mode with k ranks: all ranks' traffic is local:
+    (5k-4)/k S per rank x k ranks."""
+    return (5 * k - 4) * S
+
+
+def degraded_bound(healthy_busbw: float, K: int, dead: int = 1, strategy: str = "BALANCE") -> float:
+    """Surviving-bandwidth bound: Balance (K-dead)/K of healthy;
+    HotRepair model: the backup carries 2x -> 1/2."""
+    if strategy == "HOT_REPAIR":
+        return healthy_busbw * 0.5
+    return healthy_busbw * (K - dead) / K
+
+
+# ------------------------------------------------------------- App. A (NEXT)
+
+def stage_times(Y: float, n: int, g: int, X: float, D: float = 1.0, B: float = 1.0):
+    """T1, T2, T3."""
+    if not 0 < X < 1:
+        raise ValueError("X must lie in (0, 1)")
+    a = 2 * (n * g - 1) / (n * g)
+    b = 2 * ((n - 1) * g - 1) / ((n - 1) * g)
+    T1 = a * (1 - Y) * D / ((1 - X) * B)
+    T2 = b * Y * D / (X * B)
+    T3 = Y * D / (X * B)
+    return T1, T2, T3
+
+
+def total_time(Y, n, g, X, D=1.0, B=1.0) -> float:
+    """T(Y) = max(T1, T2) + T3."""
+    T1, T2, T3 = stage_times(Y, n, g, X, D, B)
+    return max(T1, T2) + T3
+
+
+def threshold(n: int, g: int) -> float:
+    """App. A Step 2: X = ng / (3ng - 2)."""
+    return n * g / (3 * n * g - 2)
+
+
+def y_star(n: int, g: int, X: float) -> float:
+    """App. A Step 1: Y* = X + X(1-X) / (X + (g(n-1)-1) n)."""
+    return X + X * (1 - X) / (X + (g * (n - 1) - 1) * n)
+
+
+def optimal_partition(n: int, g: int, X: float) -> float:
+    """App. A Step 3: Y = 0 if X <= threshold else Y*."""
+    return 0.0 if X <= threshold(n, g) else y_star(n, g, X)
+
+
+def bottleneck_load(Y: float, D: float = 1.0) -> float:
+    """Fig. 4 caption: degraded server volume 2(1-Y)D + YD."""
+    return 2 * (1 - Y) * D + Y * D
