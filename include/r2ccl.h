@@ -1,0 +1,313 @@
+/*
+ * r2ccl.h -- C ABI of the B200-native R²CCL hot path (arXiv 2512.25059).
+ *
+ * A fault-tolerant, chunked, multi-channel ring allreduce over NVLink 5 /
+ * NVSwitch peer mappings, one process per GPU (or k simulated ranks on one
+ * GPU).  Citations: P:n = reference PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * The paper's statement of the problem: a drop-in collective
+ * library; communicators come from a one-time bootstrap; a failure
+ * during a collective must not crash the process but be intercepted and
+ * survived transparently.
+ *
+ * Conventions (all entry points):
+ *   - Return codes, never abort: every call returns an r2_result_t.
+ *   - Plain pointers and sizes only.  Device pointers are CUDA device
+ *     addresses of the caller's GPU; "stream" is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).
+ *   - Ownership: the caller owns send/recv buffers and streams; the library
+ *     owns its scratch, flags, mailboxes, IPC mappings, host-mapped control
+ *     blocks and its monitor thread (released by r2_finalize).
+ *   - Threading: one host thread per communicator issues calls (like NCCL);
+ *     only r2_status / r2_get_event may be called concurrently.
+ *   - "collective": every rank of the communicator must make the same call
+ *     in the same order.
+ */
+#ifndef R2CCL_H
+#define R2CCL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define R2_MAX_CHANNELS 16   /* K upper bound                                   */
+#define R2_MAX_LOCAL 16      /* simulated ranks per process upper bound         */
+
+typedef enum {
+  R2_SUCCESS = 0,
+  R2_ERR_INVALID_ARG = 1,    /* bad pointer / size / config / alignment          */
+  R2_ERR_CUDA = 2,           /* a CUDA runtime call failed                       */
+  R2_ERR_BOOTSTRAP = 3,      /* out-of-band bootstrap failed                     */
+  R2_ERR_NOT_REGISTERED = 4, /* recv not inside an r2_register_multi range       */
+  R2_ERR_NO_BACKUP = 5,      /* failover chain exhausted                 */
+  R2_ERR_TIMEOUT = 6,        /* watchdog expired (reading C-13)                  */
+  R2_ERR_INTERNAL = 7
+} r2_result_t;
+
+typedef enum { R2_INT32 = 0, R2_FLOAT32 = 1, R2_BFLOAT16 = 2 } r2_dtype_t;
+
+/* Single-failure strategies (P:57 HotRepair; P:73 R²CCL-Balance). */
+typedef enum { R2_HOT_REPAIR = 0, R2_BALANCE = 1 } r2_strategy_t;
+
+/* Emulated fault kinds (App. C; SURVEY reading C-14). */
+typedef enum {
+  R2_FAULT_LOCAL = 0,   /* sender endpoint (src_rank, channel) dies           */
+  R2_FAULT_REMOTE = 1,  /* receiver endpoint (src_rank+1, channel) dies       */
+  R2_FAULT_LINK = 2,    /* ring link src_rank -> src_rank+1 on channel dies   */
+  R2_FAULT_REPAIR = 3   /* re-admit (src_rank, channel): stand-in for the
+                           periodic re-probe of P:19 / S:345                  */
+} r2_fault_kind_t;
+
+/* Probe outcomes and verdicts (reading C-10). */
+typedef enum { R2_PROBE_SUCCESS = 0, R2_PROBE_LOCAL_ERROR = 1, R2_PROBE_TIMEOUT = 2,
+               R2_PROBE_NOT_RUN = 3 } r2_probe_outcome_t;
+typedef enum {
+  R2_V_NONE = 0, R2_V_LOCAL_ENDPOINT = 1, R2_V_REMOTE_ENDPOINT = 2, R2_V_LINK = 3,
+  R2_V_ENDPOINT_UNREACHABLE_A = 4, R2_V_ENDPOINT_UNREACHABLE_B = 5,
+  R2_V_DUAL_ENDPOINT = 6, R2_V_TWO_LOCAL = 7, R2_V_INCONCLUSIVE = 8
+} r2_verdict_kind_t;
+
+typedef struct r2_comm* r2_comm_t;
+
+/*
+ * Out-of-band transport ("a separate bootstrap network").  A
+ * vtable so that the library is independent of the launcher.  All functions
+ * return 0 on success.  allgather/barrier are collective and blocking;
+ * post is non-blocking (msg <= 256 bytes); poll is non-blocking and returns 1
+ * when a message was received (src, len filled), 0 when none.
+ * r2_oob_shm_open below provides a POSIX shared-memory implementation for
+ * ranks of one node.
+ */
+typedef struct {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* sendbuf, void* recvbuf, size_t bytes);
+  int (*post)(void* ctx, int dst, const void* msg, size_t len);
+  int (*poll)(void* ctx, int* src, void* msg, size_t cap, size_t* len);
+  int (*barrier)(void* ctx);
+} r2_oob_t;
+
+/*
+ * Configuration.  r2_config_default fills the defaults listed here.
+ *   nchannels         K channels (default 8, mirrors 8 NICs/server)
+ *   ctas_per_channel  W CTAs per channel (default 4)
+ *   threads_per_cta   512
+ *   chunk_bytes       per (connection, step) chunk, multiple of 16 (512 KiB;
+ *                     reading C-3)
+ *   max_bytes         largest allreduce payload per rank (scratch sizing;
+ *                     default 1 GiB)
+ *   strategy          R2_BALANCE
+ *   probe_timeout_us  200 (reading C-13)
+ *   watchdog_ms       3000: a kernel waiting longer aborts with R2_ERR_TIMEOUT
+ *   channel_w         K integer weights (NULL = equal) for Balance
+ *   sim_ranks         world == 1 only: k >= 1 simulated ranks on one GPU
+ *                     (send/recv then hold k rank buffers back to back)
+ */
+typedef struct {
+  int nchannels;
+  int ctas_per_channel;
+  int threads_per_cta;
+  size_t chunk_bytes;
+  size_t max_bytes;
+  int strategy;
+  int probe_timeout_us;
+  int watchdog_ms;
+  int channel_w[R2_MAX_CHANNELS];
+  int use_channel_w;
+  int sim_ranks;
+} r2_config_t;
+
+/*
+ * An injected channel fault.  Fires in collective number
+ * at_seq (1 = first r2_allreduce of the communicator) when channel `channel`
+ * of sender `src_rank` starts the item (step, chunk) of origin channel
+ * `origin_channel` (-1 = its own items): the first byte_offset bytes of that
+ * item's part reach the peer (rounded down to 16 bytes), no completion flag
+ * is written (reading C-6), the transport is dead from then on
+ * (every later item of that channel, in (step, origin, chunk) order, is
+ * undelivered).  The sender's error becomes visible after detect_delay_us.
+ * poison: fill the rest of the faulted item at the peer with 0xFF.
+ * REPAIR: before collective at_seq, the endpoint/link is healthy again.
+ */
+typedef struct {
+  uint64_t at_seq;
+  int src_rank;
+  int channel;
+  int origin_channel;
+  int kind;          /* r2_fault_kind_t */
+  int step;
+  int chunk;
+  uint64_t byte_offset;
+  int detect_delay_us;
+  int poison;
+} r2_fault_t;
+
+typedef struct {
+  int kind;          /* r2_verdict_kind_t */
+  int a, b, aux;     /* endpoint ranks A (detector), B (its peer), aux (-1 none) */
+  int channel;
+  int outcome[4];    /* A->B, B->A, aux->A, aux->B (r2_probe_outcome_t)      */
+} r2_verdict_t;
+
+/* One failover record: a re-planned origin channel of one sender rank. */
+typedef struct {
+  uint64_t seq;
+  int rank;               /* sender rank of the connection                    */
+  int origin_channel;     /* whose items were rolled back / re-placed          */
+  int stopped_channel;    /* the stopped channel that triggered it             */
+  r2_verdict_t verdict;
+  int resume;             /* first stream position without completion  */
+  int floor;              /* last contiguously confirmed position             */
+  int retransmit;         /* items re-placed (exactly those w/o completion)   */
+  int strategy;
+  int assignee;           /* HOT_REPAIR: adopting channel; -1 otherwise       */
+  int chain_pos;          /* its position in the failover chain        */
+  int shares[R2_MAX_CHANNELS]; /* BALANCE: 16-B vectors of a full chunk/channel */
+  int error;              /* R2_SUCCESS or R2_ERR_NO_BACKUP                   */
+  /* timing: device %globaltimer ns on the sender's GPU, host CLOCK_MONOTONIC ns */
+  uint64_t t_fire_dev_ns, t_first_retx_dev_ns;
+  uint64_t t_detect_host_ns, t_verdict_host_ns, t_plan_host_ns;
+  double failover_ms;     /* t_first_retx_dev - t_fire_dev (-1 if unknown)     */
+} r2_event_t;
+
+typedef struct {
+  uint64_t seq;               /* collectives enqueued so far                       */
+  int last_error;             /* most recent asynchronous error (r2_result_t)     */
+  uint64_t last_error_seq;
+  int n_events;
+  int world, nlocal, nchannels;
+  uint32_t dead_endpoints[R2_MAX_LOCAL * 4]; /* bit c of word r: endpoint (r,c) */
+  uint32_t dead_links[R2_MAX_LOCAL * 4];     /* bit c of word r: link r->r+1    */
+  uint64_t bytes[R2_MAX_LOCAL][R2_MAX_CHANNELS]; /* bytes pushed per local rank/channel */
+} r2_status_t;
+
+/* Fill *cfg with the defaults documented above. */
+void r2_config_default(r2_config_t* cfg);
+
+/*
+ * r2_init -- collective.  One-time bootstrap + multi-registration
+ * (P:25-27): allocates this rank's scratch (2(n-1)/n * max_bytes),
+ * per-chunk flag words, part counters, emulated link state and probe
+ * mailboxes, exports them over CUDA IPC and maps EVERY peer's (not only the
+ * ring neighbours'), so that no mapping is created on the recovery path.
+ * Starts the monitor thread.  rank in [0, world); cuda_dev = device ordinal.
+ * world == 1 with cfg->sim_ranks = k runs k simulated ranks (oob may be NULL).
+ * Errors: INVALID_ARG, CUDA, BOOTSTRAP.  *out is NULL on error.
+ */
+r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob,
+                    const r2_config_t* cfg, r2_comm_t* out);
+
+/*
+ * r2_register_multi -- collective.  Registers the allocation that contains
+ * [dptr, dptr+bytes) with every peer (IPC export + open on all ranks,
+ * P:27 "registering each GPU buffer with multiple NICs at initialization").
+ * recv buffers of r2_allreduce must lie in a registered range; send buffers
+ * need not.  *reg_out receives an id (same on all ranks).
+ * Errors: INVALID_ARG (NULL / not a device pointer), CUDA, BOOTSTRAP.
+ */
+r2_result_t r2_register_multi(r2_comm_t comm, void* dptr, size_t bytes, uint64_t* reg_out);
+
+/* r2_deregister -- collective.  Unmaps a registration on every rank. */
+r2_result_t r2_deregister(r2_comm_t comm, uint64_t reg);
+
+/*
+ * r2_allreduce -- collective, asynchronous on `stream`.  Sum-allreduce of
+ * `count` elements (P:94 ring ReduceScatter + AllGather).  send == recv
+ * (in-place) is allowed.  Both pointers 16-byte aligned.  count == 0 is a
+ * no-op; count * elem size <= cfg.max_bytes.  In sim mode (k ranks) send and
+ * recv each hold k buffers of count elements back to back and need no
+ * registration.  Result (reading C-8): for element i of shard s,
+ * y[i] = fold(x_{s+1}[i], ..., x_{s+n-1}[i], x_s[i]) with per-hop rounding
+ * (int32 wraps, fp32 RN, bf16 = RNE(fp32 add)); bit-identical with and without
+ * faults.  A channel fault mid-collective is recovered inside the call's
+ * stream work; the stream is released only when the result is complete.  An
+ * unrecoverable failure (NO_BACKUP, TIMEOUT) still releases the stream (result
+ * undefined) and is reported by the next r2_* call and r2_status.last_error.
+ * Errors: INVALID_ARG, NOT_REGISTERED, CUDA, and pending async errors.
+ */
+r2_result_t r2_allreduce(r2_comm_t comm, const void* send, void* recv, size_t count,
+                         r2_dtype_t dt, void* stream);
+
+/*
+ * r2_allreduce_host -- as r2_allreduce, but send/recv are HOST buffers (pinned
+ * memory recommended).  Enqueues H2D copy into a library-owned registered
+ * device buffer, the allreduce and the D2H copy on `stream`; the caller
+ * synchronizes the stream before reading recv.
+ */
+r2_result_t r2_allreduce_host(r2_comm_t comm, const void* send, void* recv, size_t count,
+                              r2_dtype_t dt, void* stream);
+
+/*
+ * r2_inject_fault -- collective (same descriptor on all ranks, before the
+ * targeted seq; like SPEC's scenario fault list S:362).  Arms an emulated
+ * channel fault (NVLink faults cannot be injected on a live box).
+ * Errors: INVALID_ARG.
+ */
+r2_result_t r2_inject_fault(r2_comm_t comm, const r2_fault_t* f);
+
+/*
+ * r2_probe -- one three-point triangulation round for connection
+ * (rank -> peer, channel) started by this rank: zero-byte probe-flag kernels
+ * A->B, B->A, aux->A, aux->B (aux = lowest rank not in {A,B}, reading C-12),
+ * outcome per reading C-11, verdict per reading C-10.  Peer and aux answer
+ * through their monitor threads (no call needed on their side).  Blocks
+ * until the verdict.  In sim mode `rank_local` selects the simulated prober.
+ */
+r2_result_t r2_probe(r2_comm_t comm, int rank_local, int peer, int channel, r2_verdict_t* out);
+
+/* r2_status -- thread-safe snapshot (waits for nothing). */
+r2_result_t r2_status(r2_comm_t comm, r2_status_t* out);
+
+/* r2_get_event -- idx-th failover record (0 <= idx < n_events). */
+r2_result_t r2_get_event(r2_comm_t comm, int idx, r2_event_t* out);
+
+/*
+ * r2_sync -- synchronize the last stream used by r2_allreduce and return the
+ * async error of the collectives completed since the previous r2_sync.
+ */
+r2_result_t r2_sync(r2_comm_t comm);
+
+/* r2_finalize -- collective.  Stops the monitor, unmaps peers, frees all. */
+r2_result_t r2_finalize(r2_comm_t comm);
+
+const char* r2_strerror(r2_result_t r);
+
+/* ------------------------------------------------------------------------
+ * Host logic, exposed for parity tests (no GPU needed).
+ * ---------------------------------------------------------------------- */
+
+/* Decision table C-10.  outcome[2..3] ignored if !has_aux. */
+int r2_triangulate(const int outcome[4], int has_aux);
+
+/* Balance shares (reading C-15): floor(R*w_c/Σw) over
+ * channels whose bit is set in healthy_mask, remainder to the largest weight
+ * (ties: lowest id).  shares_out[K].  Returns R2_ERR_NO_BACKUP if mask empty. */
+r2_result_t r2_balance_shares(uint64_t R, const int* w, uint32_t healthy_mask, int K,
+                              uint64_t* shares_out);
+
+/* Failover chain of channel c (reading C-2): c+1, ..., c+K-1 mod K. */
+void r2_failover_chain(int c, int K, int* out);
+
+/* Rollback on a completion ledger. */
+void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
+
+/* Geometry of one allreduce (SURVEY §8 header, reading C-3). */
+typedef struct {
+  uint64_t N, Np, shard, slice, chunk; /* elements */
+  int n, K, W, V, m, steps;
+} r2_geometry_t;
+r2_result_t r2_geometry(uint64_t count, r2_dtype_t dt, int n, int K, int W,
+                        size_t chunk_bytes, r2_geometry_t* out);
+
+/* POSIX shared-memory OOB for ranks of one node.  `name` must be identical
+ * on all ranks and unique per communicator (e.g. from the launcher's store).
+ * Rank 0 creates the segment; others attach (waits up to 60 s). */
+r2_result_t r2_oob_shm_open(const char* name, int rank, int world, r2_oob_t* out);
+r2_result_t r2_oob_shm_close(r2_oob_t* oob);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* R2CCL_H */

@@ -1,0 +1,620 @@
+// r2_comm.cpp -- the C ABI of the R²CCL hot path: bootstrap + multi-
+// registration, per-call planning (the
+// planner reads the health records; plan-time Balance / HotRepair for dead
+// channels), the allreduce launch, fault injection, probes and status.
+#include "r2_comm.h"
+
+#include <cuda.h>
+#include <string.h>
+#include <time.h>
+
+#include <algorithm>
+#include <chrono>
+#include <thread>
+
+namespace {
+
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t e_ = (x);                      \
+    if (e_ != cudaSuccess) return R2_ERR_CUDA; \
+  } while (0)
+
+int elem_bytes(r2_dtype_t dt) { return dt == R2_BFLOAT16 ? 2 : 4; }
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
+  ArenaLayout L{};
+  const size_t q = (size_t)n * K * 16;
+  L.slot_bytes = std::max<size_t>(align_up(std::max<size_t>(max_bytes, 16), q) / n, 16 * K);
+  const size_t slice_cap = L.slot_bytes / K;
+  L.m_cap = (int)std::max<size_t>((slice_cap + chunk - 1) / chunk, (size_t)W);
+  const int steps = n > 1 ? 2 * n - 2 : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  L.scratch = take((size_t)2 * std::max(n - 1, 1) * L.slot_bytes);
+  L.flags = take((size_t)steps * K * L.m_cap * 4);
+  L.counters = take((size_t)steps * K * L.m_cap * 8);
+  L.ep_dead = take((size_t)n * K * 4);
+  L.link_dead = take((size_t)n * K * 4);
+  L.alert = take(4);
+  L.mailbox = take((size_t)n * K * 4);
+  L.desc = take(8 * 8);
+  L.misc = take(sizeof(MiscDev));
+  L.stage = take(L.slot_bytes);
+  L.total = align_up(off, 4096);
+  return L;
+}
+
+RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
+  RankPtrs p;
+  p.scratch = base + L.scratch;
+  p.flags = (unsigned int*)(base + L.flags);
+  p.counters = (unsigned long long*)(base + L.counters);
+  p.ep_dead = (unsigned int*)(base + L.ep_dead);
+  p.link_dead = (unsigned int*)(base + L.link_dead);
+  p.alert = (unsigned int*)(base + L.alert);
+  p.mailbox = (unsigned int*)(base + L.mailbox);
+  p.desc = (unsigned long long*)(base + L.desc);
+  p.misc = (MiscDev*)(base + L.misc);
+  p.stage = base + L.stage;
+  return p;
+}
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+r2_result_t alloc_base(void* dptr, char** base, size_t* size) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+      return R2_ERR_CUDA;
+    fn = (PFN_getAddressRange)f;
+  }
+  CUdeviceptr b = 0;
+  size_t s = 0;
+  if (fn(&b, &s, (CUdeviceptr)dptr) != CUDA_SUCCESS) return R2_ERR_INVALID_ARG;
+  *base = (char*)b;
+  *size = s;
+  return R2_SUCCESS;
+}
+
+struct RegXchg {
+  cudaIpcMemHandle_t h;
+  unsigned long long base, dptr, bytes;
+};
+
+// Open (or reuse) the IPC mapping of `peer`'s allocation `base`.
+r2_result_t open_peer(r2_comm* c, int peer, const RegXchg& x, void** out) {
+  auto key = std::make_pair(peer, (unsigned long long)x.base);
+  auto it = c->ipc_cache.find(key);
+  if (it != c->ipc_cache.end()) {
+    it->second.second++;
+    *out = it->second.first;
+    return R2_SUCCESS;
+  }
+  void* p = nullptr;
+  if (cudaIpcOpenMemHandle(&p, x.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return R2_ERR_CUDA;
+  c->ipc_cache[key] = std::make_pair(p, 1);
+  *out = p;
+  return R2_SUCCESS;
+}
+
+void close_peer(r2_comm* c, void* p) {
+  for (auto it = c->ipc_cache.begin(); it != c->ipc_cache.end(); ++it)
+    if (it->second.first == p) {
+      if (--it->second.second == 0) {
+        cudaIpcCloseMemHandle(p);
+        c->ipc_cache.erase(it);
+      }
+      return;
+    }
+}
+
+int take_async_error(r2_comm* c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  int e = c->unreported_error;
+  c->unreported_error = R2_SUCCESS;
+  return e;
+}
+
+}  // namespace
+
+uint64_t r2_now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (uint64_t)ts.tv_sec * 1000000000ull + ts.tv_nsec;
+}
+
+extern "C" void r2_config_default(r2_config_t* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->nchannels = 8;
+  cfg->ctas_per_channel = 4;
+  cfg->threads_per_cta = 512;
+  cfg->chunk_bytes = 512 * 1024;
+  cfg->max_bytes = (size_t)1 << 30;
+  cfg->strategy = R2_BALANCE;
+  cfg->probe_timeout_us = 200;
+  cfg->watchdog_ms = 3000;
+  cfg->use_channel_w = 0;
+  for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
+  cfg->sim_ranks = 1;
+}
+
+extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,
+                               r2_comm_t* out) {
+  if (!out) return R2_ERR_INVALID_ARG;
+  *out = nullptr;
+  r2_config_t cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else r2_config_default(&cfg);
+  if (world < 1 || rank < 0 || rank >= world) return R2_ERR_INVALID_ARG;
+  if (cfg.nchannels < 1 || cfg.nchannels > R2_MAXK || cfg.ctas_per_channel < 1 || cfg.ctas_per_channel > R2_MAXW)
+    return R2_ERR_INVALID_ARG;
+  if (cfg.threads_per_cta < 32 || cfg.threads_per_cta > 512 || cfg.threads_per_cta % 32) return R2_ERR_INVALID_ARG;
+  if (cfg.chunk_bytes < 16 || cfg.chunk_bytes % 16 || cfg.max_bytes < 16) return R2_ERR_INVALID_ARG;
+  if (cfg.strategy != R2_HOT_REPAIR && cfg.strategy != R2_BALANCE) return R2_ERR_INVALID_ARG;
+  if (cfg.sim_ranks < 1 || cfg.sim_ranks > R2_MAXL || (world > 1 && cfg.sim_ranks != 1)) return R2_ERR_INVALID_ARG;
+  if (world > 1 && (!oob || !oob->allgather || !oob->post || !oob->poll || !oob->barrier)) return R2_ERR_INVALID_ARG;
+  if (world > R2_MAX_LOCAL * 4) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(cuda_dev) != cudaSuccess) return R2_ERR_CUDA;
+
+  r2_comm* c = new r2_comm();
+  c->rank = rank;
+  c->world = world;
+  c->dev = cuda_dev;
+  c->cfg = cfg;
+  c->sim = (world == 1 && cfg.sim_ranks > 1);
+  c->n = c->sim ? cfg.sim_ranks : world;
+  c->nlocal = c->sim ? c->n : 1;
+  c->first_rank = c->sim ? 0 : rank;
+  c->K = cfg.nchannels;
+  c->W = cfg.ctas_per_channel;
+  c->threads = cfg.threads_per_cta;
+  for (int k = 0; k < c->K; ++k) c->weights[k] = cfg.use_channel_w ? (unsigned)std::max(cfg.channel_w[k], 1) : 1u;
+  if (oob) {
+    c->oob = *oob;
+    c->has_oob = world > 1;
+  }
+  c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes);
+  const int steps = c->n > 1 ? 2 * c->n - 2 : 1;
+  auto fail = [&](r2_result_t e) {
+    delete c;
+    return e;
+  };
+  if ((long long)steps * c->lay.m_cap > R2_BITMAP_WORDS * 32) return fail(R2_ERR_INVALID_ARG);
+  if (c->n > 1) {
+    c->max_coop = r2_max_coop_ctas(c->threads);
+    if (c->nlocal * c->K * c->W > c->max_coop) return fail(R2_ERR_INVALID_ARG);
+  }
+
+  // ---- arenas (scratch, flags, counters, fabric state, mailboxes)
+  c->arena.resize(c->nlocal);
+  c->ctrl_host.resize(c->nlocal);
+  c->ctrl_dev.resize(c->nlocal);
+  for (int l = 0; l < c->nlocal; ++l) {
+    if (cudaMalloc(&c->arena[l], c->lay.total) != cudaSuccess) return fail(R2_ERR_CUDA);
+    if (cudaMemset(c->arena[l], 0, c->lay.total) != cudaSuccess) return fail(R2_ERR_CUDA);
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, sizeof(Ctrl), cudaHostAllocMapped) != cudaSuccess) return fail(R2_ERR_CUDA);
+    memset(h, 0, sizeof(Ctrl));
+    c->ctrl_host[l] = (Ctrl*)h;
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(R2_ERR_CUDA);
+    c->ctrl_dev[l] = (Ctrl*)d;
+  }
+  {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, sizeof(int) * r2_comm::kProbeSlots, cudaHostAllocMapped) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+    c->probe_res_host = (volatile int*)h;
+    for (int i = 0; i < r2_comm::kProbeSlots; ++i) c->probe_res_host[i] = -1;
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(R2_ERR_CUDA);
+    c->probe_res_dev = (int*)d;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(R2_ERR_CUDA);
+
+  // ---- map every peer's arena (multi-registration at init)
+  c->peers_host.assign((size_t)c->nlocal * c->n, RankPtrs{});
+  if (c->sim) {
+    for (int l = 0; l < c->nlocal; ++l)
+      for (int p = 0; p < c->n; ++p) c->peers_host[l * c->n + p] = ptrs_of(c->arena[p], c->lay);
+  } else if (world == 1) {
+    c->peers_host[0] = ptrs_of(c->arena[0], c->lay);
+  } else {
+    RegXchg mine{};
+    if (cudaIpcGetMemHandle(&mine.h, c->arena[0]) != cudaSuccess) return fail(R2_ERR_CUDA);
+    mine.base = (unsigned long long)c->arena[0];
+    std::vector<RegXchg> all(world);
+    if (c->oob.allgather(c->oob.ctx, &mine, all.data(), sizeof(RegXchg))) return fail(R2_ERR_BOOTSTRAP);
+    c->peer_arena_opened.assign(world, nullptr);
+    for (int p = 0; p < world; ++p) {
+      char* b = c->arena[0];
+      if (p != rank) {
+        void* op = nullptr;
+        if (cudaIpcOpenMemHandle(&op, all[p].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+          return fail(R2_ERR_CUDA);
+        c->peer_arena_opened[p] = op;
+        b = (char*)op;
+      }
+      c->peers_host[p] = ptrs_of(b, c->lay);
+    }
+  }
+  if (cudaMalloc(&c->peers_dev, sizeof(RankPtrs) * c->peers_host.size()) != cudaSuccess) return fail(R2_ERR_CUDA);
+  if (cudaMemcpy(c->peers_dev, c->peers_host.data(), sizeof(RankPtrs) * c->peers_host.size(),
+                 cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(R2_ERR_CUDA);
+  c->regtab_host.assign((size_t)R2_MAX_REGS * c->n, 0ull);
+  if (cudaMalloc(&c->regtab_dev, sizeof(unsigned long long) * c->regtab_host.size()) != cudaSuccess)
+    return fail(R2_ERR_CUDA);
+  if (cudaMemset(c->regtab_dev, 0, sizeof(unsigned long long) * c->regtab_host.size()) != cudaSuccess)
+    return fail(R2_ERR_CUDA);
+
+  c->ep_dead.assign((size_t)c->n * c->K, 0);
+  c->link_dead.assign((size_t)c->n * c->K, 0);
+  c->handled_err.assign((size_t)c->nlocal * c->K, 0);
+  c->timeout_seq.assign(c->nlocal, 0);
+  c->epoch.assign(c->nlocal, 0);
+  c->plan_seq.assign(c->nlocal, 0);
+  c->cur_plan.assign(c->nlocal, {});
+  if (cudaStreamCreateWithFlags(&c->mon_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(R2_ERR_CUDA);
+  if (c->has_oob && c->oob.barrier(c->oob.ctx)) return fail(R2_ERR_BOOTSTRAP);
+  if (c->n > 1) c->mon = std::thread(r2_monitor_main, c);
+  *out = c;
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_register_multi(r2_comm_t c, void* dptr, size_t bytes, uint64_t* reg_out) {
+  if (!c || !dptr || !reg_out) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  if (c->sim || c->world == 1) {
+    Reg rg{(uint64_t)c->regs.size(), true, (char*)dptr, bytes, {}, {}};
+    c->regs.push_back(rg);
+    *reg_out = rg.id;
+    return R2_SUCCESS;
+  }
+  if (c->regs.size() >= R2_MAX_REGS) return R2_ERR_INVALID_ARG;
+  char* base = nullptr;
+  size_t size = 0;
+  r2_result_t e = alloc_base(dptr, &base, &size);
+  if (e != R2_SUCCESS) return e;
+  if ((char*)dptr + bytes > base + size) return R2_ERR_INVALID_ARG;
+  RegXchg mine{};
+  CK(cudaIpcGetMemHandle(&mine.h, base));
+  mine.base = (unsigned long long)base;
+  mine.dptr = (unsigned long long)dptr;
+  mine.bytes = bytes;
+  std::vector<RegXchg> all(c->world);
+  if (c->oob.allgather(c->oob.ctx, &mine, all.data(), sizeof(RegXchg))) return R2_ERR_BOOTSTRAP;
+  Reg rg;
+  rg.id = c->regs.size();
+  rg.active = true;
+  rg.dptr = (char*)dptr;
+  rg.bytes = bytes;
+  rg.peer_ptr.assign(c->world, 0);
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) {
+      rg.peer_ptr[p] = (unsigned long long)dptr;
+      continue;
+    }
+    void* op = nullptr;
+    e = open_peer(c, p, all[p], &op);
+    if (e != R2_SUCCESS) return e;
+    rg.opened.push_back(op);
+    rg.peer_ptr[p] = (unsigned long long)op + (all[p].dptr - all[p].base);
+  }
+  for (int p = 0; p < c->world; ++p) c->regtab_host[rg.id * c->n + p] = rg.peer_ptr[p];
+  CK(cudaMemcpy(c->regtab_dev + rg.id * c->n, &c->regtab_host[rg.id * c->n], sizeof(unsigned long long) * c->n,
+                cudaMemcpyHostToDevice));
+  c->regs.push_back(rg);
+  *reg_out = rg.id;
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_deregister(r2_comm_t c, uint64_t reg) {
+  if (!c || reg >= c->regs.size() || !c->regs[reg].active) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  if (c->has_oob && c->oob.barrier(c->oob.ctx)) return R2_ERR_BOOTSTRAP;
+  Reg& rg = c->regs[reg];
+  for (void* p : rg.opened) close_peer(c, p);
+  rg.opened.clear();
+  rg.active = false;
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_inject_fault(r2_comm_t c, const r2_fault_t* f) {
+  if (!c || !f) return R2_ERR_INVALID_ARG;
+  if (f->kind < R2_FAULT_LOCAL || f->kind > R2_FAULT_REPAIR) return R2_ERR_INVALID_ARG;
+  if (f->src_rank < 0 || f->src_rank >= c->n || f->channel < 0 || f->channel >= c->K) return R2_ERR_INVALID_ARG;
+  if (f->origin_channel < -1 || f->origin_channel >= c->K) return R2_ERR_INVALID_ARG;
+  if (f->kind != R2_FAULT_REPAIR && (f->step < 0 || f->chunk < 0)) return R2_ERR_INVALID_ARG;
+  if (f->at_seq <= c->seq) return R2_ERR_INVALID_ARG;   // must precede the targeted collective
+  c->faults.push_back(*f);
+  return R2_SUCCESS;
+}
+
+static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                                     void* stream) {
+  const int E = elem_bytes(dt);
+  if (c->n == 1) {
+    if (send != recv) CK(cudaMemcpyAsync(recv, send, count * E, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    c->last_stream = stream;
+    return R2_SUCCESS;
+  }
+  r2_geometry_t g;
+  r2_result_t e = r2_geometry(count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
+  if (e != R2_SUCCESS) return e;
+  if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap || g.steps * g.m > R2_BITMAP_WORDS * 32)
+    return R2_ERR_INVALID_ARG;
+  const uint32_t seq = (uint32_t)(c->seq + 1);
+
+  LaunchParams p;
+  memset(&p, 0, sizeof(p));
+  p.seq = seq;
+  p.n = c->n;
+  p.K = c->K;
+  p.W = c->W;
+  p.m = g.m;
+  p.steps = g.steps;
+  p.nlocal = c->nlocal;
+  p.first_rank = c->first_rank;
+  p.dtype = dt == R2_INT32 ? R2D_INT32 : (dt == R2_FLOAT32 ? R2D_FLOAT32 : R2D_BF16);
+  p.elem_bytes = E;
+  p.V = g.V;
+  p.inplace = send == recv;
+  p.strategy = c->cfg.strategy;
+  p.sim = c->sim;
+  p.N = g.N;
+  p.Np = g.Np;
+  p.shard = g.shard;
+  p.slice = g.slice;
+  p.chunk = g.chunk;
+  p.slot_bytes = c->lay.slot_bytes;
+  p.watchdog_ns = (unsigned long long)c->cfg.watchdog_ms * 1000000ull;
+  for (int k = 0; k < c->K; ++k) p.weights[k] = c->weights[k];
+  p.peers = c->peers_dev;
+  p.regtab = c->regtab_dev;
+
+  // recv publication (real mode) / rank buffers (sim mode)
+  for (int l = 0; l < c->nlocal; ++l) {
+    p.send[l] = (const char*)send + (size_t)l * count * E;
+    p.recv[l] = (char*)recv + (size_t)l * count * E;
+    p.ctrl[l] = c->ctrl_dev[l];
+  }
+  if (!c->sim) {
+    int found = -1;
+    for (size_t i = 0; i < c->regs.size(); ++i) {
+      const Reg& rg = c->regs[i];
+      if (rg.active && (char*)recv >= rg.dptr && (char*)recv + count * E <= rg.dptr + rg.bytes) {
+        found = (int)i;
+        break;
+      }
+    }
+    if (found < 0) return R2_ERR_NOT_REGISTERED;
+    p.recv_reg[0] = found;
+    p.recv_off[0] = (unsigned long long)((char*)recv - c->regs[found].dptr);
+  }
+
+  // faults armed for this seq; REPAIRs take effect before it (stand-in for re-probe)
+  std::vector<std::pair<int, int>> repairs;
+  for (const r2_fault_t& f : c->faults) {
+    if (f.at_seq != seq) continue;
+    if (f.kind == R2_FAULT_REPAIR) {
+      repairs.push_back({f.src_rank, f.channel});
+      continue;
+    }
+    if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
+    FaultDev& d = p.faults[p.nfaults++];
+    d.rank = f.src_rank;
+    d.channel = f.channel;
+    d.origin = f.origin_channel < 0 ? f.channel : f.origin_channel;
+    d.kind = f.kind;
+    d.t = f.step;
+    d.j = f.chunk;
+    d.b = f.byte_offset;
+    d.detect_delay_us = f.detect_delay_us;
+    d.poison = f.poison;
+  }
+  {
+    std::lock_guard<std::mutex> gl(c->mu);
+    for (auto& rc : repairs) {
+      c->ep_dead[rc.first * c->K + rc.second] = 0;
+      c->link_dead[rc.first * c->K + rc.second] = 0;
+    }
+    for (int l = 0; l < c->nlocal; ++l) {
+      const int r = c->first_rank + l;
+      uint32_t mask = 0;
+      for (int k = 0; k < c->K; ++k)
+        if (r2_conn_ok(c, r, k)) mask |= 1u << k;
+      if (!mask) return R2_ERR_NO_BACKUP;
+      p.conn_mask[l] = mask;
+    }
+  }
+  for (auto& rc : repairs)
+    for (int l = 0; l < c->nlocal; ++l) {
+      const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
+      CK(cudaMemsetAsync(me.ep_dead + rc.first * c->K + rc.second, 0, 4, (cudaStream_t)stream));
+      CK(cudaMemsetAsync(me.link_dead + rc.first * c->K + rc.second, 0, 4, (cudaStream_t)stream));
+    }
+
+  LaunchInfo li{};
+  li.seq = seq;
+  li.m = g.m;
+  li.steps = g.steps;
+  li.V = g.V;
+  li.slice = g.slice;
+  li.chunk = g.chunk;
+  for (int l = 0; l < c->nlocal; ++l) li.conn_mask[l] = p.conn_mask[l];
+  li.nfaults = p.nfaults;
+  for (int i = 0; i < p.nfaults; ++i) li.faults[i] = p.faults[i];
+  {
+    std::lock_guard<std::mutex> gl(c->mu);
+    c->launches[seq] = li;
+    while (c->launches.size() > 64) c->launches.erase(c->launches.begin());
+  }
+  c->seq = seq;
+  int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W, c->threads, stream);
+  c->last_stream = stream;
+  if (rc != 0) return R2_ERR_CUDA;
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_allreduce(r2_comm_t c, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                                    void* stream) {
+  if (!c) return R2_ERR_INVALID_ARG;
+  int ae = take_async_error(c);
+  if (ae != R2_SUCCESS) return (r2_result_t)ae;
+  if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
+  if (count == 0) return R2_SUCCESS;
+  if (!send || !recv || ((uintptr_t)send & 15) || ((uintptr_t)recv & 15)) return R2_ERR_INVALID_ARG;
+  if (count * (size_t)elem_bytes(dt) > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  return enqueue_allreduce(c, send, recv, count, dt, stream);
+}
+
+extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                                         void* stream) {
+  if (!c || !send || !recv) return R2_ERR_INVALID_ARG;
+  int ae = take_async_error(c);
+  if (ae != R2_SUCCESS) return (r2_result_t)ae;
+  if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
+  if (count == 0) return R2_SUCCESS;
+  const size_t bytes = count * (size_t)elem_bytes(dt);
+  if (bytes > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  const size_t need = c->cfg.max_bytes * c->nlocal;
+  if (!c->host_stage) {
+    CK(cudaMalloc(&c->host_stage, need));
+    c->host_stage_bytes = need;
+    r2_result_t e = r2_register_multi(c, c->host_stage, need, &c->host_stage_reg);
+    if (e != R2_SUCCESS) return e;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int l = 0; l < c->nlocal; ++l)
+    CK(cudaMemcpyAsync(c->host_stage + l * bytes, (const char*)send + l * bytes, bytes, cudaMemcpyHostToDevice, s));
+  r2_result_t e = enqueue_allreduce(c, c->host_stage, c->host_stage, count, dt, stream);
+  if (e != R2_SUCCESS) return e;
+  for (int l = 0; l < c->nlocal; ++l)
+    CK(cudaMemcpyAsync((char*)recv + l * bytes, c->host_stage + l * bytes, bytes, cudaMemcpyDeviceToHost, s));
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_sync(r2_comm_t c) {
+  if (!c) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  if (cudaStreamSynchronize((cudaStream_t)c->last_stream) != cudaSuccess) return R2_ERR_CUDA;
+  // give the monitor a moment to record a NO_BACKUP / TIMEOUT for the last seq
+  for (int i = 0; i < 50; ++i) {
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      if (c->unreported_error != R2_SUCCESS) break;
+      bool busy = !c->replans.empty();
+      if (!busy) break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  return (r2_result_t)take_async_error(c);
+}
+
+extern "C" r2_result_t r2_probe(r2_comm_t c, int rank_local, int peer, int channel, r2_verdict_t* out) {
+  if (!c || !out || c->n < 2) return R2_ERR_INVALID_ARG;
+  if (rank_local < 0 || rank_local >= c->nlocal || peer < 0 || peer >= c->n || channel < 0 || channel >= c->K)
+    return R2_ERR_INVALID_ARG;
+  const int a = c->first_rank + rank_local;
+  if (peer == a) return R2_ERR_INVALID_ARG;
+  uint32_t id;
+  {
+    std::lock_guard<std::mutex> g(c->pmu);
+    id = ((uint32_t)a << 24) | (++c->round_counter & 0xFFFFFF);
+    c->probe_requests.push_back({rank_local, {peer, channel}});
+    c->probe_request_ids.push_back(id);
+  }
+  uint64_t t0 = r2_now_ns();
+  for (;;) {
+    {
+      std::lock_guard<std::mutex> g(c->pmu);
+      auto it = c->finished_rounds.find(id);
+      if (it != c->finished_rounds.end()) {
+        *out = it->second;
+        c->finished_rounds.erase(it);
+        return R2_SUCCESS;
+      }
+    }
+    if (r2_now_ns() - t0 > 10ull * 1000000000ull) return R2_ERR_TIMEOUT;
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
+  if (!c || !out) return R2_ERR_INVALID_ARG;
+  memset(out, 0, sizeof(*out));
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    out->seq = c->seq;
+    out->last_error = c->last_error;
+    out->last_error_seq = c->last_error_seq;
+    out->n_events = (int)c->events.size();
+    out->world = c->n;
+    out->nlocal = c->nlocal;
+    out->nchannels = c->K;
+    for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
+      for (int k = 0; k < c->K; ++k) {
+        if (c->ep_dead[r * c->K + k]) out->dead_endpoints[r] |= 1u << k;
+        if (c->link_dead[r * c->K + k]) out->dead_links[r] |= 1u << k;
+      }
+  }
+  if (c->n > 1) {
+    if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<MiscDev> m(c->nlocal);
+    for (int l = 0; l < c->nlocal; ++l) {
+      const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
+      CK(cudaMemcpyAsync(&m[l], me.misc, sizeof(MiscDev), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+    for (int l = 0; l < c->nlocal; ++l)
+      for (int k = 0; k < c->K; ++k) out->bytes[l][k] = m[l].bytes[k];
+  }
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_get_event(r2_comm_t c, int idx, r2_event_t* out) {
+  if (!c || !out) return R2_ERR_INVALID_ARG;
+  std::lock_guard<std::mutex> g(c->mu);
+  if (idx < 0 || idx >= (int)c->events.size()) return R2_ERR_INVALID_ARG;
+  *out = c->events[idx];
+  return R2_SUCCESS;
+}
+
+extern "C" r2_result_t r2_finalize(r2_comm_t c) {
+  if (!c) return R2_ERR_INVALID_ARG;
+  cudaSetDevice(c->dev);
+  cudaDeviceSynchronize();
+  if (c->has_oob) c->oob.barrier(c->oob.ctx);
+  c->stop.store(true);
+  if (c->mon.joinable()) c->mon.join();
+  for (auto& rg : c->regs)
+    for (void* p : rg.opened) close_peer(c, p);
+  for (void* p : c->peer_arena_opened)
+    if (p) cudaIpcCloseMemHandle(p);
+  if (c->has_oob) c->oob.barrier(c->oob.ctx);
+  for (char* a : c->arena) cudaFree(a);
+  for (Ctrl* h : c->ctrl_host) cudaFreeHost(h);
+  if (c->probe_res_host) cudaFreeHost((void*)c->probe_res_host);
+  if (c->peers_dev) cudaFree(c->peers_dev);
+  if (c->regtab_dev) cudaFree(c->regtab_dev);
+  if (c->host_stage) cudaFree(c->host_stage);
+  if (c->mon_stream) cudaStreamDestroy(c->mon_stream);
+  delete c;
+  return R2_SUCCESS;
+}

@@ -1,0 +1,122 @@
+// r2_hostlogic.cpp -- pure host logic of the R²CCL control plane.
+//   r2_triangulate      decision table C-10
+//   r2_balance_shares   R²CCL-Balance integer shares (C-15)
+//   r2_failover_chain   ordered backups (C-2)
+//   r2_rollback         sender resume / receiver floor
+//   r2_geometry         shards / slices / chunks (SURVEY §8 header, C-3)
+#include <string.h>
+
+#include "r2_comm.h"
+
+extern "C" int r2_triangulate(const int o[4], int has_aux) {
+  const int S = R2_PROBE_SUCCESS, L = R2_PROBE_LOCAL_ERROR, T = R2_PROBE_TIMEOUT;
+  const int ab = o[0], ba = o[1];
+  if (ab == L && ba == L) return R2_V_TWO_LOCAL;
+  if (ab == L) return R2_V_LOCAL_ENDPOINT;
+  if (ba == L) return R2_V_REMOTE_ENDPOINT;
+  if (ab == S && ba == S) return R2_V_NONE;
+  if ((ab == T && ba == S) || (ab == S && ba == T)) return R2_V_LINK;
+  // both endpoints timed out
+  if (!has_aux) return R2_V_INCONCLUSIVE;
+  const int xa = o[2], xb = o[3];
+  if (xa == L || xb == L) return R2_V_INCONCLUSIVE;
+  if (xa == S && xb == S) return R2_V_LINK;
+  if (xa == T && xb == S) return R2_V_ENDPOINT_UNREACHABLE_A;
+  if (xa == S && xb == T) return R2_V_ENDPOINT_UNREACHABLE_B;
+  return R2_V_DUAL_ENDPOINT;
+}
+
+extern "C" r2_result_t r2_balance_shares(uint64_t R, const int* w, uint32_t mask, int K, uint64_t* out) {
+  if (!w || !out || K <= 0 || K > R2_MAX_CHANNELS) return R2_ERR_INVALID_ARG;
+  uint64_t tot = 0;
+  int top = -1;
+  for (int k = 0; k < K; ++k) {
+    out[k] = 0;
+    if ((mask >> k & 1u) && w[k] > 0) {
+      tot += (uint64_t)w[k];
+      if (top < 0 || w[k] > w[top]) top = k;
+    }
+  }
+  if (tot == 0) return R2_ERR_NO_BACKUP;
+  uint64_t sum = 0;
+  for (int k = 0; k < K; ++k)
+    if ((mask >> k & 1u) && w[k] > 0) {
+      out[k] = (uint64_t)((unsigned __int128)R * (uint64_t)w[k] / tot);
+      sum += out[k];
+    }
+  out[top] += R - sum;
+  return R2_SUCCESS;
+}
+
+extern "C" void r2_failover_chain(int c, int K, int* out) {
+  for (int d = 1; d < K; ++d) out[d - 1] = (c + d) % K;
+}
+
+extern "C" void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor) {
+  int r = npos;
+  for (int q = 0; q < npos; ++q)
+    if (!completed[q]) {
+      r = q;
+      break;
+    }
+  if (resume) *resume = r;
+  if (floor) *floor = r - 1;
+}
+
+static int elem_bytes_of(r2_dtype_t dt) { return dt == R2_BFLOAT16 ? 2 : 4; }
+
+extern "C" r2_result_t r2_geometry(uint64_t count, r2_dtype_t dt, int n, int K, int W, size_t chunk_bytes,
+                                   r2_geometry_t* g) {
+  if (!g || n < 1 || K < 1 || W < 1 || chunk_bytes < 16 || chunk_bytes % 16) return R2_ERR_INVALID_ARG;
+  if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
+  const int E = elem_bytes_of(dt), V = 16 / E;
+  const uint64_t q = (uint64_t)n * K * V;
+  const uint64_t Nmin = count ? count : 1;
+  const uint64_t Np_cap = (Nmin + q - 1) / q * q;
+  const uint64_t slice = Np_cap / ((uint64_t)n * K);
+  const uint64_t slice_bytes = slice * E;
+  uint64_t per_worker = ((slice_bytes + W - 1) / W + 15) / 16 * 16;
+  uint64_t chunkb = chunk_bytes < per_worker ? chunk_bytes : per_worker;
+  if (chunkb < 16) chunkb = 16;
+  memset(g, 0, sizeof(*g));
+  g->N = count;
+  g->Np = count ? Np_cap : 0;
+  g->shard = g->Np / n;
+  g->slice = count ? slice : 0;
+  g->chunk = chunkb / E;
+  g->n = n;
+  g->K = K;
+  g->W = W;
+  g->V = V;
+  g->m = count ? (int)((g->slice + g->chunk - 1) / g->chunk) : 0;
+  g->steps = 2 * n - 2;
+  return R2_SUCCESS;
+}
+
+int r2_first_healthy_in_chain(int origin, uint32_t mask, int K) {
+  for (int d = 1; d < K; ++d) {
+    int c = (origin + d) % K;
+    if (mask >> c & 1u) return c;
+  }
+  return -1;
+}
+
+bool r2_conn_ok(const r2_comm* comm, int r, int c) {
+  const int n = comm->n, K = comm->K;
+  const int r1 = (r + 1) % n;
+  return !comm->ep_dead[r * K + c] && !comm->ep_dead[r1 * K + c] && !comm->link_dead[r * K + c];
+}
+
+extern "C" const char* r2_strerror(r2_result_t r) {
+  switch (r) {
+    case R2_SUCCESS: return "success";
+    case R2_ERR_INVALID_ARG: return "invalid argument";
+    case R2_ERR_CUDA: return "CUDA error";
+    case R2_ERR_BOOTSTRAP: return "out-of-band bootstrap error";
+    case R2_ERR_NOT_REGISTERED: return "recv buffer not registered";
+    case R2_ERR_NO_BACKUP: return "failover chain exhausted (no healthy channel)";
+    case R2_ERR_TIMEOUT: return "watchdog timeout";
+    case R2_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown error";
+}

@@ -1,0 +1,139 @@
+// r2_internal.h -- structures shared by the host control code (r2_comm.cpp,
+// r2_monitor.cpp) and the sm_100a kernels (r2_kernels.cu).
+//
+// Memory layout per rank (one cudaMalloc "arena", IPC-exported to every peer,
+// P:27 "register each GPU buffer with all NICs" -> here: mapped into every
+// peer process once, at init):
+//
+//   scratch   [2 parities][n-1 RS slots][slot_bytes]   peer-written partials
+//   flags     u32 [2n-2 steps][K][m_cap]               completion words (=seq)
+//   counters  u64 [2n-2][K][m_cap]                     Balance part counters
+//   ep_dead   u32 [n][K]   link_dead u32 [n][K]        emulated fabric state
+//   alert     u32                                      seq of last fault firing
+//   mailbox   u32 [n][K]                               probe-flag targets
+//   desc      u64 [2][4]                               recv publication
+//   misc      delivered/exited/copy counters, bytes[K]
+//   stage     [slot_bytes]                             in-place own shard y
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#define R2_MAXL 16
+#define R2_MAXK 16
+#define R2_MAXW 16
+#define R2_MAXF 8
+#define R2_MAX_REGS 64
+#define R2_BITMAP_WORDS 64            // 2048 stream positions per origin
+#define R2_MAX_CTAS_PER_RANK (R2_MAXK * R2_MAXW)
+
+enum { R2D_INT32 = 0, R2D_FLOAT32 = 1, R2D_BF16 = 2 };
+
+// CTA states written to the host-mapped control block
+enum { CTA_IDLE = 0, CTA_RUNNING = 1, CTA_DRAINING = 2, CTA_STOPPED = 3, CTA_EXITED = 4 };
+// stop causes
+enum { STOP_NONE = 0, STOP_FAULT_FIRED = 1, STOP_FAULT_TABLE = 2, STOP_DEATH = 3, STOP_HOST = 4,
+       STOP_ABORT = 5, STOP_TIMEOUT = 6 };
+// plan entry modes
+enum { PLAN_NONE = 0, PLAN_HOT = 1, PLAN_BAL = 2 };
+
+struct MiscDev {
+  unsigned int delivered;     // items whose flag this rank set in this collective
+  unsigned int exited;        // CTAs that left the kernel
+  unsigned int copy_next;     // in-place staging copy work counter
+  unsigned int abort_seq;     // == seq: a CTA of this rank timed out, all stop
+  unsigned long long bytes[R2_MAXK];  // cumulative bytes pushed per carrier channel
+  unsigned long long first_retx_ns;   // min over adopters (debug)
+};
+
+struct RankPtrs {            // one rank's arena as seen from some process
+  char* scratch;
+  unsigned int* flags;
+  unsigned long long* counters;
+  unsigned int* ep_dead;
+  unsigned int* link_dead;
+  unsigned int* alert;
+  unsigned int* mailbox;
+  unsigned long long* desc;
+  MiscDev* misc;
+  char* stage;
+};
+
+struct ArenaLayout {
+  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, total;
+  size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
+  int m_cap;
+};
+
+// ------------------------------------------------------------------ control
+struct PlanEntry {           // dynamic re-placement of one origin channel
+  unsigned int origin, mode, assignee, mask;
+  unsigned int bitmap[R2_BITMAP_WORDS];
+};
+
+struct CtaRec {
+  volatile unsigned int seq, state, cause, ack_epoch;
+  volatile unsigned int adopt_tag, stop_t, stop_o, stop_j;   // adopt_tag = seq<<8 | epoch
+  volatile unsigned long long t_stop, t_first_adopt;
+};
+
+struct ErrRec {              // one per channel: the stop that needs handling
+  volatile unsigned int seq, cause, origin, q;
+  volatile unsigned long long t_fire;
+};
+
+struct Ctrl {                // host-mapped, one per local rank
+  volatile unsigned int plan_seq, epoch, freeze, abort;
+  volatile unsigned int stop_mask, nentries, pad0, pad1;
+  PlanEntry entries[R2_MAXK];
+  ErrRec err[R2_MAXK];
+  CtaRec cta[R2_MAX_CTAS_PER_RANK];
+};
+
+// ------------------------------------------------------------------ launch
+struct FaultDev {
+  unsigned int rank, channel, origin, kind;
+  unsigned int t, j, detect_delay_us, poison;
+  unsigned long long b;
+};
+
+struct LaunchParams {
+  unsigned int seq;
+  int n, K, W, m, steps, nlocal, first_rank;
+  int dtype, elem_bytes, V, inplace, strategy, sim;
+  unsigned long long N, Np, shard, slice, chunk;   // elements
+  size_t slot_bytes;
+  unsigned long long watchdog_ns;
+  int nfaults;
+  FaultDev faults[R2_MAXF];
+  unsigned int weights[R2_MAXK];
+  unsigned int conn_mask[R2_MAXL];       // static plan: usable outgoing channels
+  const char* send[R2_MAXL];
+  char* recv[R2_MAXL];
+  int recv_reg[R2_MAXL];                 // registration id of recv (real mode)
+  unsigned long long recv_off[R2_MAXL];  // offset of recv inside the registration
+  const RankPtrs* peers;                 // [nlocal][n] device array
+  const unsigned long long* regtab;      // [R2_MAX_REGS][n] peer registered bases
+  Ctrl* ctrl[R2_MAXL];                   // device aliases of host-mapped blocks
+};
+
+struct ProbeParams {
+  unsigned int* target_mailbox;          // &mailbox[prober][channel] in target arena
+  const unsigned int* ep_dead;           // prober's replicated fabric state
+  const unsigned int* link_dead;
+  int prober, target, channel, n, K;
+  unsigned int token;
+  unsigned long long timeout_ns;
+  volatile int* result;                  // host-mapped: r2_probe_outcome_t
+};
+
+// host-side launchers implemented in r2_kernels.cu
+#ifdef __cplusplus
+extern "C++" {
+#endif
+int r2_launch_allreduce(const LaunchParams& p, int nctas, int threads, void* stream);
+int r2_launch_probe(const ProbeParams& p, void* stream);
+int r2_kernel_smem_bytes();
+int r2_max_coop_ctas(int threads);
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,836 @@
+// r2_kernels.cu -- sm_100a kernels of the R²CCL hot path (arXiv 2512.25059).
+//
+// r2_allreduce_kernel: one persistent (cooperative) launch per collective.
+// CTA (l, c, w) serves local rank l, channel c (a CTA group = the bandwidth
+// unit standing in for a NIC, SURVEY reading C-1) and chunk lane w (chunks
+// j = w, w+W, ...).  It walks its work list in global (step, origin, chunk)
+// order -- own items and adopted items merged -- which keeps adoption
+// deadlock-free (SURVEY §7 hard part 3):
+//
+//   RS  step t <= n-2 : x_r[shard] (+ scratch partial) -> peer scratch  (Fig. 3)
+//   t = n-1 (fused)   : partial + x_r[own shard] -> own recv + peer recv
+//   AG  step t >= n   : own recv[shard] -> peer recv
+//
+// Every item moves 16-byte vectors straight into the peer's memory over
+// NVLink (CUDA-IPC mapping), then one thread issues fence.acq_rel.sys and
+// stores the completion word (= seq) into the RECEIVER's flag array (the
+// RDMA work-completion analogue; reading C-4).
+//
+// Fault path: an armed fault fires at (rank, channel, step,
+// origin, chunk): the first b bytes reach the peer, no flag is written, the
+// emulated fabric state is marked dead on every rank, an error record is
+// posted to the host-mapped control block and the channel stops.  The host
+// monitor (r2_monitor.cpp) notifies peers out of band, triangulates with
+// r2_probe_kernel, rolls back from the flags and publishes a re-placement
+// plan; surviving CTAs adopt the residual chunks (HotRepair: the first
+// healthy channel of the failover chain; Balance: a weight-proportional part
+// of every residual chunk on every healthy channel) and deliver them to the
+// canonical addresses with the canonical flags.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "r2_internal.h"
+
+namespace {
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ unsigned int ld_acquire_sys(const volatile unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_relaxed_sys(const volatile unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys64(const volatile unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(volatile unsigned int* p, unsigned int v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint4 ld_cg(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ------------------------------------------------------------------ one hop
+// int32: two's-complement wrap (C-9); fp32: IEEE RN add (no FMA, no FTZ);
+// bf16: fp32 add then cvt.rn (RNE) back to bf16 at every hop (C-8).
+__device__ __forceinline__ unsigned int add_bf16x2(unsigned int a, unsigned int b) {
+  float a_lo = __uint_as_float(a << 16), a_hi = __uint_as_float(a & 0xFFFF0000u);
+  float b_lo = __uint_as_float(b << 16), b_hi = __uint_as_float(b & 0xFFFF0000u);
+  float s_lo = __fadd_rn(a_lo, b_lo), s_hi = __fadd_rn(a_hi, b_hi);
+  unsigned int d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(s_hi), "f"(s_lo));
+  return d;
+}
+template <int DT>
+__device__ __forceinline__ unsigned int add32(unsigned int a, unsigned int b) {
+  if (DT == R2D_INT32) return a + b;
+  if (DT == R2D_FLOAT32) return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(b)));
+  return add_bf16x2(a, b);
+}
+template <int DT>
+__device__ __forceinline__ uint4 vadd(uint4 a, uint4 b) {
+  return make_uint4(add32<DT>(a.x, b.x), add32<DT>(a.y, b.y), add32<DT>(a.z, b.z), add32<DT>(a.w, b.w));
+}
+
+// masked (tail) user-buffer access: lanes >= valid read as 0 / are not written
+__device__ __forceinline__ uint4 ld_user(const char* p, int valid, int E) {
+  if (valid >= 16 / E) return ld_cg(p);
+  unsigned int w[4] = {0, 0, 0, 0};
+  if (valid > 0) {
+    if (E == 4) {
+      for (int i = 0; i < valid; ++i) w[i] = ((const volatile unsigned int*)p)[i];
+    } else {
+      for (int i = 0; i < valid; ++i) {
+        unsigned int h = ((const volatile unsigned short*)p)[i];
+        w[i >> 1] |= h << (16 * (i & 1));
+      }
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ void st_user(char* p, uint4 v, int valid, int E) {
+  if (valid >= 16 / E) { st_v4(p, v); return; }
+  unsigned int w[4] = {v.x, v.y, v.z, v.w};
+  if (E == 4) {
+    for (int i = 0; i < valid; ++i) ((volatile unsigned int*)p)[i] = w[i];
+  } else {
+    for (int i = 0; i < valid; ++i) ((volatile unsigned short*)p)[i] = (unsigned short)(w[i >> 1] >> (16 * (i & 1)));
+  }
+}
+
+enum { MODE_RS = 0, MODE_FUSED = 1, MODE_AG = 2 };
+enum { ST_OK = 0, ST_STOP = 1, ST_REPLAN = 2, ST_ABORT = 3, ST_TIMEOUT = 4 };
+
+struct Shared {
+  int decision;
+  int cause;
+  int fire;
+  unsigned int fire_nvec;
+  int poison;
+  unsigned int seen_epoch;
+  int dynamic;
+  int freeze;
+  int nent;
+  int alerted;
+  int flag;
+  unsigned int piece;
+  char* recv_next;
+  unsigned long long first_adopt;
+  unsigned long long wait_t0;
+  PlanEntry ent[R2_MAXK];
+};
+
+struct Cta {
+  const LaunchParams* p;
+  int l, r, r1, c, w, tid, nthr, cta_in_rank;
+  unsigned int seq;
+  int par;
+  bool fault_channel;
+  bool own_alive;
+  RankPtrs me, nx;
+  Ctrl* ctrl;
+  unsigned int total_items;
+  unsigned long long own_next_key;
+};
+
+__device__ __forceinline__ unsigned long long keyof(int t, int o, int j) {
+  return ((unsigned long long)t << 40) | ((unsigned long long)o << 32) | (unsigned int)j;
+}
+__device__ __forceinline__ size_t fidx(const LaunchParams& p, int t, int o, int j) {
+  return ((size_t)t * p.K + o) * (size_t)p.m + j;
+}
+__device__ __forceinline__ char* scratch_slot(const RankPtrs& rp, const LaunchParams& p, int par, int slot) {
+  return rp.scratch + ((size_t)par * (p.n - 1) + slot) * p.slot_bytes;
+}
+
+// Balance part of channel c in an item of V vectors (reading C-15):
+// floor(V*w/Σw) per healthy channel in id order, remainder to the top weight
+// (ties -> lowest id).  Same rule as r2_balance_shares on the host.
+__device__ void bal_part(unsigned int V, unsigned int mask, const unsigned int* w, int K, int c,
+                         unsigned int& lo, unsigned int& hi, unsigned int& parts) {
+  unsigned long long tot = 0;
+  int top = -1;
+  for (int k = 0; k < K; ++k)
+    if (mask >> k & 1u) {
+      tot += w[k];
+      if (top < 0 || w[k] > w[top]) top = k;
+    }
+  lo = hi = 0;
+  parts = 0;
+  if (tot == 0) return;
+  unsigned long long sum = 0;
+  for (int k = 0; k < K; ++k)
+    if (mask >> k & 1u) sum += (unsigned long long)V * w[k] / tot;
+  unsigned int rem = V - (unsigned int)sum;
+  unsigned int off = 0;
+  for (int k = 0; k < K; ++k) {
+    if (!(mask >> k & 1u)) continue;
+    unsigned int sh = (unsigned int)((unsigned long long)V * w[k] / tot) + (k == top ? rem : 0u);
+    if (sh) parts++;
+    if (k == c) {
+      lo = off;
+      hi = off + sh;
+    }
+    off += sh;
+  }
+}
+
+// --------------------------------------------------------------- data mover
+// Vectors [0, nvec) of one item part; e0 = global element of vector 0.
+//   src    : x (RS/fused) or own recv (AG), user memory (masked by N)
+//   s_in   : scratch partial (RS t>0, fused) or null
+//   d_rem  : peer scratch (RS, full vectors) or peer recv (fused/AG, masked)
+//   d_loc  : fused only: own stage (in-place, full) or own recv (masked)
+template <int DT>
+__device__ void move(const Cta& k, const char* src, const char* s_in, char* d_rem, bool rem_user, char* d_loc,
+                     bool loc_user, unsigned long long e0, unsigned int nvec) {
+  const LaunchParams& p = *k.p;
+  const int E = p.elem_bytes, V = p.V;
+  const unsigned int stride = k.nthr;
+  if (e0 + (unsigned long long)nvec * V <= p.N) {
+    // fast path: every vector is inside the user buffer
+    unsigned int v = k.tid;
+    for (; v + 3 * stride < nvec; v += 4 * stride) {
+      uint4 a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = ld_cg(src + (size_t)(v + u * stride) * 16);
+      if (s_in) {
+        uint4 b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = ld_cg(s_in + (size_t)(v + u * stride) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = vadd<DT>(b[u], a[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) st_v4(d_rem + (size_t)(v + u * stride) * 16, a[u]);
+      if (d_loc) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) st_v4(d_loc + (size_t)(v + u * stride) * 16, a[u]);
+      }
+    }
+    for (; v < nvec; v += stride) {
+      uint4 a = ld_cg(src + (size_t)v * 16);
+      if (s_in) a = vadd<DT>(ld_cg(s_in + (size_t)v * 16), a);
+      st_v4(d_rem + (size_t)v * 16, a);
+      if (d_loc) st_v4(d_loc + (size_t)v * 16, a);
+    }
+    return;
+  }
+  // tail path: vectors straddling / beyond N
+  for (unsigned int v = k.tid; v < nvec; v += stride) {
+    long long ev = (long long)(e0 + (unsigned long long)v * V);
+    long long left = (long long)p.N - ev;
+    int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+    uint4 a = ld_user(src + (size_t)v * 16, valid, E);
+    if (s_in) a = vadd<DT>(ld_cg(s_in + (size_t)v * 16), a);
+    if (rem_user) st_user(d_rem + (size_t)v * 16, a, valid, E);
+    else st_v4(d_rem + (size_t)v * 16, a);
+    if (d_loc) {
+      if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E);
+      else st_v4(d_loc + (size_t)v * 16, a);
+    }
+  }
+}
+
+// ------------------------------------------------------------ control polls
+// Thread 0 only.  Looks at the device-local abort word, the alert word
+// (set on every rank by a firing fault) and, once alerted, the host-mapped
+// control block (abort, stop mask, plan epoch).
+__device__ int poll_control(const Cta& k, Shared& sh) {
+  if (ld_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq) == k.seq) return ST_ABORT;
+  if (!sh.alerted) {
+    if (ld_relaxed_sys(k.me.alert) == k.seq) sh.alerted = 1;
+  }
+  if (sh.alerted) {
+    Ctrl* C = k.ctrl;
+    if (ld_relaxed_sys(&C->plan_seq) == k.seq) {
+      if (ld_relaxed_sys(&C->abort)) {
+        sh.cause = STOP_ABORT;
+        return ST_ABORT;
+      }
+      if (ld_relaxed_sys(&C->stop_mask) >> k.c & 1u) {
+        sh.cause = STOP_HOST;
+        return ST_STOP;
+      }
+      if (ld_acquire_sys(&C->epoch) != sh.seen_epoch) return ST_REPLAN;
+    }
+  }
+  return ST_OK;
+}
+
+__device__ __forceinline__ bool conn_phys_dead(const Cta& k) {
+  if (k.fault_channel) return false;   // deterministic stop rule applies instead
+  const LaunchParams& p = *k.p;
+  return ld_relaxed_sys(k.me.ep_dead + k.r * p.K + k.c) | ld_relaxed_sys(k.me.ep_dead + k.r1 * p.K + k.c) |
+         ld_relaxed_sys(k.me.link_dead + k.r * p.K + k.c);
+}
+
+// watchdog: returns true when expired
+__device__ __forceinline__ bool watchdog(const Cta& k, Shared& sh) {
+  unsigned long long now = gtimer();
+  if (sh.wait_t0 == 0) { sh.wait_t0 = now; return false; }
+  return now - sh.wait_t0 > k.p->watchdog_ns;
+}
+
+// thread 0: wait until *f >= seq with periodic control polls
+__device__ int wait_word(const Cta& k, Shared& sh, const volatile unsigned int* f, bool check_death) {
+  sh.wait_t0 = 0;
+  unsigned int it = 0;
+  while ((int)(ld_acquire_sys(f) - k.seq) < 0) {
+    if ((++it & 31u) == 0) {
+      int s = poll_control(k, sh);
+      if (s != ST_OK) return s;
+      if (check_death && conn_phys_dead(k)) {
+        sh.cause = STOP_DEATH;
+        return ST_STOP;
+      }
+      if (watchdog(k, sh)) {
+        sh.cause = STOP_TIMEOUT;
+        return ST_TIMEOUT;
+      }
+    }
+  }
+  return ST_OK;
+}
+
+// thread 0: peer's recv pointer for this seq (real mode: published descriptor)
+__device__ int resolve_recv_next(const Cta& k, Shared& sh) {
+  const LaunchParams& p = *k.p;
+  if (sh.recv_next) return ST_OK;
+  if (p.sim) {
+    sh.recv_next = p.recv[k.r1 - p.first_rank];
+    return ST_OK;
+  }
+  const volatile unsigned long long* d = k.nx.desc + k.par * 4;
+  sh.wait_t0 = 0;
+  unsigned int it = 0;
+  while ((unsigned int)ld_relaxed_sys64(d) != k.seq) {
+    if ((++it & 31u) == 0) {
+      int s = poll_control(k, sh);
+      if (s != ST_OK) return s;
+      if (watchdog(k, sh)) {
+        sh.cause = STOP_TIMEOUT;
+        return ST_TIMEOUT;
+      }
+    }
+  }
+  fence_sys();
+  unsigned long long reg = ld_relaxed_sys64(d + 1), off = ld_relaxed_sys64(d + 2);
+  sh.recv_next = (char*)(p.regtab[reg * p.n + k.r1] + off);
+  return ST_OK;
+}
+
+// thread 0: fire an armed fault ("Failures may occur mid-chunk").
+__device__ void fire_fault(const Cta& k, const FaultDev& f, int t, int o, int j) {
+  const LaunchParams& p = *k.p;
+  unsigned long long t_fire = gtimer();
+  fence_sys();
+  for (int q = 0; q < p.n; ++q) {
+    const RankPtrs& rp = p.peers[k.l * p.n + q];
+    if (f.kind == 2) st_relaxed_sys(rp.link_dead + k.r * p.K + k.c, 1u);        // LINK
+    else if (f.kind == 0) st_relaxed_sys(rp.ep_dead + k.r * p.K + k.c, 1u);     // LOCAL
+    else st_relaxed_sys(rp.ep_dead + k.r1 * p.K + k.c, 1u);                     // REMOTE
+  }
+  fence_sys();
+  for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peers[k.l * p.n + q].alert, k.seq);
+  fence_sys();
+  // the sender's transport error surfaces after detect_delay_us (reading C-17)
+  unsigned long long delay = (unsigned long long)f.detect_delay_us * 1000ull;
+  while (gtimer() - t_fire < delay) {
+  }
+  ErrRec& e = k.ctrl->err[k.c];
+  e.cause = STOP_FAULT_FIRED;
+  e.origin = (unsigned int)o;
+  e.q = (unsigned int)(t * p.m + j);
+  e.t_fire = t_fire;
+  __threadfence_system();
+  e.seq = k.seq;
+  __threadfence_system();
+}
+
+// thread 0: item delivered -> release + completion word (+ Balance counter)
+__device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, unsigned int parts,
+                              unsigned int epoch, bool own, unsigned int nbytes) {
+  const LaunchParams& p = *k.p;
+  fence_sys();
+  bool last = true;
+  const size_t fi = fidx(p, t, o, j);
+  if (parts > 1) {
+    unsigned long long* ctr = k.me.counters + fi;
+    const unsigned long long tag = (unsigned long long)(((k.seq & 0xFFFFFFu) << 8) | (epoch & 0xFFu)) << 32;
+    unsigned long long old = *(volatile unsigned long long*)ctr, prev, nw;
+    unsigned int cnt;
+    for (;;) {
+      cnt = ((old & 0xFFFFFFFF00000000ull) == tag) ? (unsigned int)(old & 0xFFFFFFFFu) + 1u : 1u;
+      nw = tag | cnt;
+      prev = atomicCAS(ctr, old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+    last = cnt == parts;
+    if (last) fence_sys();
+  }
+  if (last) {
+    st_relaxed_sys(k.nx.flags + fi, k.seq);
+    atomicAdd(&k.me.misc->delivered, 1u);
+  }
+  atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nbytes);
+  if (!own && sh.first_adopt == 0) {
+    // failover latency endpoint: first retransmitted chunk's flag
+    sh.first_adopt = gtimer();
+    CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
+    rec.t_first_adopt = sh.first_adopt;
+    __threadfence_system();
+    rec.adopt_tag = (k.seq << 8) | (epoch & 0xFFu);
+  }
+}
+
+// ------------------------------------------------------------------ an item
+template <int DT>
+__device__ int do_item(Cta& k, Shared& sh, int t, int o, int j, unsigned int lo, unsigned int hi,
+                       unsigned int parts, unsigned int epoch, bool own) {
+  const LaunchParams& p = *k.p;
+  const int n = p.n;
+  if (k.tid == 0) {
+    int st = ST_OK;
+    sh.fire = 0;
+    const unsigned long long key = keyof(t, o, j);
+    // deterministic fault rule: channel dead from the armed key on (C-6)
+    for (int i = 0; i < p.nfaults && st == ST_OK; ++i) {
+      const FaultDev& f = p.faults[i];
+      if ((int)f.rank != k.r || (int)f.channel != k.c || f.kind > 2) continue;
+      unsigned long long kf = keyof(f.t, f.origin, f.j);
+      if (key > kf) {
+        st = ST_STOP;
+        sh.cause = STOP_FAULT_TABLE;
+      } else if (key == kf) {
+        sh.fire = 1 + i;
+        unsigned long long bv = f.b / 16;
+        sh.fire_nvec = (unsigned int)(bv < (hi - lo) ? bv : (hi - lo));
+        sh.poison = f.poison;
+      }
+    }
+    if (st == ST_OK) st = poll_control(k, sh);
+    if (st == ST_OK && conn_phys_dead(k)) {
+      st = ST_STOP;
+      sh.cause = STOP_DEATH;
+    }
+    if (st == ST_OK && t > 0) st = wait_word(k, sh, k.me.flags + fidx(p, t - 1, o, j), true);
+    if (st == ST_OK && t >= n - 1) st = resolve_recv_next(k, sh);
+    sh.decision = st;
+  }
+  __syncthreads();
+  // copy the broadcast into registers: thread 0 may rewrite `sh` as soon as
+  // everybody has passed the next barrier
+  const int st = sh.decision;
+  const int fire = sh.fire;
+  const unsigned int fire_nvec = sh.fire_nvec;
+  const int poison = sh.poison;
+  char* const recv_next = sh.recv_next;
+  if (st != ST_OK) {
+    __syncthreads();
+    return st;
+  }
+
+  // addresses
+  const int E = p.elem_bytes, V = p.V;
+  const int s = (t <= n - 2) ? ((k.r - 1 - t) % n + n) % n : ((k.r - (t - n + 1)) % n + n) % n;
+  const unsigned long long off = (unsigned long long)o * p.slice + (unsigned long long)j * p.chunk +
+                                 (unsigned long long)lo * V;   // shard-local element
+  const unsigned long long e0 = (unsigned long long)s * p.shard + off;
+  const unsigned int nvec = fire ? fire_nvec : (hi - lo);
+  if (t <= n - 2) {
+    const char* s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
+    move<DT>(k, p.send[k.l] + e0 * E, s_in, scratch_slot(k.nx, p, k.par, t) + off * E, false, nullptr,
+             false, e0, nvec);
+  } else if (t == n - 1) {
+    char* d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
+    move<DT>(k, p.send[k.l] + e0 * E, scratch_slot(k.me, p, k.par, n - 2) + off * E, recv_next + e0 * E,
+             true, d_loc, !p.inplace, e0, nvec);
+  } else {
+    move<DT>(k, p.recv[k.l] + e0 * E, nullptr, recv_next + e0 * E, true, nullptr, false, e0, nvec);
+  }
+  if (fire && poison) {
+    // poison the rest of the faulted part at the peer (reading C-6)
+    char* dst = (t <= n - 2) ? scratch_slot(k.nx, p, k.par, t) + off * E : recv_next + e0 * E;
+    const unsigned int total = hi - lo;
+    for (unsigned int v = nvec + k.tid; v < total; v += k.nthr) {
+      long long ev = (long long)(e0 + (unsigned long long)v * V);
+      long long left = (long long)p.N - ev;
+      int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+      if (t <= n - 2) st_v4(dst + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+      else st_user(dst + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, E);
+    }
+  }
+  __syncthreads();
+  if (k.tid == 0) {
+    if (fire) {
+      atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nvec * 16ull);
+      fire_fault(k, p.faults[fire - 1], t, o, j);
+      sh.cause = STOP_FAULT_FIRED;
+    } else {
+      complete_item(k, sh, t, o, j, parts, epoch, own, (hi - lo) * 16u);
+    }
+  }
+  return fire ? ST_STOP : ST_OK;
+}
+
+// thread 0 writes this CTA's record
+__device__ void post_state(const Cta& k, unsigned int state, unsigned int cause) {
+  CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
+  rec.cause = cause;
+  rec.t_stop = gtimer();
+  __threadfence_system();
+  rec.state = state;
+  __threadfence_system();
+}
+
+// all threads: pull the dynamic plan from the control block
+__device__ void load_plan(Cta& k, Shared& sh) {
+  if (k.tid == 0) {
+    Ctrl* C = k.ctrl;
+    unsigned int e = ld_acquire_sys(&C->epoch);
+    sh.seen_epoch = e;
+    sh.freeze = (int)ld_relaxed_sys(&C->freeze);
+    sh.nent = (int)ld_relaxed_sys(&C->nentries);
+    sh.first_adopt = 0;
+  }
+  __syncthreads();
+  if (!sh.freeze) {
+    const int words = (int)(sizeof(PlanEntry) / 4);
+    for (int i = k.tid; i < sh.nent * words; i += k.nthr)
+      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)k.ctrl->entries) + i);
+    if (k.tid == 0) sh.dynamic = 1;
+  }
+  __syncthreads();
+  if (k.tid == 0) {
+    __threadfence_system();
+    k.ctrl->cta[k.cta_in_rank].ack_epoch = sh.seen_epoch;
+    __threadfence_system();
+  }
+  __syncthreads();
+}
+
+// all threads: the merged work list, in (step, origin, chunk) order
+template <int DT>
+__device__ int run_list(Cta& k, Shared& sh) {
+  const LaunchParams& p = *k.p;
+  for (int t = 0; t < p.steps; ++t) {
+    for (int o = 0; o < p.K; ++o) {
+      const bool own = (o == k.c) && k.own_alive;
+      unsigned int mode = PLAN_NONE, mask = 0, assignee = 0, epoch = 0;
+      const unsigned int* bm = nullptr;
+      if (!own) {
+        if (sh.freeze) continue;
+        if (sh.dynamic) {
+          for (int e = 0; e < sh.nent; ++e)
+            if ((int)sh.ent[e].origin == o) {
+              mode = sh.ent[e].mode;
+              mask = sh.ent[e].mask;
+              assignee = sh.ent[e].assignee;
+              bm = sh.ent[e].bitmap;
+            }
+          epoch = sh.seen_epoch;
+        } else if (!(p.conn_mask[k.l] >> o & 1u)) {
+          mask = p.conn_mask[k.l];
+          if (p.strategy == 0) {
+            mode = PLAN_HOT;
+            assignee = 0xFFFFFFFFu;
+            for (int d = 1; d < p.K; ++d)
+              if (mask >> ((o + d) % p.K) & 1u) {
+                assignee = (unsigned int)((o + d) % p.K);
+                break;
+              }
+          } else {
+            mode = PLAN_BAL;
+          }
+        }
+        if (mode == PLAN_NONE) continue;
+        if (mode == PLAN_HOT && assignee != (unsigned int)k.c) continue;
+        if (mode == PLAN_BAL && !(mask >> k.c & 1u)) continue;
+      }
+      for (int j = k.w; j < p.m; j += p.W) {
+        const unsigned long long key = keyof(t, o, j);
+        if (own && key < k.own_next_key) continue;
+        const int q = t * p.m + j;
+        if (bm && !(bm[q >> 5] >> (q & 31) & 1u)) continue;
+        const unsigned int Vj = (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
+        unsigned int lo = 0, hi = Vj, parts = 1;
+        if (!own && mode == PLAN_BAL) {
+          bal_part(Vj, mask, p.weights, p.K, k.c, lo, hi, parts);
+          if (hi == lo) continue;
+        }
+        int st = do_item<DT>(k, sh, t, o, j, lo, hi, parts, epoch, own);
+        if (st != ST_OK) return st;
+        if (own) k.own_next_key = key + 1;
+      }
+    }
+  }
+  return ST_OK;
+}
+
+// all threads: wait for the whole rank to finish (delivered + final flags)
+__device__ int drain(Cta& k, Shared& sh) {
+  const LaunchParams& p = *k.p;
+  if (k.tid == 0) {
+    post_state(k, CTA_DRAINING, 0);
+    sh.wait_t0 = 0;
+  }
+  for (;;) {
+    if (k.tid == 0) {
+      int st = poll_control(k, sh);
+      int cand = 0;
+      if (st == ST_OK) {
+        cand = ld_relaxed_sys((volatile unsigned int*)&k.me.misc->delivered) >= k.total_items;
+        if (!cand) {
+          if (watchdog(k, sh)) {
+            st = ST_TIMEOUT;
+            sh.cause = STOP_TIMEOUT;
+          } else {
+            __nanosleep(200);
+          }
+        }
+      }
+      sh.decision = st;
+      sh.flag = cand;
+    }
+    __syncthreads();
+    const int st = sh.decision;
+    const int cand = sh.flag;
+    __syncthreads();
+    if (st != ST_OK) return st;
+    if (!cand) continue;
+    // all final incoming completion words present?
+    int ok = 1;
+    const int nf = p.K * p.m;
+    const unsigned int* fin = k.me.flags + fidx(p, p.steps - 1, 0, 0);
+    for (int i = k.tid; i < nf; i += k.nthr)
+      if ((int)(ld_acquire_sys(fin + i) - k.seq) < 0) ok = 0;
+    if (__syncthreads_and(ok)) return ST_OK;
+    if (k.tid == 0) sh.flag = watchdog(k, sh) ? -1 : 0;
+    __syncthreads();
+    const int expired = sh.flag == -1;
+    __syncthreads();
+    if (expired) {
+      if (k.tid == 0) sh.cause = STOP_TIMEOUT;
+      return ST_TIMEOUT;
+    }
+  }
+}
+
+// in-place: copy the staged own shard into recv (pieces grabbed atomically)
+__device__ void copy_stage(Cta& k, Shared& sh) {
+  const LaunchParams& p = *k.p;
+  const unsigned long long shard_vec = p.shard / p.V;
+  const unsigned int PIECE = 4096;
+  const unsigned long long npieces = (shard_vec + PIECE - 1) / PIECE;
+  __threadfence();
+  for (;;) {
+    if (k.tid == 0) sh.piece = atomicAdd(&k.me.misc->copy_next, 1u);
+    __syncthreads();
+    const unsigned long long pc = sh.piece;
+    __syncthreads();
+    if (pc >= npieces) break;
+    const unsigned long long v0 = pc * PIECE;
+    const unsigned int nv = (unsigned int)min((unsigned long long)PIECE, shard_vec - v0);
+    const unsigned long long e0 = (unsigned long long)k.r * p.shard + v0 * p.V;
+    if (e0 >= p.N) continue;
+    for (unsigned int v = k.tid; v < nv; v += k.nthr) {
+      long long ev = (long long)(e0 + (unsigned long long)v * p.V);
+      long long left = (long long)p.N - ev;
+      int valid = left <= 0 ? 0 : (left >= p.V ? p.V : (int)left);
+      if (!valid) continue;
+      uint4 a = ld_cg(k.me.stage + (v0 + v) * 16);
+      st_user(p.recv[k.l] + (size_t)ev * p.elem_bytes, a, valid, p.elem_bytes);
+    }
+  }
+}
+
+template <int DT>
+__device__ void cta_main(Cta& k, Shared& sh) {
+  int st;
+  unsigned int exit_state = CTA_EXITED;
+  for (;;) {
+    st = run_list<DT>(k, sh);
+    if (st == ST_REPLAN) {
+      load_plan(k, sh);
+      continue;
+    }
+    if (st != ST_OK) break;
+    st = drain(k, sh);
+    if (st == ST_REPLAN) {
+      load_plan(k, sh);
+      continue;
+    }
+    break;
+  }
+  if (st == ST_OK) {
+    if (k.p->inplace) copy_stage(k, sh);
+  } else if (k.tid == 0) {
+    exit_state = (st == ST_STOP) ? CTA_STOPPED : CTA_EXITED;
+    if (st == ST_TIMEOUT) {
+      // local abort: the rest of this rank stops waiting too
+      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
+    }
+    if (st == ST_STOP && sh.cause == STOP_DEATH) {
+      // bilateral awareness starts at the detecting sender
+      ErrRec& e = k.ctrl->err[k.c];
+      if (e.seq != k.seq) {
+        e.cause = STOP_DEATH;
+        e.origin = (unsigned int)k.c;
+        e.q = 0;
+        e.t_fire = gtimer();
+        __threadfence_system();
+        e.seq = k.seq;
+      }
+    }
+  }
+  if (k.tid == 0) {
+    post_state(k, exit_state, st == ST_OK ? 0u : (unsigned int)sh.cause);
+    const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
+    unsigned int v = atomicAdd(&k.me.misc->exited, 1u);
+    if (v == per_rank - 1) {
+      // last CTA of this rank: nobody reads these any more in this launch
+      k.me.misc->delivered = 0;
+      k.me.misc->copy_next = 0;
+      __threadfence();
+      atomicExch(&k.me.misc->exited, 0u);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_constant__ LaunchParams p) {
+  __shared__ Shared sh;
+  Cta k;
+  k.p = &p;
+  const int per_rank = p.K * p.W;
+  k.l = blockIdx.x / per_rank;
+  k.cta_in_rank = blockIdx.x % per_rank;
+  k.c = k.cta_in_rank / p.W;
+  k.w = k.cta_in_rank % p.W;
+  k.r = p.first_rank + k.l;
+  k.r1 = (k.r + 1) % p.n;
+  k.tid = threadIdx.x;
+  k.nthr = blockDim.x;
+  k.seq = p.seq;
+  k.par = (int)(p.seq & 1u);
+  k.me = p.peers[k.l * p.n + k.r];
+  k.nx = p.peers[k.l * p.n + k.r1];
+  k.ctrl = p.ctrl[k.l];
+  k.total_items = (unsigned int)(p.steps * p.K * p.m);
+  k.own_alive = (p.conn_mask[k.l] >> k.c) & 1u;
+  k.own_next_key = 0;
+  k.fault_channel = false;
+  for (int i = 0; i < p.nfaults; ++i)
+    if ((int)p.faults[i].rank == k.r && (int)p.faults[i].channel == k.c && p.faults[i].kind <= 2)
+      k.fault_channel = true;
+  if (k.tid == 0) {
+    sh.decision = 0;
+    sh.cause = 0;
+    sh.fire = 0;
+    sh.seen_epoch = 0;
+    sh.dynamic = 0;
+    sh.freeze = 0;
+    sh.nent = 0;
+    sh.alerted = 0;
+    sh.recv_next = nullptr;
+    sh.first_adopt = 0;
+    sh.wait_t0 = 0;
+    CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
+    rec.ack_epoch = 0;
+    rec.cause = 0;
+    rec.seq = k.seq;
+    __threadfence_system();
+    rec.state = CTA_RUNNING;
+    if (!p.sim && k.cta_in_rank == 0) {
+      // publish our recv (registration id, offset) for the upstream rank
+      volatile unsigned long long* d = k.me.desc + k.par * 4;
+      d[1] = (unsigned long long)p.recv_reg[k.l];
+      d[2] = p.recv_off[k.l];
+      fence_sys();
+      d[0] = k.seq;
+      fence_sys();
+    }
+  }
+  __syncthreads();
+  if (p.dtype == R2D_INT32) cta_main<R2D_INT32>(k, sh);
+  else if (p.dtype == R2D_FLOAT32) cta_main<R2D_FLOAT32>(k, sh);
+  else cta_main<R2D_BF16>(k, sh);
+}
+
+// ------------------------------------------------------------ probe kernel
+// Zero-byte probe: a flag-only store into the target's per-(prober,
+// channel) mailbox over the peer mapping, then a read-back of the same word
+// (the completion).  Emulated outcome (reading C-11): LOCAL_ERROR if the
+// prober's endpoint is dead; the store is dropped (-> TIMEOUT after the
+// timeout) if the target's endpoint or a link between them is dead.
+__global__ void r2_probe_kernel(const __grid_constant__ ProbeParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int res;
+  const int K = p.K, c = p.channel;
+  if (ld_relaxed_sys(p.ep_dead + p.prober * K + c)) {
+    res = 1;
+  } else {
+    bool link = ((p.target == (p.prober + 1) % p.n) && ld_relaxed_sys(p.link_dead + p.prober * K + c)) ||
+                ((p.prober == (p.target + 1) % p.n) && ld_relaxed_sys(p.link_dead + p.target * K + c));
+    bool dropped = link || ld_relaxed_sys(p.ep_dead + p.target * K + c);
+    if (!dropped) {
+      st_relaxed_sys(p.target_mailbox, p.token);
+      fence_sys();
+    }
+    res = 2;
+    unsigned long long t0 = gtimer();
+    while (gtimer() - t0 < p.timeout_ns) {
+      if (!dropped && ld_acquire_sys(p.target_mailbox) == p.token) {
+        res = 0;
+        break;
+      }
+    }
+  }
+  *p.result = res;
+  __threadfence_system();
+}
+
+}  // namespace
+
+int r2_launch_allreduce(const LaunchParams& p, int nctas, int threads, void* stream) {
+  void* args[] = {(void*)&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
+                                              (cudaStream_t)stream);
+  return (int)e;
+}
+
+int r2_launch_probe(const ProbeParams& p, void* stream) {
+  r2_probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+int r2_kernel_smem_bytes() { return (int)sizeof(Shared); }
+
+int r2_max_coop_ctas(int threads) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, r2_allreduce_kernel, threads, 0);
+  return nsm * per;
+}

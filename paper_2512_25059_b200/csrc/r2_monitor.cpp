@@ -1,0 +1,674 @@
+// r2_monitor.cpp -- the per-process monitor thread: R²CCL's failure
+// detection and mitigation control plane (PAPER §4).
+//
+//   1. detection: a stopped channel posts an error record into the
+//      host-mapped control block (the CQ/QP error of P:744);
+//   2. bilateral awareness: NOTIFY to every rank over the out-of-band
+//      channel;
+//   3. localization: a three-point triangulation round -- zero-byte
+//      probe-flag kernels A->B, B->A, aux->A, aux->B -- and the decision
+//      table of reading C-10; the verdict is broadcast to all ranks;
+//   4. live migration: every rank whose outgoing connection the verdict
+//      condemns waits for that channel to quiesce, rolls back from the
+//      completion flags (first chunk without completion / last confirmed
+//      chunk) and publishes a re-placement plan: the first healthy
+//      channel of the failover chain (HotRepair) or a
+//      weight-proportional split over all healthy channels (R²CCL-Balance,
+//      P:73).  A later failure of an adopting channel re-evaluates the
+//      rollback and moves on (P:36 successive failover); an exhausted chain
+//      aborts the collective with NO_BACKUP.
+#include <string.h>
+#include <time.h>
+
+#include <algorithm>
+#include <chrono>
+#include <thread>
+
+#include "r2_comm.h"
+
+namespace {
+
+void deliver_local(r2_comm* c, const Msg& m) {
+  std::lock_guard<std::mutex> g(c->qmu);
+  c->localq.push_back(m);
+}
+
+bool is_local(const r2_comm* c, int rank) { return rank >= c->first_rank && rank < c->first_rank + c->nlocal; }
+
+int aux_of(int a, int b, int n) {
+  for (int r = 0; r < n; ++r)
+    if (r != a && r != b) return r;
+  return -1;
+}
+
+void broadcast(r2_comm* c, Msg m) {
+  for (int d = 0; d < c->n; ++d) r2_send_msg(c, d, m);
+}
+
+const LaunchInfo* launch_of(r2_comm* c, uint32_t seq) {
+  auto it = c->launches.find(seq);
+  return it == c->launches.end() ? nullptr : &it->second;
+}
+
+// ------------------------------------------------------------------ probes
+void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int owner, uint32_t round_id,
+                 uint32_t seq) {
+  const int l = prober - c->first_rank;
+  const int idx = c->probe_res_next;
+  c->probe_res_next = (c->probe_res_next + 1) % r2_comm::kProbeSlots;
+  c->probe_res_host[idx] = -1;
+  const RankPtrs& tgt = c->peers_host[l * c->n + target];
+  const RankPtrs& me = c->peers_host[l * c->n + prober];
+  ProbeParams pp;
+  pp.target_mailbox = tgt.mailbox + prober * c->K + channel;
+  pp.ep_dead = me.ep_dead;
+  pp.link_dead = me.link_dead;
+  pp.prober = prober;
+  pp.target = target;
+  pp.channel = channel;
+  pp.n = c->n;
+  pp.K = c->K;
+  pp.token = ++c->probe_token;
+  if (pp.token == 0) pp.token = ++c->probe_token;
+  pp.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
+  pp.result = c->probe_res_dev + idx;
+  int rc = r2_launch_probe(pp, c->mon_stream);
+  PendingProbe pr{prober, target, channel, slot, l, owner, round_id, seq, c->probe_res_host + idx, idx};
+  if (rc != 0) c->probe_res_host[idx] = R2_PROBE_NOT_RUN;
+  c->probes.push_back(pr);
+}
+
+void round_result(r2_comm* c, uint32_t id, int slot, int outcome) {
+  for (size_t i = 0; i < c->rounds.size(); ++i) {
+    Round& rd = c->rounds[i];
+    if (rd.id != id) continue;
+    rd.outcomes[slot] = outcome;
+    for (int s = 0; s < rd.need; ++s)
+      if (rd.outcomes[s] < 0) return;
+    const int v = r2_triangulate(rd.outcomes, rd.aux >= 0);
+    Msg m{};
+    m.type = MSG_VERDICT;
+    m.seq = rd.seq;
+    m.round_owner = rd.a;
+    m.round_id = rd.id;
+    m.a = rd.a;
+    m.b = rd.b;
+    m.aux = rd.aux;
+    m.channel = rd.channel;
+    m.verdict = v;
+    for (int s = 0; s < 4; ++s) m.outcomes[s] = s < rd.need ? rd.outcomes[s] : R2_PROBE_NOT_RUN;
+    {
+      std::lock_guard<std::mutex> g(c->pmu);
+      r2_verdict_t vd{};
+      vd.kind = v;
+      vd.a = rd.a;
+      vd.b = rd.b;
+      vd.aux = rd.aux;
+      vd.channel = rd.channel;
+      for (int s = 0; s < 4; ++s) vd.outcome[s] = m.outcomes[s];
+      c->finished_rounds[rd.id] = vd;
+    }
+    c->rounds.erase(c->rounds.begin() + i);
+    broadcast(c, m);
+    return;
+  }
+}
+
+void start_round(r2_comm* c, uint32_t id, uint32_t seq, int a, int b, int channel) {
+  Round rd{};
+  rd.id = id;
+  rd.seq = seq;
+  rd.a = a;
+  rd.b = b;
+  rd.aux = aux_of(a, b, c->n);
+  rd.channel = channel;
+  rd.local = a - c->first_rank;
+  rd.need = rd.aux >= 0 ? 4 : 2;
+  for (int s = 0; s < 4; ++s) rd.outcomes[s] = -1;
+  rd.t_start = r2_now_ns();
+  c->rounds.push_back(rd);
+  // A -> B locally; B -> A, aux -> A, aux -> B by their owners
+  start_probe(c, a, b, channel, 0, a, id, seq);
+  Msg m{};
+  m.type = MSG_PROBE_REQ;
+  m.seq = seq;
+  m.round_owner = a;
+  m.round_id = id;
+  m.channel = channel;
+  m.prober = b; m.target = a; m.slot = 1;
+  r2_send_msg(c, b, m);
+  if (rd.aux >= 0) {
+    m.prober = rd.aux; m.target = a; m.slot = 2;
+    r2_send_msg(c, rd.aux, m);
+    m.prober = rd.aux; m.target = b; m.slot = 3;
+    r2_send_msg(c, rd.aux, m);
+  }
+}
+
+bool progress_probes(r2_comm* c) {
+  bool busy = false;
+  for (size_t i = 0; i < c->probes.size();) {
+    PendingProbe& pr = c->probes[i];
+    int v = *pr.res_host;
+    if (v < 0) {
+      ++i;
+      continue;
+    }
+    busy = true;
+    PendingProbe done = pr;
+    c->probes.erase(c->probes.begin() + i);
+    if (is_local(c, done.round_owner)) {
+      round_result(c, done.round_id, done.slot, v);
+    } else {
+      Msg m{};
+      m.type = MSG_PROBE_RES;
+      m.seq = done.seq;
+      m.round_owner = done.round_owner;
+      m.round_id = done.round_id;
+      m.slot = done.slot;
+      m.outcome = v;
+      r2_send_msg(c, done.round_owner, m);
+    }
+  }
+  return busy;
+}
+
+// ------------------------------------------------------------------ ctrl
+void ctrl_init_for(r2_comm* c, int l, uint32_t seq) {
+  if (c->plan_seq[l] == seq) return;
+  Ctrl* C = c->ctrl_host[l];
+  C->abort = 0;
+  C->freeze = 0;
+  C->stop_mask = 0;
+  C->nentries = 0;
+  C->epoch = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  C->plan_seq = seq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->plan_seq[l] = seq;
+  c->epoch[l] = 0;
+  c->cur_plan[l].clear();
+}
+
+void set_abort(r2_comm* c, int l, uint32_t seq) {
+  ctrl_init_for(c, l, seq);
+  Ctrl* C = c->ctrl_host[l];
+  C->abort = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+}
+
+void record_error(r2_comm* c, int err, uint32_t seq) {
+  std::lock_guard<std::mutex> g(c->mu);
+  c->last_error = err;
+  c->last_error_seq = seq;
+  c->unreported_error = err;
+}
+
+// ------------------------------------------------------------------ verdicts
+void on_verdict(r2_comm* c, const Msg& m) {
+  const int K = c->K, n = c->n;
+  std::vector<int> kill_ep;
+  bool kill_link = false;
+  switch (m.verdict) {
+    case R2_V_LOCAL_ENDPOINT:
+    case R2_V_ENDPOINT_UNREACHABLE_A: kill_ep.push_back(m.a); break;
+    case R2_V_REMOTE_ENDPOINT:
+    case R2_V_ENDPOINT_UNREACHABLE_B: kill_ep.push_back(m.b); break;
+    case R2_V_DUAL_ENDPOINT:
+    case R2_V_TWO_LOCAL: kill_ep.push_back(m.a); kill_ep.push_back(m.b); break;
+    case R2_V_LINK:
+    case R2_V_INCONCLUSIVE: kill_link = true; break;   // S:356 migrate anyway
+    default: break;
+  }
+  r2_verdict_t vd{};
+  vd.kind = m.verdict;
+  vd.a = m.a;
+  vd.b = m.b;
+  vd.aux = m.aux;
+  vd.channel = m.channel;
+  for (int s = 0; s < 4; ++s) vd.outcome[s] = m.outcomes[s];
+  std::lock_guard<std::mutex> g(c->mu);
+  for (int e : kill_ep) c->ep_dead[e * K + m.channel] = 1;
+  if (kill_link && m.b == (m.a + 1) % n) c->link_dead[m.a * K + m.channel] = 1;
+  if (m.seq == 0) return;
+  const LaunchInfo* li = launch_of(c, m.seq);
+  if (!li) return;
+  for (int l = 0; l < c->nlocal; ++l) {
+    const int r = c->first_rank + l;
+    for (int k = 0; k < K; ++k) {
+      if (!(li->conn_mask[l] >> k & 1u)) continue;       // statically adopted already
+      if (r2_conn_ok(c, r, k)) continue;
+      auto key = std::make_pair(m.seq, l * K + k);
+      if (c->planned.count(key)) continue;
+      // a connection this rank detected itself waits for its own round
+      auto dk = c->planned.find(std::make_pair(m.seq, -(l * K + k) - 1));
+      if (dk != c->planned.end() && !(m.a == r && m.channel == k)) continue;
+      c->planned[key] = 1;
+      Replan rp{};
+      rp.seq = m.seq;
+      rp.l = l;
+      rp.channel = k;
+      rp.verdict = vd;
+      rp.stage = 0;
+      rp.t_verdict = r2_now_ns();
+      rp.t_detect = rp.t_verdict;
+      auto dt = c->planned.find(std::make_pair(m.seq, -(l * K + k) - 1));
+      (void)dt;
+      c->replans.push_back(rp);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ messages
+bool handle_msg(r2_comm* c, const Msg& m) {
+  switch (m.type) {
+    case MSG_NOTIFY:
+      // bilateral awareness: the peer learns the connection failed;
+      // its kernel keeps waiting on the canonical flags, which the
+      // sender's re-placement will deliver.
+      break;
+    case MSG_PROBE_REQ:
+      if (is_local(c, m.prober)) start_probe(c, m.prober, m.target, m.channel, m.slot, m.round_owner, m.round_id, m.seq);
+      break;
+    case MSG_PROBE_RES:
+      round_result(c, m.round_id, m.slot, m.outcome);
+      break;
+    case MSG_VERDICT:
+      on_verdict(c, m);
+      break;
+    case MSG_ABORT:
+      for (int l = 0; l < c->nlocal; ++l) set_abort(c, l, m.seq);
+      record_error(c, m.error ? m.error : R2_ERR_NO_BACKUP, m.seq);
+      break;
+  }
+  return true;
+}
+
+bool drain_messages(r2_comm* c) {
+  bool busy = false;
+  for (;;) {
+    Msg m;
+    bool got = false;
+    {
+      std::lock_guard<std::mutex> g(c->qmu);
+      if (!c->localq.empty()) {
+        m = c->localq.front();
+        c->localq.pop_front();
+        got = true;
+      }
+    }
+    if (!got && c->has_oob) {
+      int src = -1;
+      size_t len = 0;
+      if (c->oob.poll(c->oob.ctx, &src, &m, sizeof(m), &len) == 1 && len == sizeof(m)) got = true;
+    }
+    if (!got) break;
+    busy = true;
+    handle_msg(c, m);
+  }
+  return busy;
+}
+
+// ------------------------------------------------------------------ detection
+bool scan_device_records(r2_comm* c) {
+  bool busy = false;
+  const int K = c->K;
+  for (int l = 0; l < c->nlocal; ++l) {
+    Ctrl* C = c->ctrl_host[l];
+    const int r = c->first_rank + l;
+    for (int k = 0; k < K; ++k) {
+      ErrRec& e = C->err[k];
+      const uint32_t s = e.seq;
+      if (!s || s == c->handled_err[l * K + k]) continue;
+      std::atomic_thread_fence(std::memory_order_acquire);
+      c->handled_err[l * K + k] = s;
+      busy = true;
+      const uint64_t now = r2_now_ns();
+      {
+        std::lock_guard<std::mutex> g(c->mu);
+        // remember that this rank detected (seq, l, k) itself -> use own round
+        c->planned[std::make_pair(s, -(l * K + k) - 1)] = 1;
+      }
+      // bilateral awareness
+      Msg nm{};
+      nm.type = MSG_NOTIFY;
+      nm.seq = s;
+      nm.a = r;
+      nm.b = (r + 1) % c->n;
+      nm.channel = k;
+      nm.t_fire = e.t_fire;
+      broadcast(c, nm);
+      uint32_t id;
+      {
+        std::lock_guard<std::mutex> g(c->pmu);
+        id = ((uint32_t)r << 24) | (++c->round_counter & 0xFFFFFF);
+      }
+      start_round(c, id, s, r, (r + 1) % c->n, k);
+      (void)now;
+    }
+    // watchdog expiries -> abort everywhere
+    for (int i = 0; i < K * c->W; ++i) {
+      CtaRec& rec = C->cta[i];
+      if (rec.cause == STOP_TIMEOUT && rec.seq != 0 && c->timeout_seq[l] != rec.seq) {
+        const uint32_t s = rec.seq;
+        c->timeout_seq[l] = s;   // report once
+        record_error(c, R2_ERR_TIMEOUT, s);
+        Msg m{};
+        m.type = MSG_ABORT;
+        m.seq = s;
+        m.error = R2_ERR_TIMEOUT;
+        broadcast(c, m);
+        busy = true;
+        break;
+      }
+    }
+  }
+  return busy;
+}
+
+// ------------------------------------------------------------------ re-plans
+bool channel_quiesced(r2_comm* c, int l, int k, uint32_t seq) {
+  Ctrl* C = c->ctrl_host[l];
+  for (int w = 0; w < c->W; ++w) {
+    CtaRec& rec = C->cta[k * c->W + w];
+    if (rec.seq != seq) return false;
+    unsigned st = rec.state;
+    if (st != CTA_STOPPED && st != CTA_DRAINING && st != CTA_EXITED) return false;
+  }
+  return true;
+}
+
+bool channel_stopped(r2_comm* c, int l, int k, uint32_t seq) {
+  Ctrl* C = c->ctrl_host[l];
+  for (int w = 0; w < c->W; ++w) {
+    CtaRec& rec = C->cta[k * c->W + w];
+    if (rec.seq == seq && rec.state == CTA_STOPPED) return true;
+  }
+  return false;
+}
+
+bool freeze_acked(r2_comm* c, int l, uint32_t seq, uint32_t epoch) {
+  Ctrl* C = c->ctrl_host[l];
+  for (int i = 0; i < c->K * c->W; ++i) {
+    CtaRec& rec = C->cta[i];
+    if (rec.seq != seq) continue;                 // not started: sees the freeze first
+    unsigned st = rec.state;
+    if (st != CTA_RUNNING && st != CTA_DRAINING) continue;
+    if (rec.ack_epoch != epoch) return false;
+  }
+  return true;
+}
+
+void publish_plan(r2_comm* c, Replan& rp) {
+  const int l = rp.l, K = c->K, r = c->first_rank + l, r1 = (r + 1) % c->n;
+  Ctrl* C = c->ctrl_host[l];
+  LaunchInfo li;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    const LaunchInfo* p = launch_of(c, rp.seq);
+    if (!p) return;
+    li = *p;
+  }
+  const int m = li.m, steps = li.steps;
+  // rollback: read the receiver's completion words (reading C-4)
+  std::vector<unsigned int> flags((size_t)steps * K * m);
+  const RankPtrs& nx = c->peers_host[l * c->n + r1];
+  cudaMemcpyAsync(flags.data(), nx.flags, flags.size() * 4, cudaMemcpyDeviceToHost, c->mon_stream);
+  cudaStreamSynchronize(c->mon_stream);
+  auto done = [&](int t, int o, int j) { return (int)(flags[((size_t)t * K + o) * m + j] - rp.seq) >= 0; };
+
+  // healthy: assignable channels; dead: origins re-placed now (statically
+  // dead, or known dead AND quiesced -- a known-dead channel whose CTAs are
+  // still draining items below its fault point waits for its own re-plan)
+  uint32_t healthy = 0, dead = 0;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    for (int k = 0; k < K; ++k) {
+      const bool known_ok = r2_conn_ok(c, r, k) && (li.conn_mask[l] >> k & 1u);
+      if (known_ok && !channel_stopped(c, l, k, rp.seq)) healthy |= 1u << k;
+      if (!(li.conn_mask[l] >> k & 1u) || (!known_ok && channel_quiesced(c, l, k, rp.seq))) dead |= 1u << k;
+    }
+  }
+  // what did the stopped channel carry under the previous plan?
+  auto carried_by = [&](int k, int o) -> bool {
+    if (c->epoch[l] > 0) {
+      for (const PlanEntry& e : c->cur_plan[l])
+        if ((int)e.origin == o) return (e.mode == PLAN_HOT) ? (int)e.assignee == k : (e.mask >> k & 1u);
+      return false;
+    }
+    if (li.conn_mask[l] >> o & 1u) return false;
+    if (c->cfg.strategy == R2_HOT_REPAIR) return r2_first_healthy_in_chain(o, li.conn_mask[l], K) == k;
+    return li.conn_mask[l] >> k & 1u;
+  };
+  std::vector<PlanEntry> ents;
+  std::vector<r2_event_t> evs;
+  bool nobackup = false;
+  const uint64_t now = r2_now_ns();
+  for (int o = 0; o < K; ++o) {
+    if (!(dead >> o & 1u)) continue;
+    PlanEntry pe;
+    memset(&pe, 0, sizeof(pe));
+    pe.origin = o;
+    std::vector<uint8_t> comp((size_t)steps * m);
+    int nres = 0;
+    for (int t = 0; t < steps; ++t)
+      for (int j = 0; j < m; ++j) {
+        bool d = done(t, o, j);
+        comp[(size_t)t * m + j] = d;
+        if (!d) {
+          int q = t * m + j;
+          pe.bitmap[q >> 5] |= 1u << (q & 31);
+          nres++;
+        }
+      }
+    int resume = 0, floor = 0;
+    r2_rollback(comp.data(), steps * m, &resume, &floor);
+    r2_event_t ev;
+    memset(&ev, 0, sizeof(ev));
+    ev.seq = rp.seq;
+    ev.rank = r;
+    ev.origin_channel = o;
+    ev.stopped_channel = rp.channel;
+    ev.verdict = rp.verdict;
+    ev.resume = resume;
+    ev.floor = floor;
+    ev.retransmit = nres;
+    ev.strategy = c->cfg.strategy;
+    ev.assignee = -1;
+    ev.chain_pos = -1;
+    ev.failover_ms = -1.0;
+    ev.t_detect_host_ns = rp.t_detect;
+    ev.t_verdict_host_ns = rp.t_verdict;
+    ev.t_plan_host_ns = now;
+    if (c->cfg.strategy == R2_HOT_REPAIR) {
+      int a = r2_first_healthy_in_chain(o, healthy, K);
+      if (a < 0) nobackup = true;
+      pe.mode = PLAN_HOT;
+      pe.assignee = a < 0 ? 0 : a;
+      pe.mask = healthy;
+      ev.assignee = a;
+      ev.chain_pos = a < 0 ? -1 : ((a - o - 1) % K + K) % K;
+    } else {
+      pe.mode = PLAN_BAL;
+      pe.mask = healthy;
+      uint64_t sh[R2_MAX_CHANNELS];
+      int w[R2_MAX_CHANNELS];
+      for (int k = 0; k < K; ++k) w[k] = (int)c->weights[k];
+      if (r2_balance_shares(li.chunk / li.V, w, healthy, K, sh) != R2_SUCCESS) nobackup = true;
+      else
+        for (int k = 0; k < K; ++k) ev.shares[k] = (int)sh[k];
+    }
+    if (nobackup) ev.error = R2_ERR_NO_BACKUP;
+    const bool record = (o == rp.channel) || (carried_by(rp.channel, o) && nres > 0);
+    if (record) {
+      ErrRec& er = C->err[rp.channel];
+      if (er.seq == rp.seq) ev.t_fire_dev_ns = er.t_fire;
+      evs.push_back(ev);
+    }
+    ents.push_back(pe);
+  }
+  if (nobackup || healthy == 0) {
+    set_abort(c, l, rp.seq);
+    record_error(c, R2_ERR_NO_BACKUP, rp.seq);
+    Msg m2{};
+    m2.type = MSG_ABORT;
+    m2.seq = rp.seq;
+    m2.error = R2_ERR_NO_BACKUP;
+    broadcast(c, m2);
+    std::lock_guard<std::mutex> g(c->mu);
+    for (auto& ev : evs) {
+      ev.error = R2_ERR_NO_BACKUP;
+      c->events.push_back(ev);
+    }
+    return;
+  }
+  // publish: entries, unfreeze, new epoch (device reloads and acks)
+  for (size_t i = 0; i < ents.size(); ++i) memcpy((void*)&C->entries[i], &ents[i], sizeof(PlanEntry));
+  C->nentries = (unsigned)ents.size();
+  C->freeze = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->epoch[l]++;
+  C->epoch = c->epoch[l];
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->cur_plan[l] = ents;
+  std::lock_guard<std::mutex> g(c->mu);
+  for (auto& ev : evs) {
+    c->events.push_back(ev);
+    EventTiming et{(int)c->events.size() - 1, l, rp.seq, c->epoch[l], ev.t_fire_dev_ns};
+    c->timings.push_back(et);
+  }
+}
+
+bool progress_replans(r2_comm* c) {
+  bool busy = false;
+  for (size_t i = 0; i < c->replans.size();) {
+    Replan& rp = c->replans[i];
+    const int l = rp.l;
+    Ctrl* C = c->ctrl_host[l];
+    bool fault_channel = false;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      const LaunchInfo* li = launch_of(c, rp.seq);
+      if (li)
+        for (int f = 0; f < li->nfaults; ++f)
+          if ((int)li->faults[f].rank == c->first_rank + l && (int)li->faults[f].channel == rp.channel)
+            fault_channel = true;
+    }
+    ctrl_init_for(c, l, rp.seq);
+    if (rp.stage == 0) {
+      if (!fault_channel && !(C->stop_mask >> rp.channel & 1u)) {
+        C->stop_mask = C->stop_mask | (1u << rp.channel);
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+      }
+      if (!channel_quiesced(c, l, rp.channel, rp.seq)) {
+        ++i;
+        continue;
+      }
+      // freeze adopted work when other channels may hold parts of it
+      bool need_freeze = c->epoch[l] > 0;
+      {
+        std::lock_guard<std::mutex> g(c->mu);
+        const LaunchInfo* li = launch_of(c, rp.seq);
+        const uint32_t full = (c->K >= 32) ? 0xFFFFFFFFu : ((1u << c->K) - 1u);
+        if (li && li->conn_mask[l] != full) need_freeze = true;
+      }
+      if (need_freeze) {
+        C->freeze = 1;
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        c->epoch[l]++;
+        C->epoch = c->epoch[l];
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        rp.freeze_epoch = c->epoch[l];
+        rp.stage = 1;
+        busy = true;
+        ++i;
+        continue;
+      }
+      rp.stage = 2;
+    }
+    if (rp.stage == 1) {
+      if (!freeze_acked(c, l, rp.seq, rp.freeze_epoch)) {
+        ++i;
+        continue;
+      }
+      rp.stage = 2;
+    }
+    publish_plan(c, rp);
+    busy = true;
+    c->replans.erase(c->replans.begin() + i);
+  }
+  return busy;
+}
+
+bool progress_timings(r2_comm* c) {
+  bool busy = false;
+  for (size_t i = 0; i < c->timings.size();) {
+    EventTiming& et = c->timings[i];
+    Ctrl* C = c->ctrl_host[et.l];
+    const uint32_t tag = (et.seq << 8) | (et.epoch & 0xFFu);
+    unsigned long long best = 0;
+    bool all_done = true;
+    for (int k = 0; k < c->K * c->W; ++k) {
+      CtaRec& rec = C->cta[k];
+      if (rec.adopt_tag == tag) {
+        unsigned long long t = rec.t_first_adopt;
+        if (t && (!best || t < best)) best = t;
+      }
+      if (rec.seq == et.seq && rec.state != CTA_EXITED && rec.state != CTA_STOPPED) all_done = false;
+    }
+    std::lock_guard<std::mutex> g(c->mu);
+    r2_event_t& ev = c->events[et.event_index];
+    if (best && et.t_fire_dev) {
+      ev.t_first_retx_dev_ns = best;
+      ev.failover_ms = (double)(long long)(best - et.t_fire_dev) / 1e6;
+    }
+    if (all_done) {
+      c->timings.erase(c->timings.begin() + i);
+      busy = true;
+    } else {
+      ++i;
+    }
+  }
+  return busy;
+}
+
+bool take_probe_requests(r2_comm* c) {
+  std::pair<int, std::pair<int, int>> req;
+  uint32_t id;
+  {
+    std::lock_guard<std::mutex> g(c->pmu);
+    if (c->probe_requests.empty()) return false;
+    req = c->probe_requests.front();
+    id = c->probe_request_ids.front();
+    c->probe_requests.pop_front();
+    c->probe_request_ids.pop_front();
+  }
+  start_round(c, id, 0, c->first_rank + req.first, req.second.first, req.second.second);
+  return true;
+}
+
+}  // namespace
+
+void r2_send_msg(r2_comm* c, int dst, Msg m) {
+  m.src = c->rank;
+  m.dst = dst;
+  if (c->sim || dst == c->rank) {
+    deliver_local(c, m);
+    return;
+  }
+  c->oob.post(c->oob.ctx, dst, &m, sizeof(m));
+}
+
+void r2_monitor_main(r2_comm* c) {
+  cudaSetDevice(c->dev);
+  while (!c->stop.load()) {
+    bool busy = false;
+    busy |= scan_device_records(c);
+    busy |= drain_messages(c);
+    busy |= progress_probes(c);
+    busy |= progress_replans(c);
+    busy |= progress_timings(c);
+    busy |= take_probe_requests(c);
+    if (!busy) std::this_thread::sleep_for(std::chrono::microseconds(10));
+  }
+}

@@ -1,0 +1,77 @@
+"""torch glue: tensors -> (pointer, count, dtype, stream) for the C ABI, and
+communicator bootstrap from torch.distributed's environment / c10d store
+(the process-group bootstrap of P:657 carries only the OOB segment name).
+PyTorch provides device memory, streams and process groups -- nothing else.
+"""
+from __future__ import annotations
+
+import itertools
+import os
+
+import torch
+
+from . import r2ccl as R
+
+TORCH_DTYPES = {torch.int32: R.INT32, torch.float32: R.FLOAT32, torch.bfloat16: R.BFLOAT16}
+_counter = itertools.count()
+
+
+def r2_dtype(t: torch.Tensor) -> int:
+    try:
+        return TORCH_DTYPES[t.dtype]
+    except KeyError as e:
+        raise TypeError(f"r2ccl supports int32/float32/bfloat16, not {t.dtype}") from e
+
+
+def comm_from_env(cfg: R.Config | None = None, store=None) -> R.Comm:
+    """One communicator per process, ranks from RANK / WORLD_SIZE / LOCAL_RANK
+    (torchrun).  world > 1 needs an initialised default process group (its
+    store carries the OOB name) or an explicit c10d store."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    if world == 1:
+        return R.Comm(0, 1, local, None, cfg)
+    if store is None:
+        store = torch.distributed.distributed_c10d._get_default_store()
+    key = f"r2ccl/oob/{next(_counter)}"
+    if rank == 0:
+        name = R.unique_name()
+        store.set(key, name)
+    else:
+        name = store.get(key).decode()
+    oob = R.oob_shm_open(name, rank, world)
+    return R.Comm(rank, world, local, oob, cfg)
+
+
+def register(comm: R.Comm, t: torch.Tensor) -> int:
+    """Collective: register t's storage with every peer (r2_register_multi)."""
+    return comm.register_multi(t.data_ptr(), t.numel() * t.element_size())
+
+
+def allreduce(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Sum-allreduce send -> recv (in place when recv is None / send).
+
+    Sim mode (one process, k simulated ranks): send/recv hold the k rank
+    buffers back to back (leading dimension k)."""
+    if recv is None:
+        recv = send
+    if not (send.is_cuda and recv.is_cuda):
+        raise ValueError("device tensors required (use allreduce_host for host buffers)")
+    if not (send.is_contiguous() and recv.is_contiguous()):
+        raise ValueError("contiguous tensors required")
+    if send.dtype != recv.dtype or send.numel() != recv.numel():
+        raise ValueError("send/recv must match in dtype and size")
+    count = send.numel() // (comm.n if comm.sim else 1)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    comm.allreduce(send.data_ptr(), recv.data_ptr(), count, r2_dtype(send), s.cuda_stream)
+    return recv
+
+
+def allreduce_host(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None) -> torch.Tensor:
+    """Host (ideally pinned) tensors: H2D, allreduce, D2H on `stream`."""
+    count = send.numel() // (comm.n if comm.sim else 1)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    comm.allreduce_host(send.data_ptr(), recv.data_ptr(), count, r2_dtype(send), s.cuda_stream)
+    return recv

@@ -1,0 +1,272 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle, in simulated-
+rank mode: k ranks on one B200 in one cooperative kernel (the 1-GPU
+"local reduce" configuration; ranks that wait on each other must not be
+separate launches on one GPU).  Bit-exact for all dtypes;
+failover records compared field by field with oracle Layer 2."""
+import numpy as np
+import pytest
+import torch
+
+import r2inputs
+from oracle import protocol as OP
+from tests.gpu_util import (check_result, norm_event, oracle_faults, oracle_geom, poisoned, run, same_bits,
+                            sim_comm, to_dev, to_np)
+from paper_2512_25059_b200 import build as B
+from paper_2512_25059_b200 import r2ccl as R
+from paper_2512_25059_b200 import torch_api as T
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def setup(cuda_required):
+    B.build()
+    torch.cuda.set_device(0)
+
+
+_COMMS = {}
+
+
+def healthy_comm(n, K=4, W=2, chunk=64 * 1024):
+    key = (n, K, W, chunk)
+    if key not in _COMMS:
+        _COMMS[key] = sim_comm(n, K, W, chunk)
+    return _COMMS[key]
+
+
+# ------------------------------------------------------------ fault-free
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+@pytest.mark.parametrize("N", [1, 1000, 12345, (1 << 20) + 7])
+def test_fault_free_parity(dtype, n, N):
+    comm = healthy_comm(n)
+    xs = r2inputs.inputs(n, N, dtype, seed=1000 + n)
+    rc, out = run(comm, xs, dtype)
+    assert rc == R.SUCCESS
+    check_result(out, xs, oracle_geom(comm, N, dtype), dtype)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+@pytest.mark.parametrize("K,W,chunk", [(1, 1, 16), (2, 3, 4096), (8, 2, 512 * 1024), (3, 1, 48)])
+def test_fault_free_configs(dtype, K, W, chunk):
+    n, N = 4, 200_003
+    comm = healthy_comm(n, K, W, chunk)
+    xs = r2inputs.inputs(n, N, dtype, seed=77)
+    rc, out = run(comm, xs, dtype)
+    assert rc == R.SUCCESS
+    check_result(out, xs, oracle_geom(comm, N, dtype), dtype)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_inplace_parity(dtype):
+    n, N = 4, 300_001
+    comm = healthy_comm(n)
+    xs = r2inputs.inputs(n, N, dtype, seed=5)
+    rc, out = run(comm, xs, dtype, inplace=True)
+    assert rc == R.SUCCESS
+    check_result(out, xs, oracle_geom(comm, N, dtype), dtype)
+
+
+def test_many_calls_and_wrap_inputs():
+    """Consecutive collectives alternate scratch parity; flags are seq-tagged."""
+    n, N = 3, 100_000
+    comm = healthy_comm(n)
+    for i in range(7):
+        xs = r2inputs.inputs(n, N, "int32", seed=i, dist="wrap")
+        rc, out = run(comm, xs, "int32")
+        assert rc == R.SUCCESS
+        check_result(out, xs, oracle_geom(comm, N, "int32"), "int32")
+
+
+def test_invalid_args():
+    comm = healthy_comm(2)
+    t = torch.zeros((2, 64), dtype=torch.float32, device="cuda")
+    with pytest.raises(R.R2Error) as e:
+        comm.allreduce(t.data_ptr() + 4, t.data_ptr(), 10, R.FLOAT32)
+    assert e.value.code == R.ERR_INVALID_ARG
+    with pytest.raises(R.R2Error):
+        comm.allreduce(t.data_ptr(), t.data_ptr(), (16 << 20), R.FLOAT32)
+    comm.allreduce(t.data_ptr(), t.data_ptr(), 0, R.FLOAT32)  # no-op
+
+
+def test_host_buffers():
+    n, N = 4, 50_000
+    comm = healthy_comm(n)
+    xs = r2inputs.inputs(n, N, "float32", seed=9)
+    send = torch.from_numpy(np.stack(xs)).pin_memory()
+    recv = torch.empty_like(send).pin_memory()
+    T.allreduce_host(comm, send, recv)
+    assert comm.sync() == R.SUCCESS
+    check_result(recv.numpy(), xs, oracle_geom(comm, N, "float32"), "float32")
+
+
+# ------------------------------------------------------------ faults
+
+def faulted(n, K, W, N, dtype, faults, strategy="BALANCE", chunk=64 * 1024, inplace=False, seed=3):
+    comm = sim_comm(n, K, W, chunk, strategy=strategy)
+    for f in faults:
+        comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(n, N, dtype, seed=seed)
+    rc, out = run(comm, xs, dtype, inplace=inplace)
+    g = oracle_geom(comm, N, dtype)
+    return comm, xs, rc, out, g
+
+
+def oracle_of(xs, g, dtype, faults, strategy, inplace=False):
+    return OP.simulate(xs, g, dtype, faults=oracle_faults(faults), strategy=strategy, seed=1, inplace=inplace)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32"])
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_config1_link_fault(dtype, strategy):
+    """BASELINE configs[0]: 4 ranks, 1 MiB, K=2, 16 KiB chunks, LINK fault on
+    (1 -> 2, ch 0) at t=1, j=3, b=8 KiB."""
+    f = dict(kind="LINK", src_rank=1, channel=0, step=1, chunk=3, byte_offset=8192, poison=1)
+    comm, xs, rc, out, g = faulted(4, 2, 1, 262144, dtype, [f], strategy, chunk=16384)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, dtype)
+    ev = [norm_event(e) for e in comm.events()]
+    want = [norm_event(e) for e in oracle_of(xs, g, dtype, [f], strategy).events]
+    assert ev == want
+    assert ev[0]["resume"] == 11 and ev[0]["retransmit"] == 37 and ev[0]["verdict"] == "LINK"
+    assert comm.events()[0]["failover_ms"] > 0
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+@pytest.mark.parametrize("W", [1, 3])
+@pytest.mark.parametrize("dtype", ["bfloat16", "int32"])
+def test_link_fault_events_exact(strategy, W, dtype):
+    n, K, N = 4, 4, 400_000
+    f = dict(kind="LINK", src_rank=2, channel=1, step=2, chunk=1, byte_offset=5000, poison=1)
+    comm, xs, rc, out, g = faulted(n, K, W, N, dtype, [f], strategy, chunk=16384)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, dtype)
+    res = oracle_of(xs, g, dtype, [f], strategy)
+    assert [norm_event(e) for e in comm.events()] == [norm_event(e) for e in res.events]
+    st = comm.status()
+    assert np.array_equal(np.array(st["bytes"])[:, :K], res.bytes_sent)
+
+
+@pytest.mark.parametrize("kind", ["LOCAL", "REMOTE"])
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_endpoint_faults(kind, strategy):
+    n, K, N = 4, 3, 300_000
+    f = dict(kind=kind, src_rank=1, channel=2, step=1, chunk=0, byte_offset=16 * 100, poison=1)
+    comm, xs, rc, out, g = faulted(n, K, 2, N, "bfloat16", [f], strategy, chunk=8192)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "bfloat16")
+    evs = comm.events()
+    prim = [e for e in evs if e["rank"] == 1 and e["origin"] == 2]
+    assert len(prim) == 1
+    want = "LOCAL_ENDPOINT" if kind == "LOCAL" else "REMOTE_ENDPOINT"
+    assert prim[0]["verdict"] == want and prim[0]["resume"] == 1 * g.m + 0
+    st = comm.status()
+    dead_rank = 1 if kind == "LOCAL" else 2
+    assert (dead_rank, 2) in st["dead_endpoints"]
+    # both ring connections through the dead endpoint were re-placed (C-14)
+    assert {e["rank"] for e in evs} == {dead_rank - 1, dead_rank}
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_successive_failover(strategy):
+    """Config 4: a second fault on the adopting backup mid-retransmit."""
+    n, K, N = 4, 4, 400_000
+    f1 = dict(kind="LINK", src_rank=3, channel=1, step=1, chunk=2, byte_offset=4096)
+    f2 = dict(kind="LINK", src_rank=3, channel=2, step=3, chunk=1, byte_offset=0, origin_channel=1)
+    comm, xs, rc, out, g = faulted(n, K, 2, N, "bfloat16", [f1, f2], strategy, chunk=8192)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "bfloat16")
+    res = oracle_of(xs, g, "bfloat16", [f1, f2], strategy)
+    assert len(res.fired) == 2
+    got = sorted((norm_event(e) for e in comm.events()), key=lambda e: (e["stopped_channel"], e["origin"]))
+    want = sorted((norm_event(e) for e in res.events), key=lambda e: (e["stopped_channel"], e["origin"]))
+    assert got == want
+
+
+def test_no_backup_releases_stream():
+    n, K, N = 3, 2, 100_000
+    f1 = dict(kind="LINK", src_rank=1, channel=0, step=1, chunk=0, byte_offset=0)
+    f2 = dict(kind="LINK", src_rank=1, channel=1, step=2, chunk=0, byte_offset=0, origin_channel=0)
+    comm, xs, rc, out, g = faulted(n, K, 1, N, "int32", [f1, f2], "HOT_REPAIR", chunk=8192)
+    assert rc == R.ERR_NO_BACKUP
+    assert comm.status()["last_error"] == R.ERR_NO_BACKUP
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_degraded_static_plan_and_repair(strategy):
+    """Later calls run a plan-time placement around the dead channel;
+    REPAIR re-admits it."""
+    n, K, N = 4, 4, 500_000
+    f = dict(kind="LINK", src_rank=0, channel=3, step=0, chunk=0, byte_offset=0)
+    comm, xs, rc, out, g = faulted(n, K, 2, N, "float32", [f], strategy, chunk=16384)
+    assert rc == R.SUCCESS
+    b0 = np.array(comm.status()["bytes"])[:, :K]
+    xs2 = r2inputs.inputs(n, N, "float32", seed=42)
+    rc, out = run(comm, xs2, "float32")
+    assert rc == R.SUCCESS
+    check_result(out, xs2, g, "float32")
+    b1 = np.array(comm.status()["bytes"])[:, :K] - b0
+    res = OP.simulate(xs2, g, "float32", strategy=strategy, health={"dead_links": [(0, 3)]}, seed=0)
+    assert np.array_equal(b1, res.bytes_sent)
+    comm.inject_fault(at_seq=comm.status()["seq"] + 1, kind="REPAIR", src_rank=0, channel=3)
+    rc, out = run(comm, xs2, "float32")
+    assert rc == R.SUCCESS and comm.status()["dead_links"] == []
+    check_result(out, xs2, g, "float32")
+
+
+def test_inplace_with_fault_in_fused_step():
+    """A retransmitted final-add chunk must not read an overwritten input."""
+    n, K, N = 4, 2, 200_000
+    f = dict(kind="LINK", src_rank=2, channel=0, step=3, chunk=0, byte_offset=2048)
+    comm, xs, rc, out, g = faulted(n, K, 2, N, "bfloat16", [f], "BALANCE", chunk=8192, inplace=True)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "bfloat16")
+
+
+def test_probe_verdicts():
+    comm = sim_comm(4, 4, 1)
+    v = comm.probe(peer=2, channel=1, rank_local=1)
+    assert v["verdict"] == "NONE" and v["outcomes"] == ("S", "S", "S", "S") and v["aux"] == 0
+    f = dict(kind="LINK", src_rank=1, channel=1, step=0, chunk=0, byte_offset=0)
+    comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(4, 10_000, "int32", seed=1)
+    rc, out = run(comm, xs, "int32")
+    assert rc == R.SUCCESS
+    v = comm.probe(peer=2, channel=1, rank_local=1)
+    assert v["verdict"] == "LINK" and v["outcomes"] == ("T", "T", "S", "S")
+    v = comm.probe(peer=3, channel=1, rank_local=2)
+    assert v["verdict"] == "NONE"
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_brute_force_small(strategy):
+    """Every (rank, channel, q) x kind on n=3, K=3, m=2 (one comm, REPAIR in
+    between): buffers always bit-exact, LINK records exact."""
+    n, K, W = 3, 3, 2
+    comm = sim_comm(n, K, W, chunk_bytes=64, strategy=strategy)
+    N = n * K * 2 * 16   # int32: 4 vectors per chunk -> m = 2
+    xs = r2inputs.inputs(n, N, "int32", seed=123)
+    g = oracle_geom(comm, N, "int32")
+    assert g.m == 2
+    for r in range(n):
+        for c in range(K):
+            for q in range(g.steps * g.m):
+                for kind in ("LINK", "LOCAL", "REMOTE"):
+                    t, j = divmod(q, g.m)
+                    seq = comm.status()["seq"] + 1
+                    f = dict(kind=kind, src_rank=r, channel=c, step=t, chunk=j, byte_offset=16, poison=1)
+                    comm.inject_fault(at_seq=seq, **f)
+                    ne = len(comm.events())
+                    rc, out = run(comm, xs, "int32")
+                    assert rc == R.SUCCESS, f
+                    check_result(out, xs, g, "int32")
+                    if kind == "LINK":
+                        want = [norm_event(e) for e in oracle_of(xs, g, "int32", [f], strategy).events]
+                        assert [norm_event(e) for e in comm.events()[ne:]] == want, f
+                    # re-admit everything before the next case
+                    for rr in range(n):
+                        for cc in range(K):
+                            comm.inject_fault(at_seq=seq + 1, kind="REPAIR", src_rank=rr, channel=cc)
+                    rc, out = run(comm, xs, "int32")
+                    assert rc == R.SUCCESS
