@@ -217,8 +217,8 @@ r2_result_t r2_deregister(r2_comm_t comm, uint64_t reg);
  * `count` elements (P:94 ring ReduceScatter + AllGather).  send == recv
  * (in-place) is allowed.  Both pointers 16-byte aligned.  count == 0 is a
  * no-op; count * elem size <= cfg.max_bytes.  In sim mode (k ranks) send and
- * recv each hold k buffers of count elements back to back and need no
- * registration.  Result (reading C-8): for element i of shard s,
+ * recv each hold k rank buffers of count elements, rank l's starting at byte
+ * l * roundup(count * elem size, 16), and need no registration.  Result (reading C-8): for element i of shard s,
  * y[i] = fold(x_{s+1}[i], ..., x_{s+n-1}[i], x_s[i]) with per-hop rounding
  * (int32 wraps, fp32 RN, bf16 = RNE(fp32 add)); bit-identical with and without
  * faults.  A channel fault mid-collective is recovered inside the call's

@@ -5,6 +5,7 @@
 #include "r2_comm.h"
 
 #include <cuda.h>
+#include <stdlib.h>
 #include <string.h>
 #include <time.h>
 
@@ -47,6 +48,8 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
   L.desc = take(8 * 8);
   L.misc = take(sizeof(MiscDev));
   L.stage = take(L.slot_bytes);
+  L.bits_words = (int)(((size_t)steps * L.m_cap + 31) / 32);
+  L.plan_bits = take((size_t)K * L.bits_words * 4);
   L.total = align_up(off, 4096);
   return L;
 }
@@ -63,6 +66,7 @@ RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
   p.desc = (unsigned long long*)(base + L.desc);
   p.misc = (MiscDev*)(base + L.misc);
   p.stage = base + L.stage;
+  p.plan_bits = (unsigned int*)(base + L.plan_bits);
   return p;
 }
 
@@ -125,6 +129,8 @@ int take_async_error(r2_comm* c) {
 }
 
 }  // namespace
+
+int r2_debug = getenv("R2_DEBUG") ? atoi(getenv("R2_DEBUG")) : 0;
 
 uint64_t r2_now_ns() {
   timespec ts;
@@ -189,7 +195,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     delete c;
     return e;
   };
-  if ((long long)steps * c->lay.m_cap > R2_BITMAP_WORDS * 32) return fail(R2_ERR_INVALID_ARG);
+  (void)steps;
   if (c->n > 1) {
     c->max_coop = r2_max_coop_ctas(c->threads);
     if (c->nlocal * c->K * c->W > c->max_coop) return fail(R2_ERR_INVALID_ARG);
@@ -266,6 +272,23 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   c->plan_seq.assign(c->nlocal, 0);
   c->cur_plan.assign(c->nlocal, {});
   if (cudaStreamCreateWithFlags(&c->mon_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(R2_ERR_CUDA);
+  if (c->n > 1) {
+    // pre-load the kernels (see r2_warmup): a healthy self-probe
+    const RankPtrs& me = c->peers_host[c->first_rank];
+    ProbeParams pp{};
+    pp.target_mailbox = me.mailbox + c->first_rank * c->K;
+    pp.ep_dead = me.ep_dead;
+    pp.link_dead = me.link_dead;
+    pp.prober = pp.target = c->first_rank;
+    pp.channel = 0;
+    pp.n = c->n;
+    pp.K = c->K;
+    pp.token = 0x5eed;
+    pp.timeout_ns = 1000000ull;
+    pp.result = c->probe_res_dev + (r2_comm::kProbeSlots - 1);
+    if (r2_warmup(pp, c->mon_stream) != 0) return fail(R2_ERR_CUDA);
+    c->probe_res_host[r2_comm::kProbeSlots - 1] = -1;
+  }
   if (c->has_oob && c->oob.barrier(c->oob.ctx)) return fail(R2_ERR_BOOTSTRAP);
   if (c->n > 1) c->mon = std::thread(r2_monitor_main, c);
   *out = c;
@@ -352,8 +375,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   r2_geometry_t g;
   r2_result_t e = r2_geometry(count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
   if (e != R2_SUCCESS) return e;
-  if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap || g.steps * g.m > R2_BITMAP_WORDS * 32)
-    return R2_ERR_INVALID_ARG;
+  if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
   const uint32_t seq = (uint32_t)(c->seq + 1);
 
   LaunchParams p;
@@ -378,15 +400,17 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   p.slice = g.slice;
   p.chunk = g.chunk;
   p.slot_bytes = c->lay.slot_bytes;
+  p.bits_words = c->lay.bits_words;
   p.watchdog_ns = (unsigned long long)c->cfg.watchdog_ms * 1000000ull;
   for (int k = 0; k < c->K; ++k) p.weights[k] = c->weights[k];
   p.peers = c->peers_dev;
   p.regtab = c->regtab_dev;
 
   // recv publication (real mode) / rank buffers (sim mode)
+  const size_t stride = align_up(count * E, 16);   // sim mode: 16-B aligned rank rows
   for (int l = 0; l < c->nlocal; ++l) {
-    p.send[l] = (const char*)send + (size_t)l * count * E;
-    p.recv[l] = (char*)recv + (size_t)l * count * E;
+    p.send[l] = (const char*)send + (size_t)l * stride;
+    p.recv[l] = (char*)recv + (size_t)l * stride;
     p.ctrl[l] = c->ctrl_dev[l];
   }
   if (!c->sim) {
@@ -411,6 +435,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
       repairs.push_back({f.src_rank, f.channel});
       continue;
     }
+    if (f.step >= g.steps || f.chunk >= g.m) continue;   // no such item: never fires
     if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
     FaultDev& d = p.faults[p.nfaults++];
     d.rank = f.src_rank;
@@ -490,7 +515,8 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
   const size_t bytes = count * (size_t)elem_bytes(dt);
   if (bytes > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
-  const size_t need = c->cfg.max_bytes * c->nlocal;
+  const size_t stride = align_up(bytes, 16);
+  const size_t need = align_up(c->cfg.max_bytes, 16) * c->nlocal;
   if (!c->host_stage) {
     CK(cudaMalloc(&c->host_stage, need));
     c->host_stage_bytes = need;
@@ -498,12 +524,21 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
     if (e != R2_SUCCESS) return e;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  for (int l = 0; l < c->nlocal; ++l)
-    CK(cudaMemcpyAsync(c->host_stage + l * bytes, (const char*)send + l * bytes, bytes, cudaMemcpyHostToDevice, s));
+  // one contiguous copy each way when the host rows are packed like the stage
+  if (stride == bytes || c->nlocal == 1) {
+    CK(cudaMemcpyAsync(c->host_stage, send, bytes * c->nlocal, cudaMemcpyHostToDevice, s));
+  } else {
+    for (int l = 0; l < c->nlocal; ++l)
+      CK(cudaMemcpyAsync(c->host_stage + l * stride, (const char*)send + l * stride, bytes, cudaMemcpyHostToDevice, s));
+  }
   r2_result_t e = enqueue_allreduce(c, c->host_stage, c->host_stage, count, dt, stream);
   if (e != R2_SUCCESS) return e;
-  for (int l = 0; l < c->nlocal; ++l)
-    CK(cudaMemcpyAsync((char*)recv + l * bytes, c->host_stage + l * bytes, bytes, cudaMemcpyDeviceToHost, s));
+  if (stride == bytes || c->nlocal == 1) {
+    CK(cudaMemcpyAsync(recv, c->host_stage, bytes * c->nlocal, cudaMemcpyDeviceToHost, s));
+  } else {
+    for (int l = 0; l < c->nlocal; ++l)
+      CK(cudaMemcpyAsync((char*)recv + l * stride, c->host_stage + l * stride, bytes, cudaMemcpyDeviceToHost, s));
+  }
   return R2_SUCCESS;
 }
 

@@ -162,6 +162,19 @@ struct r2_comm {
   unsigned int probe_token = 1;
 };
 
+// tracing (R2_DEBUG=1): control-plane events with host timestamps
+#include <stdio.h>
+extern int r2_debug;
+uint64_t r2_now_ns();
+#define R2LOG(...)                                                          \
+  do {                                                                      \
+    if (r2_debug) {                                                         \
+      fprintf(stderr, "[r2 %.6f] ", (double)r2_now_ns() / 1e9);             \
+      fprintf(stderr, __VA_ARGS__);                                         \
+      fputc('\n', stderr);                                                  \
+    }                                                                       \
+  } while (0)
+
 // r2_monitor.cpp
 void r2_monitor_main(r2_comm* comm);
 void r2_send_msg(r2_comm* comm, int dst, Msg m);

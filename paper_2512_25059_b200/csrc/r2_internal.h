@@ -56,18 +56,19 @@ struct RankPtrs {            // one rank's arena as seen from some process
   unsigned long long* desc;
   MiscDev* misc;
   char* stage;
+  unsigned int* plan_bits;   // [K][bits_words] residual bitmaps of the dynamic plan
 };
 
 struct ArenaLayout {
-  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, total;
+  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, plan_bits, total;
   size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
   int m_cap;
+  int bits_words;             // 32-bit words per origin bitmap: ceil(steps * m_cap / 32)
 };
 
 // ------------------------------------------------------------------ control
 struct PlanEntry {           // dynamic re-placement of one origin channel
-  unsigned int origin, mode, assignee, mask;
-  unsigned int bitmap[R2_BITMAP_WORDS];
+  unsigned int origin, mode, assignee, mask;   // residual bitmap: arena plan_bits[origin]
 };
 
 struct CtaRec {
@@ -102,6 +103,7 @@ struct LaunchParams {
   int dtype, elem_bytes, V, inplace, strategy, sim;
   unsigned long long N, Np, shard, slice, chunk;   // elements
   size_t slot_bytes;
+  int bits_words;
   unsigned long long watchdog_ns;
   int nfaults;
   FaultDev faults[R2_MAXF];
@@ -134,6 +136,7 @@ int r2_launch_allreduce(const LaunchParams& p, int nctas, int threads, void* str
 int r2_launch_probe(const ProbeParams& p, void* stream);
 int r2_kernel_smem_bytes();
 int r2_max_coop_ctas(int threads);
+int r2_warmup(const ProbeParams& p, void* stream);
 #ifdef __cplusplus
 }
 #endif

@@ -420,7 +420,9 @@ __device__ int do_item(Cta& k, Shared& sh, int t, int o, int j, unsigned int lo,
       const FaultDev& f = p.faults[i];
       if ((int)f.rank != k.r || (int)f.channel != k.c || f.kind > 2) continue;
       unsigned long long kf = keyof(f.t, f.origin, f.j);
-      if (key > kf) {
+      // own-origin faults: deterministic "dead from k* on" for every lane of
+      // the channel; adopted-item faults fire when (and if) carried
+      if (key > kf && (int)f.origin == k.c) {
         st = ST_STOP;
         sh.cause = STOP_FAULT_TABLE;
       } else if (key == kf) {
@@ -548,7 +550,7 @@ __device__ int run_list(Cta& k, Shared& sh) {
               mode = sh.ent[e].mode;
               mask = sh.ent[e].mask;
               assignee = sh.ent[e].assignee;
-              bm = sh.ent[e].bitmap;
+              bm = k.me.plan_bits + (size_t)o * p.bits_words;
             }
           epoch = sh.seen_epoch;
         } else if (!(p.conn_mask[k.l] >> o & 1u)) {
@@ -573,7 +575,7 @@ __device__ int run_list(Cta& k, Shared& sh) {
         const unsigned long long key = keyof(t, o, j);
         if (own && key < k.own_next_key) continue;
         const int q = t * p.m + j;
-        if (bm && !(bm[q >> 5] >> (q & 31) & 1u)) continue;
+        if (bm && !(ld_relaxed_sys(bm + (q >> 5)) >> (q & 31) & 1u)) continue;
         const unsigned int Vj = (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
         unsigned int lo = 0, hi = Vj, parts = 1;
         if (!own && mode == PLAN_BAL) {
@@ -742,7 +744,8 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   k.own_next_key = 0;
   k.fault_channel = false;
   for (int i = 0; i < p.nfaults; ++i)
-    if ((int)p.faults[i].rank == k.r && (int)p.faults[i].channel == k.c && p.faults[i].kind <= 2)
+    if ((int)p.faults[i].rank == k.r && (int)p.faults[i].channel == k.c && p.faults[i].kind <= 2 &&
+        (int)p.faults[i].origin == k.c)
       k.fault_channel = true;
   if (k.tid == 0) {
     sh.decision = 0;
@@ -826,6 +829,23 @@ int r2_launch_probe(const ProbeParams& p, void* stream) {
 }
 
 int r2_kernel_smem_bytes() { return (int)sizeof(Shared); }
+
+// Load both kernels at init.  With CUDA 12 lazy module loading, the first
+// launch of a not-yet-loaded kernel can wait for the running persistent
+// allreduce kernel -- which itself waits for the probe verdict (deadlock
+// until the watchdog).  A warm-up launch of the probe kernel (self-probe of a
+// healthy mailbox) and an attribute query of the allreduce kernel load them.
+int r2_warmup(const ProbeParams& p, void* stream) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, r2_allreduce_kernel);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncGetAttributes(&a, r2_probe_kernel);
+  if (e != cudaSuccess) return (int)e;
+  r2_probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  return (int)cudaStreamSynchronize((cudaStream_t)stream);
+}
 
 int r2_max_coop_ctas(int threads) {
   int dev = 0, nsm = 0, per = 0;

@@ -73,6 +73,7 @@ void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int 
   pp.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
   pp.result = c->probe_res_dev + idx;
   int rc = r2_launch_probe(pp, c->mon_stream);
+  R2LOG("probe launch %d->%d ch%d slot%d round %08x rc=%d", prober, target, channel, slot, round_id, rc);
   PendingProbe pr{prober, target, channel, slot, l, owner, round_id, seq, c->probe_res_host + idx, idx};
   if (rc != 0) c->probe_res_host[idx] = R2_PROBE_NOT_RUN;
   c->probes.push_back(pr);
@@ -86,6 +87,8 @@ void round_result(r2_comm* c, uint32_t id, int slot, int outcome) {
     for (int s = 0; s < rd.need; ++s)
       if (rd.outcomes[s] < 0) return;
     const int v = r2_triangulate(rd.outcomes, rd.aux >= 0);
+    R2LOG("verdict round %08x seq %u (%d->%d ch%d aux %d) outcomes %d%d%d%d -> %d", rd.id, rd.seq, rd.a, rd.b,
+          rd.channel, rd.aux, rd.outcomes[0], rd.outcomes[1], rd.outcomes[2], rd.outcomes[3], v);
     Msg m{};
     m.type = MSG_VERDICT;
     m.seq = rd.seq;
@@ -157,6 +160,7 @@ bool progress_probes(r2_comm* c) {
     busy = true;
     PendingProbe done = pr;
     c->probes.erase(c->probes.begin() + i);
+    R2LOG("probe result %d->%d ch%d slot%d = %d", done.prober, done.target, done.channel, done.slot, v);
     if (is_local(c, done.round_owner)) {
       round_result(c, done.round_id, done.slot, v);
     } else {
@@ -244,6 +248,7 @@ void on_verdict(r2_comm* c, const Msg& m) {
       auto dk = c->planned.find(std::make_pair(m.seq, -(l * K + k) - 1));
       if (dk != c->planned.end() && !(m.a == r && m.channel == k)) continue;
       c->planned[key] = 1;
+      R2LOG("replan queued seq %u rank %d ch%d (verdict %d from %d)", m.seq, r, k, m.verdict, m.a);
       Replan rp{};
       rp.seq = m.seq;
       rp.l = l;
@@ -323,6 +328,7 @@ bool scan_device_records(r2_comm* c) {
       std::atomic_thread_fence(std::memory_order_acquire);
       c->handled_err[l * K + k] = s;
       busy = true;
+      R2LOG("detect seq %u rank %d ch%d cause %u origin %u q %u", s, r, k, e.cause, e.origin, e.q);
       const uint64_t now = r2_now_ns();
       {
         std::lock_guard<std::mutex> g(c->mu);
@@ -444,6 +450,8 @@ void publish_plan(r2_comm* c, Replan& rp) {
   std::vector<r2_event_t> evs;
   bool nobackup = false;
   const uint64_t now = r2_now_ns();
+  const int bw = c->lay.bits_words;
+  std::vector<unsigned int> bits((size_t)K * bw, 0u);
   for (int o = 0; o < K; ++o) {
     if (!(dead >> o & 1u)) continue;
     PlanEntry pe;
@@ -451,13 +459,14 @@ void publish_plan(r2_comm* c, Replan& rp) {
     pe.origin = o;
     std::vector<uint8_t> comp((size_t)steps * m);
     int nres = 0;
+    unsigned int* bm = bits.data() + (size_t)o * bw;
     for (int t = 0; t < steps; ++t)
       for (int j = 0; j < m; ++j) {
         bool d = done(t, o, j);
         comp[(size_t)t * m + j] = d;
         if (!d) {
           int q = t * m + j;
-          pe.bitmap[q >> 5] |= 1u << (q & 31);
+          bm[q >> 5] |= 1u << (q & 31);
           nres++;
         }
       }
@@ -523,6 +532,10 @@ void publish_plan(r2_comm* c, Replan& rp) {
     return;
   }
   // publish: entries, unfreeze, new epoch (device reloads and acks)
+  // residual bitmaps -> device memory first (read by the CTAs after the epoch)
+  unsigned int* dbits = c->peers_host[l * c->n + r].plan_bits;
+  cudaMemcpyAsync(dbits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, c->mon_stream);
+  cudaStreamSynchronize(c->mon_stream);
   for (size_t i = 0; i < ents.size(); ++i) memcpy((void*)&C->entries[i], &ents[i], sizeof(PlanEntry));
   C->nentries = (unsigned)ents.size();
   C->freeze = 0;
@@ -551,8 +564,9 @@ bool progress_replans(r2_comm* c) {
       const LaunchInfo* li = launch_of(c, rp.seq);
       if (li)
         for (int f = 0; f < li->nfaults; ++f)
-          if ((int)li->faults[f].rank == c->first_rank + l && (int)li->faults[f].channel == rp.channel)
-            fault_channel = true;
+          if ((int)li->faults[f].rank == c->first_rank + l && (int)li->faults[f].channel == rp.channel &&
+              li->faults[f].origin == li->faults[f].channel)
+            fault_channel = true;   // its lanes stop deterministically; never stop_mask it
     }
     ctrl_init_for(c, l, rp.seq);
     if (rp.stage == 0) {
@@ -594,6 +608,7 @@ bool progress_replans(r2_comm* c) {
       rp.stage = 2;
     }
     publish_plan(c, rp);
+    R2LOG("plan published seq %u rank %d ch%d epoch %u", rp.seq, c->first_rank + l, rp.channel, c->epoch[l]);
     busy = true;
     c->replans.erase(c->replans.begin() + i);
   }

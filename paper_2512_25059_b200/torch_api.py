@@ -50,11 +50,25 @@ def register(comm: R.Comm, t: torch.Tensor) -> int:
     return comm.register_multi(t.data_ptr(), t.numel() * t.element_size())
 
 
-def allreduce(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+def _count(comm: R.Comm, t: torch.Tensor, count: int | None) -> int:
+    if not comm.sim:
+        return t.numel() if count is None else count
+    # sim mode: [k, row] with 16-byte aligned rows; count <= row elements
+    if t.dim() != 2 or t.shape[0] != comm.n:
+        raise ValueError(f"sim mode expects a [{comm.n}, row] tensor")
+    row, E = t.shape[1], t.element_size()
+    count = row if count is None else count
+    if (row * E) % 16 or -(-count * E // 16) * 16 != row * E:
+        raise ValueError("sim-mode rows must be roundup(count * elem, 16) bytes long")
+    return count
+
+
+def allreduce(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor | None = None, stream=None,
+              count: int | None = None) -> torch.Tensor:
     """Sum-allreduce send -> recv (in place when recv is None / send).
 
-    Sim mode (one process, k simulated ranks): send/recv hold the k rank
-    buffers back to back (leading dimension k)."""
+    Sim mode (one process, k simulated ranks): send/recv are [k, row]
+    tensors; rank l's buffer is row l (rows 16-byte aligned)."""
     if recv is None:
         recv = send
     if not (send.is_cuda and recv.is_cuda):
@@ -63,15 +77,16 @@ def allreduce(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor | None = None
         raise ValueError("contiguous tensors required")
     if send.dtype != recv.dtype or send.numel() != recv.numel():
         raise ValueError("send/recv must match in dtype and size")
-    count = send.numel() // (comm.n if comm.sim else 1)
+    n = _count(comm, send, count)
     s = stream if stream is not None else torch.cuda.current_stream()
-    comm.allreduce(send.data_ptr(), recv.data_ptr(), count, r2_dtype(send), s.cuda_stream)
+    comm.allreduce(send.data_ptr(), recv.data_ptr(), n, r2_dtype(send), s.cuda_stream)
     return recv
 
 
-def allreduce_host(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None) -> torch.Tensor:
+def allreduce_host(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None,
+                   count: int | None = None) -> torch.Tensor:
     """Host (ideally pinned) tensors: H2D, allreduce, D2H on `stream`."""
-    count = send.numel() // (comm.n if comm.sim else 1)
+    n = _count(comm, send, count)
     s = stream if stream is not None else torch.cuda.current_stream()
-    comm.allreduce_host(send.data_ptr(), recv.data_ptr(), count, r2_dtype(send), s.cuda_stream)
+    comm.allreduce_host(send.data_ptr(), recv.data_ptr(), n, r2_dtype(send), s.cuda_stream)
     return recv

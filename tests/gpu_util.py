@@ -15,8 +15,16 @@ from paper_2512_25059_b200 import torch_api as T
 TD = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
 
 
+def row_len(N: int, dtype: str) -> int:
+    """Sim-mode rank rows are 16-byte aligned: roundup(N, 16 / elem)."""
+    v = 16 // r2inputs.elem_bytes(dtype)
+    return max(-(-N // v) * v, v)
+
+
 def to_dev(arrs: list, dtype: str) -> torch.Tensor:
-    a = np.stack(arrs)
+    N = len(arrs[0])
+    a = np.zeros((len(arrs), row_len(N, dtype)), dtype=arrs[0].dtype)
+    a[:, :N] = np.stack(arrs)
     if dtype == "bfloat16":
         return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).cuda()
     return torch.from_numpy(a.copy()).cuda()
@@ -30,7 +38,7 @@ def to_np(t: torch.Tensor, dtype: str) -> np.ndarray:
 
 
 def poisoned(n: int, N: int, dtype: str) -> torch.Tensor:
-    t = torch.empty((n, N), dtype=TD[dtype], device="cuda")
+    t = torch.empty((n, row_len(N, dtype)), dtype=TD[dtype], device="cuda")
     t.view(torch.uint8).fill_(0xFF)
     return t
 
@@ -53,9 +61,13 @@ def run(comm: R.Comm, xs: list, dtype: str, inplace=False):
     N = len(xs[0])
     send = to_dev(xs, dtype)
     recv = send if inplace else poisoned(n, N, dtype)
-    T.allreduce(comm, send, recv)
+    T.allreduce(comm, send, recv, count=N)
     rc = comm.sync()
-    return rc, to_np(recv, dtype)
+    out = to_np(recv, dtype)
+    # the row padding past N must never be written (out-of-place: still poison)
+    if not inplace and out.shape[1] > N:
+        assert np.all(out[:, N:].view(np.uint8) == 0xFF), "wrote past count"
+    return rc, out[:, :N]
 
 
 def same_bits(a, b) -> bool:
