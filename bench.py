@@ -1,0 +1,452 @@
+"""bench.py -- R²CCL hot path on B200: fault-tolerant ring allreduce.
+
+Workload (BASELINE.json configs[2]): 256 MiB bf16
+per rank, K = 8 channels, 512 KiB chunks.
+  N = 1  (default): 8 simulated ranks on one B200 in one cooperative kernel
+         (the "1 GPU local reduce" configuration; all traffic is HBM).
+  N > 1 (torchrun): one process per GPU, CUDA-IPC peer stores over NVLink 5.
+One step = one allreduce (one kernel launch) over inputs resident in HBM
+(2 GiB touched per step > 126 MB L2: no flush needed).  Metric: aggregate
+bus bandwidth = sum over ranks of 2(n-1)/n * S / t (nccl-tests bus bytes).
+After the timed healthy steps the same run measures the single-failure
+scenario: failover latency, the faulted call, degraded Balance / HotRepair
+steady state against the surviving-bandwidth bound, bit-identity.
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed on the
+host cores on a bounded sample of the same workload, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="r2", choices=["r2", "reference"])
+    ap.add_argument("--bytes", type=int, default=256 * MIB, help="payload per rank")
+    ap.add_argument("--sim-ranks", type=int, default=8)
+    ap.add_argument("--channels", type=int, default=8)
+    ap.add_argument("--ctas", type=int, default=0, help="CTAs per channel (0 = auto)")
+    ap.add_argument("--threads", type=int, default=512)
+    ap.add_argument("--chunk", type=int, default=512 * 1024)
+    ap.add_argument("--no-fault", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            time.sleep(0.06)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.out = ""
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle baseline
+def oracle_rate(k: int, sample_bytes: int, reps: int = 1) -> dict:
+    """Time the CPU oracle (Layer 2 protocol simulator) on k ranks x sample."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import r2inputs
+    from oracle import protocol as OP
+    from oracle.geometry import Geometry, effective_chunk_bytes
+    N = sample_bytes // 2
+    xs = r2inputs.inputs(k, N, "bfloat16", seed=1)
+    g = Geometry(k, 8, N, 2, effective_chunk_bytes(N, k, 8, 2, 512 * 1024, 1))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        OP.simulate(xs, g, "bfloat16", seed=0)
+    t = (time.perf_counter() - t0) / reps
+    agg = k * 2 * (k - 1) / k * sample_bytes / t / 1e9
+    return {"seconds": t, "agg_busbw_GBs": agg}
+
+
+def cpu_info() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ GPU arm
+def fill_inputs(send, seed):
+    import torch
+    g = torch.Generator(device=send.device)
+    g.manual_seed(seed)
+    send.copy_(torch.randn(send.shape, generator=g, device=send.device, dtype=torch.float32).to(send.dtype))
+
+
+def sample_parity(send, recv, k_or_world, shard_elems, rank_rows=True, n_sample=4096, seed=5):
+    """Oracle Layer-1 fold on sampled elements, compared with the GPU result."""
+    import numpy as np
+    import torch
+    from oracle import semantic as OS
+    N = send.shape[-1]
+    rng = np.random.default_rng(seed)
+    idx = np.unique(rng.integers(0, N, size=n_sample))
+    it = torch.from_numpy(idx).to(send.device)
+    xs = send[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
+    got = recv[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
+    bad = 0
+    for col, i in enumerate(idx):
+        owner = int(i) // shard_elems
+        want = OS.ring_fold([xs[r, col:col + 1] for r in range(xs.shape[0])], owner, "bfloat16")[0]
+        bad += int(np.any(got[:, col] != want))
+    return {"n_checked": int(len(idx)), "mismatches": bad}
+
+
+def timed(fn, steps, stream):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms
+
+
+def fault_scenario(make_comm, run_step, healthy_ms, S, n, K, geom_m, strategy, get_result, ref_result,
+                   fault_rank=3, fault_ch=5, t=3, j=4, b=256 * 1024, degraded_steps=20, stream=None,
+                   barrier=lambda: None, reduce_max=lambda x: x, is_root=True):
+    """Config 3: one LINK fault mid-collective, then the degraded steady state."""
+    import torch
+    comm = make_comm(strategy)
+    comm.inject_fault(at_seq=2, kind="LINK", src_rank=fault_rank % n, channel=fault_ch % K, step=min(t, 2 * n - 3),
+                      chunk=min(j, geom_m - 1), byte_offset=b, poison=1)
+    run_step(comm)                       # seq 1: healthy warm-up on this comm
+    torch.cuda.synchronize()
+    barrier()
+    ms_faulted = reduce_max(timed(lambda: run_step(comm), 1, stream))     # seq 2: faulted
+    rc = comm.sync()
+    identical = bool(torch.equal(get_result(), ref_result)) if ref_result is not None else None
+    evs = comm.events()
+    for _ in range(2):
+        run_step(comm)
+    torch.cuda.synchronize()
+    barrier()
+    ms_deg = reduce_max(timed(lambda: run_step(comm), degraded_steps, stream))
+    rc2 = comm.sync()
+    busbw = lambda ms: 2 * (n - 1) / n * S / (ms * 1e-3) / 1e9
+    bound = busbw(healthy_ms) * (K - 1) / K if strategy == "BALANCE" else busbw(healthy_ms) * 0.5
+    out = {"strategy": strategy, "rc_faulted": rc, "rc_degraded": rc2, "bit_identical_to_healthy": identical,
+           "failover_ms": [e["failover_ms"] for e in evs], "events": [
+               {k2: e[k2] for k2 in ("rank", "origin", "verdict", "resume", "floor", "retransmit")} for e in evs],
+           "ms_faulted_call": ms_faulted, "ms_healthy_call": healthy_ms,
+           "extra_ms_faulted": ms_faulted - healthy_ms,
+           "busbw_per_rank_degraded": busbw(ms_deg), "busbw_per_rank_healthy": busbw(healthy_ms),
+           "degraded_over_healthy": healthy_ms / ms_deg,
+           "surviving_bound_busbw": bound, "degraded_over_bound": busbw(ms_deg) / bound,
+           "model": "Balance bound (K-1)/K of healthy; HotRepair model 1/2 (S:742-743)"}
+    comm.finalize()
+    return out
+
+
+def run_sim(a):
+    """N = 1: k simulated ranks on one B200."""
+    import torch
+    from paper_2512_25059_b200 import build as B
+    from paper_2512_25059_b200 import r2ccl as R
+    from paper_2512_25059_b200 import torch_api as T
+    B.build()
+    torch.cuda.set_device(0)
+    k, K, S = a.sim_ranks, a.channels, a.bytes
+    W = a.ctas or max(1, min(4, 148 // (k * K)))
+    count = S // 2
+    mk = lambda strategy: R.Comm(0, 1, 0, None, R.config_default(
+        sim_ranks=k, nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk,
+        max_bytes=S, strategy=strategy))
+    comm = mk("BALANCE")
+    send = torch.empty((k, count), dtype=torch.bfloat16, device="cuda")
+    recv = torch.empty_like(send)
+    fill_inputs(send, 1234)
+    stream = torch.cuda.current_stream()
+    step = lambda c=comm: T.allreduce(c, send, recv)
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    with Clocks(0) as clk:
+        ms = timed(step, a.steps, stream)
+    assert comm.sync() == R.SUCCESS
+    g = R.geometry(count, R.BFLOAT16, k, K, W, a.chunk)
+    res = {"ms": ms, "clocks": clk.summary(), "W": W, "m": g.m}
+    if a.profile:
+        return res, None
+    ref = recv.clone()
+    res["sample_parity"] = sample_parity(send, recv, k, g.shard)
+    if not a.no_e2e:
+        hs = torch.empty((k, count), dtype=torch.bfloat16).pin_memory()
+        hr = torch.empty_like(hs).pin_memory()
+        hs.copy_(send.cpu())
+        e2e_steps = max(3, min(a.steps, 10))
+        T.allreduce_host(comm, hs, hr)
+        comm.sync()
+        ms_e2e = timed(lambda: T.allreduce_host(comm, hs, hr), e2e_steps, stream)
+        res["e2e"] = {"ms": ms_e2e, "h2d": k * S, "d2h": k * S, "steps": e2e_steps,
+                      "equal": bool(torch.equal(hr.cuda(), ref))}
+        del hs, hr
+    comm.finalize()
+    if not a.no_fault:
+        res["fault"] = []
+        for strat in ("BALANCE", "HOT_REPAIR"):
+            res["fault"].append(fault_scenario(mk, lambda c: T.allreduce(c, send, recv), ms, S, k, K, g.m, strat,
+                                               lambda: recv, ref, stream=stream))
+    return res, None
+
+
+def run_multi(a):
+    """N > 1: one process per GPU under torchrun."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_25059_b200 import build as B
+    from paper_2512_25059_b200 import r2ccl as R
+    from paper_2512_25059_b200 import torch_api as T
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    if rank == 0:
+        B.build()
+    dist.init_process_group("gloo")
+    dist.barrier()
+    B.build()
+    K, S = a.channels, a.bytes
+    W = a.ctas or 4
+    count = S // 2
+    mk = lambda strategy: T.comm_from_env(R.config_default(
+        nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+        strategy=strategy))
+    comm = mk("BALANCE")
+    send = torch.empty(count, dtype=torch.bfloat16, device="cuda")
+    recv = torch.empty_like(send)
+    fill_inputs(send, 1234 + rank)
+    T.register(comm, recv)
+    stream = torch.cuda.current_stream()
+    step = lambda c=comm: T.allreduce(c, send, recv)
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    def reduce_max(x):
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    with Clocks(local) as clk:
+        ms = reduce_max(timed(step, a.steps, stream))
+    barrier()
+    assert comm.sync() == R.SUCCESS
+    g = R.geometry(count, R.BFLOAT16, world, K, W, a.chunk)
+    res = {"ms": ms, "clocks": clk.summary(), "W": W, "m": g.m}
+    if a.profile:
+        return res, rank
+    ref = recv.clone()
+    if not a.no_e2e:
+        hs = torch.empty(count, dtype=torch.bfloat16).pin_memory()
+        hr = torch.empty_like(hs).pin_memory()
+        hs.copy_(send.cpu())
+        T.allreduce_host(comm, hs, hr)
+        comm.sync()
+        barrier()
+        e2e_steps = max(3, min(a.steps, 10))
+        ms_e2e = reduce_max(timed(lambda: T.allreduce_host(comm, hs, hr), e2e_steps, stream))
+        res["e2e"] = {"ms": ms_e2e, "h2d": S, "d2h": S, "steps": e2e_steps,
+                      "equal": bool(torch.equal(hr.cuda(), ref))}
+    if not a.no_nccl:
+        os.environ["NCCL_NVLS_ENABLE"] = "0"
+        pg = dist.new_group(backend="nccl")
+        buf = send.clone()
+        for _ in range(3):
+            dist.all_reduce(buf, group=pg)
+        barrier()
+        ms_nccl = reduce_max(timed(lambda: dist.all_reduce(buf, group=pg), a.steps, stream))
+        res["nccl"] = {"ms": ms_nccl, "busbw_per_gpu": 2 * (world - 1) / world * S / (ms_nccl * 1e-3) / 1e9,
+                       "nvls": "disabled (NCCL_NVLS_ENABLE=0; the paper disabled SHARP)",
+                       "version": ".".join(map(str, torch.cuda.nccl.version()))}
+    comm.finalize()
+    if not a.no_fault and world >= 2:
+        res["fault"] = []
+        for strat in ("BALANCE", "HOT_REPAIR"):
+            res["fault"].append(fault_scenario(
+                mk, lambda c: T.allreduce(c, send, recv), ms, S, world, K, g.m, strat, lambda: recv, ref,
+                fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0))
+    return res, rank
+
+
+def report(a, res, n_gpus, n_ranks, mode):
+    P = peaks()
+    S, K = a.bytes, a.channels
+    ms = res["ms"]
+    busbw_rank = 2 * (n_ranks - 1) / n_ranks * S / (ms * 1e-3) / 1e9
+    agg = busbw_rank * n_ranks
+    if mode == "sim":
+        hbm = (5 * n_ranks - 4) * S
+        peak = P.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": hbm / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": hbm / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in P else "fallback 6.65 TB/s",
+                "algorithmic_bytes_per_launch": hbm,
+                "per_unit": "(5k-4) x S HBM bytes per simulated allreduce (SURVEY §8(d)), k=%d" % n_ranks}
+    else:
+        nv = 2 * (n_ranks - 1) / n_ranks * S
+        peak = 770.0
+        roof = {"bound": "nvlink", "achieved": nv / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": nv / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)",
+                "frac_of_nominal_900": nv / (ms * 1e-3) / 1e9 / 900.0,
+                "algorithmic_bytes_per_launch": nv, "per_unit": "2(n-1)/n x S NVLink bytes per GPU"}
+    line = {
+        "metric": "allreduce aggregate bus bandwidth, 256 MiB bf16 per rank, healthy (+1-fault scenario in 'fault')",
+        "value": agg, "unit": "GB/s", "n_gpus": n_gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": ("allreduce %d MiB bf16/rank, %d %s ranks, K=%d channels x W=%d CTAs, %d KiB chunks"
+                                % (S // MIB, n_ranks, "simulated (1 GPU)" if mode == "sim" else "GPU", K, res["W"],
+                                   a.chunk // 1024)),
+                   "bytes_per_rank": S, "ranks": n_ranks, "mode": mode, "channels": K, "ctas_per_channel": res["W"],
+                   "chunks_per_slice": res["m"], "l2": "inputs larger than L2 (no flush)",
+                   "parallelism": f"ring allreduce over {n_ranks} ranks"},
+        "busbw_per_rank": busbw_rank,
+        "roofline": roof,
+        "gpu_launches": a.steps,
+        "clocks": res["clocks"],
+    }
+    if "sample_parity" in res:
+        line["sample_parity"] = res["sample_parity"]
+    if "e2e" in res:
+        e = res["e2e"]
+        line["e2e"] = {"value": 2 * (n_ranks - 1) / n_ranks * S / (e["ms"] * 1e-3) / 1e9 * n_ranks, "unit": "GB/s",
+                       "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"], "ms_per_step": e["ms"],
+                       "result_equal_device_path": e["equal"], "api": "r2_allreduce_host (C ABI, pinned host buffers)"}
+    if "nccl" in res:
+        line["nccl_same_box"] = res["nccl"]
+    if "fault" in res:
+        line["fault"] = res["fault"]
+    return line
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return reference_arm(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        res, rank = run_multi(a)
+        if rank == 0:
+            print(json.dumps(report(a, res, world, world, "multi")), flush=True)
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    res, _ = run_sim(a)
+    line = report(a, res, 1, a.sim_ranks, "sim")
+    if not a.no_cpu and not a.profile:
+        s = 128 * MIB
+        r = oracle_rate(a.sim_ranks, s)
+        line["cpu_baseline"] = {"value": r["agg_busbw_GBs"], "unit": "GB/s", "cores": 1, "kind": "oracle",
+                                "sample": f"{a.sim_ranks} ranks x {s // MIB} MiB bf16 (1/{a.bytes // s} of the "
+                                          f"per-rank payload), oracle/protocol.py Layer 2, fault-free, 1 thread, "
+                                          f"{r['seconds']:.1f} s on {cpu_info()} ({os.cpu_count()} cores on host)"}
+    print(json.dumps(line), flush=True)
+
+
+def reference_arm(a):
+    """The oracle as it stands, timed on the host cores (bounded samples)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    k = a.sim_ranks if int(os.environ.get("WORLD_SIZE", "1")) == 1 else int(os.environ["WORLD_SIZE"])
+    s = 1 * MIB
+    oracle_rate(k, s)    # warm
+    ts = []
+    for _ in range(a.warmup):
+        oracle_rate(k, s)
+    for _ in range(a.steps):
+        ts.append(oracle_rate(k, s)["seconds"])
+    t = sum(ts) / len(ts)
+    v = k * 2 * (k - 1) / k * s / t / 1e9
+    line = {"impl": "reference",
+            "metric": "allreduce aggregate bus bandwidth, 256 MiB bf16 per rank, healthy (+1-fault scenario in 'fault')",
+            "value": v, "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"allreduce bf16, {k} ranks, sample {s // MIB} MiB/rank per step (oracle)"},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{k} ranks x {s // MIB} MiB bf16 per step, oracle/protocol.py Layer 2, "
+                                       f"1 thread on {cpu_info()}"},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,119 @@
+"""Multi-GPU parity worker: one process per GPU under torchrun, the real
+CUDA-IPC / NVLink path of libr2ccl.so.  Every rank draws every rank's seeded
+inputs, runs the allreduce through the C ABI, compares its result bit-exactly
+with the oracle; failover records are gathered to rank 0 and compared with
+the oracle's.  Rank 0 writes a JSON summary to argv[1]."""
+import json
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import r2inputs  # noqa: E402
+from oracle import protocol as OP  # noqa: E402
+from oracle import semantic as OS  # noqa: E402
+from oracle.geometry import Geometry, effective_chunk_bytes  # noqa: E402
+from paper_2512_25059_b200 import r2ccl as R  # noqa: E402
+from paper_2512_25059_b200 import torch_api as T  # noqa: E402
+from tests.gpu_util import norm_event  # noqa: E402
+
+TD = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
+
+
+def dev_tensor(x: np.ndarray, dtype: str) -> torch.Tensor:
+    if dtype == "bfloat16":
+        return torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    return torch.from_numpy(x.copy()).cuda()
+
+
+def host(t: torch.Tensor, dtype: str) -> np.ndarray:
+    t = t.cpu()
+    return t.view(torch.int16).numpy().view(np.uint16) if dtype == "bfloat16" else t.numpy()
+
+
+def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=False, seed=0):
+    xs = r2inputs.inputs(world, N, dtype, seed=seed)
+    send = dev_tensor(xs[rank], dtype)
+    if inplace:
+        recv = send
+    else:
+        recv = torch.empty_like(send)
+        recv.view(torch.uint8).fill_(0xFF)
+    T.register(comm, recv)
+    seq = comm.status()["seq"] + 1
+    for f in faults:
+        comm.inject_fault(at_seq=seq, **f)
+    ne = len(comm.events())
+    T.allreduce(comm, send, recv)
+    rc = comm.sync()
+    E = r2inputs.elem_bytes(dtype)
+    cfg = comm.cfg
+    g = Geometry(world, cfg.nchannels, N, E,
+                 effective_chunk_bytes(N, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel))
+    y = OS.allreduce(xs, g.shard, dtype)
+    ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), y.view(np.uint8))
+    evs = [norm_event(e) for e in comm.events()[ne:]]
+    all_evs = [None] * world
+    dist.all_gather_object(all_evs, evs)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok))
+    out = {"N": N, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc, "ok": all(oks)}
+    if faults:
+        got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, inplace=inplace,
+                          faults=[OP.Fault(f["kind"], f["src_rank"], f["channel"], f["step"], f["chunk"],
+                                           f.get("byte_offset", 0)) for f in faults])
+        want = sorted((norm_event(e) for e in res.events), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        out["events_equal"] = got == want
+        out["events"] = got
+        out["want"] = want
+        fo = [e["failover_ms"] for ev in [comm.events()[ne:]] for e in ev]
+        out["failover_ms_rank"] = fo
+    return out
+
+
+def main():
+    out_path = sys.argv[1]
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    results = []
+    try:
+        for strategy in ("BALANCE", "HOT_REPAIR"):
+            cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=64 * 1024, max_bytes=64 << 20,
+                                   strategy=strategy)
+            comm = T.comm_from_env(cfg)
+            if strategy == "BALANCE":
+                for dtype in ("int32", "float32", "bfloat16"):
+                    for N in (1, 777, 100_003, (1 << 22) + 5):
+                        results.append(case(comm, rank, world, N, dtype, seed=N))
+                results.append(case(comm, rank, world, 300_001, "bfloat16", inplace=True, seed=7))
+            f = dict(kind="LINK", src_rank=world - 1, channel=1, step=max(0, world - 2), chunk=1,
+                     byte_offset=12345, poison=1)
+            results.append(case(comm, rank, world, 1 << 20, "bfloat16", [f], strategy, seed=11))
+            # degraded steady state (channel 1 of rank world-1 now dead): static plan
+            results.append(case(comm, rank, world, 1 << 20, "float32", seed=12))
+            comm.finalize()
+        if world >= 2:
+            cfg = R.config_default(nchannels=3, ctas_per_channel=2, chunk_bytes=32 * 1024, max_bytes=64 << 20)
+            comm = T.comm_from_env(cfg)
+            f = dict(kind="LOCAL", src_rank=0, channel=2, step=1, chunk=0, byte_offset=4096)
+            r = case(comm, rank, world, 500_000, "int32", [f], "BALANCE", seed=13)
+            r.pop("events_equal", None)   # secondary connection's record is timing-dependent
+            results.append(r)
+            comm.finalize()
+    except Exception:
+        traceback.print_exc()
+        results.append({"error": traceback.format_exc()})
+    if rank == 0:
+        with open(out_path, "w") as fh:
+            json.dump(results, fh, indent=1, default=str)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
