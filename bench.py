@@ -34,7 +34,7 @@ MIB = 1 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="r2", choices=["r2", "reference"])
     ap.add_argument("--bytes", type=int, default=256 * MIB, help="payload per rank")
@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--per-step", action="store_true", help="debug: per-step CUDA-event times to stderr")
+    ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling period (ms)")
+    ap.add_argument("--clock-test", action="store_true", help="debug: timing with/without the sampler")
+    ap.add_argument("--recreate", type=int, default=0, help="debug: re-create the comm R times, time each")
     return ap.parse_args()
 
 
@@ -65,28 +69,43 @@ class Clocks:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
-        self.gpu = gpu
+    period_ms = 20
+
+    def __init__(self, gpu):
+        self.gpu = gpu if isinstance(gpu, str) else str(gpu)   # "0" or "0,1,2,3"
         self.p = None
+        self.lines = []
+        self.armed = False
+        self.out = ""
+
+    def _reader(self):
+        for line in self.p.stdout:
+            if self.armed:
+                self.lines.append(line)
 
     def __enter__(self):
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                       "-lms", str(self.period_ms), "-i", self.gpu], stdout=subprocess.PIPE,
                                       stderr=subprocess.DEVNULL, text=True)
+            for _ in range(self.gpu.count(",") + 1):
+                self.p.stdout.readline()  # sampler is live before the timed region starts
+            threading.Thread(target=self._reader, daemon=True).start()
+            self.armed = True
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self.armed = False
+        self.out = "".join(self.lines)
         if self.p:
-            time.sleep(0.06)
             self.p.terminate()
             try:
-                self.out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
-                self.out = ""
+                pass
 
     def summary(self) -> dict:
         sm, mx, reasons = [], None, set()
@@ -162,6 +181,20 @@ def sample_parity(send, recv, k_or_world, shard_elems, rank_rows=True, n_sample=
     return {"n_checked": int(len(idx)), "mismatches": bad}
 
 
+class stdout_to_stderr:
+    """Route fd 1 to fd 2 (library banners must not break the one-line JSON)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def timed(fn, steps, stream):
     import torch
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -175,7 +208,7 @@ def timed(fn, steps, stream):
 
 def fault_scenario(make_comm, run_step, healthy_ms, S, n, K, geom_m, strategy, get_result, ref_result,
                    fault_rank=3, fault_ch=5, t=3, j=4, b=256 * 1024, degraded_steps=20, stream=None,
-                   barrier=lambda: None, reduce_max=lambda x: x, is_root=True):
+                   barrier=lambda: None, reduce_max=lambda x: x, is_root=True, gather=lambda evs: evs):
     """Config 3: one LINK fault mid-collective, then the degraded steady state."""
     import torch
     comm = make_comm(strategy)
@@ -187,7 +220,8 @@ def fault_scenario(make_comm, run_step, healthy_ms, S, n, K, geom_m, strategy, g
     ms_faulted = reduce_max(timed(lambda: run_step(comm), 1, stream))     # seq 2: faulted
     rc = comm.sync()
     identical = bool(torch.equal(get_result(), ref_result)) if ref_result is not None else None
-    evs = comm.events()
+    identical = bool(reduce_max(0.0 if identical else 1.0) == 0.0)
+    evs = gather(comm.events())
     for _ in range(2):
         run_step(comm)
     torch.cuda.synchronize()
@@ -278,16 +312,20 @@ def run_multi(a):
     dist.barrier()
     B.build()
     K, S = a.channels, a.bytes
-    W = a.ctas or 4
+    W = a.ctas or 16          # 8 x 16 = 128 CTAs/GPU: best of the W sweep (profiles/r01_summary.md)
     count = S // 2
-    mk = lambda strategy: T.comm_from_env(R.config_default(
-        nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
-        strategy=strategy))
-    comm = mk("BALANCE")
     send = torch.empty(count, dtype=torch.bfloat16, device="cuda")
     recv = torch.empty_like(send)
     fill_inputs(send, 1234 + rank)
-    T.register(comm, recv)
+
+    def mk(strategy):
+        c = T.comm_from_env(R.config_default(
+            nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+            strategy=strategy))
+        T.register(c, recv)     # collective: recv mapped into every peer
+        return c
+
+    comm = mk("BALANCE")
     stream = torch.cuda.current_stream()
     step = lambda c=comm: T.allreduce(c, send, recv)
 
@@ -300,15 +338,62 @@ def run_multi(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(evs):
+        out = [None] * world
+        dist.all_gather_object(out, evs)
+        return [e for part in out for e in part]
+
     for _ in range(a.warmup):
         step()
     barrier()
-    with Clocks(local) as clk:
-        ms = reduce_max(timed(step, a.steps, stream))
+    if a.per_step:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+        evs[0].record(stream)
+        for i in range(a.steps):
+            step()
+            evs[i + 1].record(stream)
+        evs[-1].synchronize()
+        d = [evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
+        print(f"[rank {rank}] per-step ms: min {min(d):.3f} med {statistics.median(d):.3f} max {max(d):.3f} "
+              f"first10 {[round(x, 3) for x in d[:10]]}", file=sys.stderr, flush=True)
+        barrier()
+    for i in range(a.recreate):
+        c2 = mk("BALANCE")
+        s2 = lambda: T.allreduce(c2, send, recv)
+        for _ in range(3):
+            s2()
+        barrier()
+        t = reduce_max(timed(s2, a.steps, stream))
+        t_again = reduce_max(timed(s2, a.steps, stream))
+        c2.finalize()
+        if rank == 0:
+            print(f"recreate {i}: {t:.3f} / {t_again:.3f} ms/step", file=sys.stderr, flush=True)
+    if a.clock_test:
+        for per in (0, 500, 200, 50, 20, 0):
+            barrier()
+            if per:
+                Clocks.period_ms = per
+                with Clocks(local) as c2:
+                    t = reduce_max(timed(step, a.steps, stream))
+                ns = c2.summary()["samples"]
+            else:
+                t, ns = reduce_max(timed(step, a.steps, stream)), 0
+            if rank == 0:
+                print(f"clock-test period {per} ms: {t:.3f} ms/step, {ns} samples", file=sys.stderr, flush=True)
+        Clocks.period_ms = a.clock_ms
+    # one sampler for all GPUs of the job, live before the barrier that opens
+    # the timed region (per-rank samplers starting inside it perturb the run)
+    clk = Clocks(",".join(str(i) for i in range(world))) if local == 0 else None
+    if clk:
+        clk.__enter__()
+    barrier()
+    ms = reduce_max(timed(step, a.steps, stream))
+    if clk:
+        clk.__exit__(None, None, None)
     barrier()
     assert comm.sync() == R.SUCCESS
     g = R.geometry(count, R.BFLOAT16, world, K, W, a.chunk)
-    res = {"ms": ms, "clocks": clk.summary(), "W": W, "m": g.m}
+    res = {"ms": ms, "clocks": clk.summary() if clk else None, "W": W, "m": g.m}
     if a.profile:
         return res, rank
     ref = recv.clone()
@@ -325,11 +410,12 @@ def run_multi(a):
                       "equal": bool(torch.equal(hr.cuda(), ref))}
     if not a.no_nccl:
         os.environ["NCCL_NVLS_ENABLE"] = "0"
-        pg = dist.new_group(backend="nccl")
-        buf = send.clone()
-        for _ in range(3):
-            dist.all_reduce(buf, group=pg)
-        barrier()
+        with stdout_to_stderr():          # NCCL prints its version banner on stdout
+            pg = dist.new_group(backend="nccl")
+            buf = send.clone()
+            for _ in range(3):
+                dist.all_reduce(buf, group=pg)
+            barrier()
         ms_nccl = reduce_max(timed(lambda: dist.all_reduce(buf, group=pg), a.steps, stream))
         res["nccl"] = {"ms": ms_nccl, "busbw_per_gpu": 2 * (world - 1) / world * S / (ms_nccl * 1e-3) / 1e9,
                        "nvls": "disabled (NCCL_NVLS_ENABLE=0; the paper disabled SHARP)",
@@ -340,7 +426,8 @@ def run_multi(a):
         for strat in ("BALANCE", "HOT_REPAIR"):
             res["fault"].append(fault_scenario(
                 mk, lambda c: T.allreduce(c, send, recv), ms, S, world, K, g.m, strat, lambda: recv, ref,
-                fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0))
+                fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0,
+                gather=gather))
     return res, rank
 
 

@@ -175,6 +175,13 @@ uint64_t r2_now_ns();
     }                                                                       \
   } while (0)
 
+// one load of a CTA record's seq|state word
+inline void rec_ss(const CtaRec& r, uint32_t* seq, uint32_t* state) {
+  unsigned long long v = r.ss;
+  *seq = (uint32_t)(v >> 32);
+  *state = (uint32_t)(v & 0xFFFFFFFFu);
+}
+
 // r2_monitor.cpp
 void r2_monitor_main(r2_comm* comm);
 void r2_send_msg(r2_comm* comm, int dst, Msg m);

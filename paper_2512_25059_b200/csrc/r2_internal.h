@@ -71,11 +71,13 @@ struct PlanEntry {           // dynamic re-placement of one origin channel
   unsigned int origin, mode, assignee, mask;   // residual bitmap: arena plan_bits[origin]
 };
 
-struct CtaRec {
-  volatile unsigned int seq, state, cause, ack_epoch;
-  volatile unsigned int adopt_tag, stop_t, stop_o, stop_j;   // adopt_tag = seq<<8 | epoch
+struct CtaRec {                       // written by one CTA, read by the monitor
+  volatile unsigned long long ss;    // seq << 32 | state   (one store: never torn)
+  volatile unsigned long long ack;   // seq << 32 | acknowledged plan epoch
+  volatile unsigned int cause, adopt_tag, pad0, pad1;        // adopt_tag = seq<<8 | epoch
   volatile unsigned long long t_stop, t_first_adopt;
 };
+#define R2_SS(seq, state) (((unsigned long long)(seq) << 32) | (unsigned long long)(state))
 
 struct ErrRec {              // one per channel: the stop that needs handling
   volatile unsigned int seq, cause, origin, q;

@@ -498,13 +498,17 @@ __device__ int do_item(Cta& k, Shared& sh, int t, int o, int j, unsigned int lo,
 }
 
 // thread 0 writes this CTA's record
-__device__ void post_state(const Cta& k, unsigned int state, unsigned int cause) {
+// (one 64-bit store of seq|state).  Only when the monitor may act on it (a
+// fault is in flight, or a stop) is it ordered after this CTA's completion
+// words with a system fence; the healthy path pays no PCIe round trip.
+__device__ void post_state(const Cta& k, const Shared& sh, unsigned int state, unsigned int cause) {
   CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
-  rec.cause = cause;
-  rec.t_stop = gtimer();
-  __threadfence_system();
-  rec.state = state;
-  __threadfence_system();
+  if (cause) rec.cause = cause;
+  if (sh.alerted || state == CTA_STOPPED) {
+    rec.t_stop = gtimer();
+    __threadfence_system();
+  }
+  rec.ss = R2_SS(k.seq, state);
 }
 
 // all threads: pull the dynamic plan from the control block
@@ -526,9 +530,8 @@ __device__ void load_plan(Cta& k, Shared& sh) {
   }
   __syncthreads();
   if (k.tid == 0) {
-    __threadfence_system();
-    k.ctrl->cta[k.cta_in_rank].ack_epoch = sh.seen_epoch;
-    __threadfence_system();
+    __threadfence_system();   // completion words before the acknowledgement
+    k.ctrl->cta[k.cta_in_rank].ack = R2_SS(k.seq, sh.seen_epoch);
   }
   __syncthreads();
 }
@@ -595,7 +598,7 @@ __device__ int run_list(Cta& k, Shared& sh) {
 __device__ int drain(Cta& k, Shared& sh) {
   const LaunchParams& p = *k.p;
   if (k.tid == 0) {
-    post_state(k, CTA_DRAINING, 0);
+    post_state(k, sh, CTA_DRAINING, 0);
     sh.wait_t0 = 0;
   }
   for (;;) {
@@ -708,7 +711,7 @@ __device__ void cta_main(Cta& k, Shared& sh) {
     }
   }
   if (k.tid == 0) {
-    post_state(k, exit_state, st == ST_OK ? 0u : (unsigned int)sh.cause);
+    post_state(k, sh, exit_state, st == ST_OK ? 0u : (unsigned int)sh.cause);
     const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
     unsigned int v = atomicAdd(&k.me.misc->exited, 1u);
     if (v == per_rank - 1) {
@@ -760,11 +763,8 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     sh.first_adopt = 0;
     sh.wait_t0 = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
-    rec.ack_epoch = 0;
     rec.cause = 0;
-    rec.seq = k.seq;
-    __threadfence_system();
-    rec.state = CTA_RUNNING;
+    rec.ss = R2_SS(k.seq, CTA_RUNNING);
     if (!p.sim && k.cta_in_rank == 0) {
       // publish our recv (registration id, offset) for the upstream rank
       volatile unsigned long long* d = k.me.desc + k.par * 4;

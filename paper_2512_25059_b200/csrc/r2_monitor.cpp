@@ -355,8 +355,10 @@ bool scan_device_records(r2_comm* c) {
     // watchdog expiries -> abort everywhere
     for (int i = 0; i < K * c->W; ++i) {
       CtaRec& rec = C->cta[i];
-      if (rec.cause == STOP_TIMEOUT && rec.seq != 0 && c->timeout_seq[l] != rec.seq) {
-        const uint32_t s = rec.seq;
+      uint32_t rs, rst;
+      rec_ss(rec, &rs, &rst);
+      if (rec.cause == STOP_TIMEOUT && rs != 0 && c->timeout_seq[l] != rs) {
+        const uint32_t s = rs;
         c->timeout_seq[l] = s;   // report once
         record_error(c, R2_ERR_TIMEOUT, s);
         Msg m{};
@@ -376,9 +378,9 @@ bool scan_device_records(r2_comm* c) {
 bool channel_quiesced(r2_comm* c, int l, int k, uint32_t seq) {
   Ctrl* C = c->ctrl_host[l];
   for (int w = 0; w < c->W; ++w) {
-    CtaRec& rec = C->cta[k * c->W + w];
-    if (rec.seq != seq) return false;
-    unsigned st = rec.state;
+    uint32_t s, st;
+    rec_ss(C->cta[k * c->W + w], &s, &st);
+    if (s != seq) return false;
     if (st != CTA_STOPPED && st != CTA_DRAINING && st != CTA_EXITED) return false;
   }
   return true;
@@ -387,8 +389,9 @@ bool channel_quiesced(r2_comm* c, int l, int k, uint32_t seq) {
 bool channel_stopped(r2_comm* c, int l, int k, uint32_t seq) {
   Ctrl* C = c->ctrl_host[l];
   for (int w = 0; w < c->W; ++w) {
-    CtaRec& rec = C->cta[k * c->W + w];
-    if (rec.seq == seq && rec.state == CTA_STOPPED) return true;
+    uint32_t s, st;
+    rec_ss(C->cta[k * c->W + w], &s, &st);
+    if (s == seq && st == CTA_STOPPED) return true;
   }
   return false;
 }
@@ -396,11 +399,11 @@ bool channel_stopped(r2_comm* c, int l, int k, uint32_t seq) {
 bool freeze_acked(r2_comm* c, int l, uint32_t seq, uint32_t epoch) {
   Ctrl* C = c->ctrl_host[l];
   for (int i = 0; i < c->K * c->W; ++i) {
-    CtaRec& rec = C->cta[i];
-    if (rec.seq != seq) continue;                 // not started: sees the freeze first
-    unsigned st = rec.state;
+    uint32_t s, st;
+    rec_ss(C->cta[i], &s, &st);
+    if (s != seq) continue;                       // not started: sees the freeze first
     if (st != CTA_RUNNING && st != CTA_DRAINING) continue;
-    if (rec.ack_epoch != epoch) return false;
+    if (C->cta[i].ack != R2_SS(seq, epoch)) return false;
   }
   return true;
 }
@@ -629,7 +632,9 @@ bool progress_timings(r2_comm* c) {
         unsigned long long t = rec.t_first_adopt;
         if (t && (!best || t < best)) best = t;
       }
-      if (rec.seq == et.seq && rec.state != CTA_EXITED && rec.state != CTA_STOPPED) all_done = false;
+      uint32_t s, st;
+      rec_ss(rec, &s, &st);
+      if (s == et.seq && st != CTA_EXITED && st != CTA_STOPPED) all_done = false;
     }
     std::lock_guard<std::mutex> g(c->mu);
     r2_event_t& ev = c->events[et.event_index];
