@@ -23,6 +23,8 @@ namespace {
 
 int elem_bytes(r2_dtype_t dt) { return dt == R2_BFLOAT16 ? 2 : 4; }
 
+constexpr int kMaxInflight = 16;   // outstanding collectives per communicator
+
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
@@ -50,6 +52,7 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
   L.stage = take(L.slot_bytes);
   L.bits_words = (int)(((size_t)steps * L.m_cap + 31) / 32);
   L.plan_bits = take((size_t)K * L.bits_words * 4);
+  L.health = take((size_t)4 * n * K * 4);
   L.total = align_up(off, 4096);
   return L;
 }
@@ -67,6 +70,7 @@ RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
   p.misc = (MiscDev*)(base + L.misc);
   p.stage = base + L.stage;
   p.plan_bits = (unsigned int*)(base + L.plan_bits);
+  p.health = (unsigned int*)(base + L.health);
   return p;
 }
 
@@ -119,6 +123,35 @@ void close_peer(r2_comm* c, void* p) {
       }
       return;
     }
+}
+
+// Monitor threads of communicators never finalized (e.g. the caller exited on
+// an error) are stopped at process exit, before the CUDA runtime unmaps the
+// host-mapped control blocks they poll.
+std::mutex g_live_mu;
+std::vector<r2_comm*> g_live;
+bool g_atexit_registered = false;
+
+void stop_live_monitors() {
+  std::lock_guard<std::mutex> g(g_live_mu);
+  for (r2_comm* c : g_live) {
+    c->stop.store(true);
+    if (c->mon.joinable()) c->mon.join();
+  }
+  g_live.clear();
+}
+
+void track_live(r2_comm* c, bool add) {
+  std::lock_guard<std::mutex> g(g_live_mu);
+  if (add) {
+    g_live.push_back(c);
+    if (!g_atexit_registered) {
+      std::atexit(stop_live_monitors);
+      g_atexit_registered = true;
+    }
+  } else {
+    g_live.erase(std::remove(g_live.begin(), g_live.end(), c), g_live.end());
+  }
 }
 
 int take_async_error(r2_comm* c) {
@@ -264,8 +297,8 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   if (cudaMemset(c->regtab_dev, 0, sizeof(unsigned long long) * c->regtab_host.size()) != cudaSuccess)
     return fail(R2_ERR_CUDA);
 
-  c->ep_dead.assign((size_t)c->n * c->K, 0);
-  c->link_dead.assign((size_t)c->n * c->K, 0);
+  c->health.assign((size_t)4 * c->n * c->K, 0u);
+  if (cudaStreamCreateWithFlags(&c->health_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(R2_ERR_CUDA);
   c->handled_err.assign((size_t)c->nlocal * c->K, 0);
   c->timeout_seq.assign(c->nlocal, 0);
   c->epoch.assign(c->nlocal, 0);
@@ -290,7 +323,10 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     c->probe_res_host[r2_comm::kProbeSlots - 1] = -1;
   }
   if (c->has_oob && c->oob.barrier(c->oob.ctx)) return fail(R2_ERR_BOOTSTRAP);
-  if (c->n > 1) c->mon = std::thread(r2_monitor_main, c);
+  if (c->n > 1) {
+    c->mon = std::thread(r2_monitor_main, c);
+    track_live(c, true);
+  }
   *out = c;
   return R2_SUCCESS;
 }
@@ -450,19 +486,14 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   }
   {
     std::lock_guard<std::mutex> gl(c->mu);
-    for (auto& rc : repairs) {
-      c->ep_dead[rc.first * c->K + rc.second] = 0;
-      c->link_dead[rc.first * c->K + rc.second] = 0;
-    }
-    for (int l = 0; l < c->nlocal; ++l) {
-      const int r = c->first_rank + l;
-      uint32_t mask = 0;
-      for (int k = 0; k < c->K; ++k)
-        if (r2_conn_ok(c, r, k)) mask |= 1u << k;
-      if (!mask) return R2_ERR_NO_BACKUP;
-      p.conn_mask[l] = mask;
-    }
+    // REPAIR re-admits (rank, channel) from this seq on (seq-indexed: no
+    // ordering against collectives already in flight is needed)
+    for (auto& rc : repairs) r2_declare_repaired(c, rc.first, rc.second, seq);
+    if (!repairs.empty() && r2_push_health(c) != 0) return R2_ERR_CUDA;
+    for (int l = 0; l < c->nlocal; ++l)
+      if (!r2_conn_mask_at(c, c->first_rank + l, seq)) return R2_ERR_NO_BACKUP;   // known exhausted
   }
+  // the emulated fabric heals in stream order
   for (auto& rc : repairs)
     for (int l = 0; l < c->nlocal; ++l) {
       const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
@@ -477,13 +508,25 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   li.V = g.V;
   li.slice = g.slice;
   li.chunk = g.chunk;
-  for (int l = 0; l < c->nlocal; ++l) li.conn_mask[l] = p.conn_mask[l];
   li.nfaults = p.nfaults;
   for (int i = 0; i < p.nfaults; ++i) li.faults[i] = p.faults[i];
   {
     std::lock_guard<std::mutex> gl(c->mu);
     c->launches[seq] = li;
     while (c->launches.size() > 64) c->launches.erase(c->launches.begin());
+  }
+  // bounded run-ahead: a full device launch queue would block the monitor's
+  // probe-kernel launches behind a spinning collective (deadlock until the
+  // watchdog), so at most kMaxInflight collectives are outstanding
+  {
+    const uint64_t t0 = r2_now_ns();
+    for (;;) {
+      uint32_t done = 0xFFFFFFFFu;
+      for (int l = 0; l < c->nlocal; ++l) done = std::min(done, (uint32_t)c->ctrl_host[l]->done_seq);
+      if ((int32_t)(seq - done) <= kMaxInflight) break;
+      if (r2_now_ns() - t0 > (uint64_t)c->cfg.watchdog_ms * 3000000ull) return R2_ERR_TIMEOUT;
+      std::this_thread::yield();
+    }
   }
   c->seq = seq;
   int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W, c->threads, stream);
@@ -600,10 +643,11 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->world = c->n;
     out->nlocal = c->nlocal;
     out->nchannels = c->K;
+    const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {
-        if (c->ep_dead[r * c->K + k]) out->dead_endpoints[r] |= 1u << k;
-        if (c->link_dead[r * c->K + k]) out->dead_links[r] |= 1u << k;
+        if (r2_ep_dead_at(c, r, k, q)) out->dead_endpoints[r] |= 1u << k;
+        if (r2_link_dead_at(c, r, k, q)) out->dead_links[r] |= 1u << k;
       }
   }
   if (c->n > 1) {
@@ -636,6 +680,7 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   cudaSetDevice(c->dev);
   cudaDeviceSynchronize();
   if (c->has_oob) c->oob.barrier(c->oob.ctx);
+  track_live(c, false);
   c->stop.store(true);
   if (c->mon.joinable()) c->mon.join();
   for (auto& rg : c->regs)
@@ -650,6 +695,7 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   if (c->regtab_dev) cudaFree(c->regtab_dev);
   if (c->host_stage) cudaFree(c->host_stage);
   if (c->mon_stream) cudaStreamDestroy(c->mon_stream);
+  if (c->health_stream) cudaStreamDestroy(c->health_stream);
   delete c;
   return R2_SUCCESS;
 }

@@ -51,7 +51,6 @@ struct LaunchInfo {                          // what the monitor needs about a s
   uint32_t seq;
   int m, steps, V;
   unsigned long long slice, chunk;
-  uint32_t conn_mask[R2_MAXL];
   int nfaults;
   FaultDev faults[R2_MAXF];
 };
@@ -130,7 +129,8 @@ struct r2_comm {
 
   // shared with the monitor (mu)
   std::mutex mu;
-  std::vector<uint8_t> ep_dead, link_dead;   // host knowledge [n*K]
+  std::vector<uint32_t> health;              // host knowledge [4][n*K] seq-indexed (r2_internal.h)
+  cudaStream_t health_stream = nullptr;
   std::vector<r2_event_t> events;
   int last_error = R2_SUCCESS;
   uint64_t last_error_seq = 0;
@@ -187,6 +187,12 @@ void r2_monitor_main(r2_comm* comm);
 void r2_send_msg(r2_comm* comm, int dst, Msg m);
 uint64_t r2_now_ns();
 
-// r2_hostlogic.cpp (internal helpers)
+// r2_hostlogic.cpp (internal helpers; health calls need comm->mu held)
 int r2_first_healthy_in_chain(int origin, uint32_t mask, int K);
-bool r2_conn_ok(const r2_comm* comm, int r, int c);
+bool r2_conn_ok_at(const r2_comm* comm, int r, int c, uint32_t q);     // connection r->r+1 on c, seq q
+uint32_t r2_conn_mask_at(const r2_comm* comm, int r, uint32_t q);
+bool r2_ep_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
+bool r2_link_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
+void r2_declare_dead(r2_comm* comm, int kind, int r, int c, uint32_t from_seq);   // kind 0 ep, 1 link
+void r2_declare_repaired(r2_comm* comm, int r, int c, uint32_t at_seq);
+int r2_push_health(r2_comm* comm);                                     // mirror to every local arena

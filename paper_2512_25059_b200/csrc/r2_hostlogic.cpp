@@ -101,10 +101,55 @@ int r2_first_healthy_in_chain(int origin, uint32_t mask, int K) {
   return -1;
 }
 
-bool r2_conn_ok(const r2_comm* comm, int r, int c) {
-  const int n = comm->n, K = comm->K;
-  const int r1 = (r + 1) % n;
-  return !comm->ep_dead[r * K + c] && !comm->ep_dead[r1 * K + c] && !comm->link_dead[r * K + c];
+// ---- seq-indexed health records (the planner's "health status records")
+static inline const uint32_t* hrow(const r2_comm* c, int which) {
+  return c->health.data() + (size_t)which * c->n * c->K;
+}
+
+bool r2_ep_dead_at(const r2_comm* c, int r, int k, uint32_t q) {
+  const int i = r * c->K + k;
+  return r2_dead_at(hrow(c, R2_H_EP_DEAD)[i], hrow(c, R2_H_EP_REP)[i], q);
+}
+
+bool r2_link_dead_at(const r2_comm* c, int r, int k, uint32_t q) {
+  const int i = r * c->K + k;
+  return r2_dead_at(hrow(c, R2_H_LINK_DEAD)[i], hrow(c, R2_H_LINK_REP)[i], q);
+}
+
+bool r2_conn_ok_at(const r2_comm* c, int r, int k, uint32_t q) {
+  const int r1 = (r + 1) % c->n;
+  return !r2_ep_dead_at(c, r, k, q) && !r2_ep_dead_at(c, r1, k, q) && !r2_link_dead_at(c, r, k, q);
+}
+
+uint32_t r2_conn_mask_at(const r2_comm* c, int r, uint32_t q) {
+  uint32_t m = 0;
+  for (int k = 0; k < c->K; ++k)
+    if (r2_conn_ok_at(c, r, k, q)) m |= 1u << k;
+  return m;
+}
+
+void r2_declare_dead(r2_comm* c, int kind, int r, int k, uint32_t from_seq) {
+  const int i = r * c->K + k;
+  uint32_t* d = c->health.data() + (size_t)(kind == 0 ? R2_H_EP_DEAD : R2_H_LINK_DEAD) * c->n * c->K;
+  const bool already = kind == 0 ? r2_ep_dead_at(c, r, k, from_seq) : r2_link_dead_at(c, r, k, from_seq);
+  if (!already) d[i] = from_seq;
+}
+
+void r2_declare_repaired(r2_comm* c, int r, int k, uint32_t at_seq) {
+  const int i = r * c->K + k;
+  const size_t nk = (size_t)c->n * c->K;
+  c->health[R2_H_EP_REP * nk + i] = at_seq;
+  c->health[R2_H_LINK_REP * nk + i] = at_seq;
+}
+
+int r2_push_health(r2_comm* c) {
+  const size_t bytes = c->health.size() * sizeof(uint32_t);
+  for (int l = 0; l < c->nlocal; ++l) {
+    const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
+    if (cudaMemcpyAsync(me.health, c->health.data(), bytes, cudaMemcpyHostToDevice, c->health_stream) != cudaSuccess)
+      return -1;
+  }
+  return cudaStreamSynchronize(c->health_stream) == cudaSuccess ? 0 : -1;
 }
 
 extern "C" const char* r2_strerror(r2_result_t r) {

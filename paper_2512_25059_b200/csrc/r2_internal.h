@@ -32,7 +32,7 @@ enum { R2D_INT32 = 0, R2D_FLOAT32 = 1, R2D_BF16 = 2 };
 enum { CTA_IDLE = 0, CTA_RUNNING = 1, CTA_DRAINING = 2, CTA_STOPPED = 3, CTA_EXITED = 4 };
 // stop causes
 enum { STOP_NONE = 0, STOP_FAULT_FIRED = 1, STOP_FAULT_TABLE = 2, STOP_DEATH = 3, STOP_HOST = 4,
-       STOP_ABORT = 5, STOP_TIMEOUT = 6 };
+       STOP_ABORT = 5, STOP_TIMEOUT = 6, STOP_NOBACKUP = 7 };
 // plan entry modes
 enum { PLAN_NONE = 0, PLAN_HOT = 1, PLAN_BAL = 2 };
 
@@ -57,10 +57,25 @@ struct RankPtrs {            // one rank's arena as seen from some process
   MiscDev* misc;
   char* stage;
   unsigned int* plan_bits;   // [K][bits_words] residual bitmaps of the dynamic plan
+  unsigned int* health;      // [4][n*K] host health records: ep dead/repair seq, link dead/repair seq
 };
 
+// Health records are seq-indexed so that collectives enqueued ahead of a
+// verdict plan consistently: an endpoint/link declared dead while collective
+// q runs is dead from q+1 on; a REPAIR armed for seq s' re-admits it from s'.
+#define R2_H_EP_DEAD 0
+#define R2_H_EP_REP 1
+#define R2_H_LINK_DEAD 2
+#define R2_H_LINK_REP 3
+#ifdef __cplusplus
+inline __host__ __device__ bool r2_dead_at(unsigned int dseq, unsigned int rseq, unsigned int q) {
+  // a REPAIR armed at the seq a death takes effect wins (it was issued later)
+  return dseq != 0 && dseq <= q && !(rseq >= dseq && rseq <= q);
+}
+#endif
+
 struct ArenaLayout {
-  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, plan_bits, total;
+  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, plan_bits, health, total;
   size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
   int m_cap;
   int bits_words;             // 32-bit words per origin bitmap: ceil(steps * m_cap / 32)
@@ -74,7 +89,7 @@ struct PlanEntry {           // dynamic re-placement of one origin channel
 struct CtaRec {                       // written by one CTA, read by the monitor
   volatile unsigned long long ss;    // seq << 32 | state   (one store: never torn)
   volatile unsigned long long ack;   // seq << 32 | acknowledged plan epoch
-  volatile unsigned int cause, adopt_tag, pad0, pad1;        // adopt_tag = seq<<8 | epoch
+  volatile unsigned int cause, adopt_tag, wait_idx, wait_val;  // adopt_tag = seq<<8 | epoch; watchdog diagnostics
   volatile unsigned long long t_stop, t_first_adopt;
 };
 #define R2_SS(seq, state) (((unsigned long long)(seq) << 32) | (unsigned long long)(state))
@@ -86,7 +101,7 @@ struct ErrRec {              // one per channel: the stop that needs handling
 
 struct Ctrl {                // host-mapped, one per local rank
   volatile unsigned int plan_seq, epoch, freeze, abort;
-  volatile unsigned int stop_mask, nentries, pad0, pad1;
+  volatile unsigned int stop_mask, nentries, done_seq, pad1;   // done_seq: last collective finished
   PlanEntry entries[R2_MAXK];
   ErrRec err[R2_MAXK];
   CtaRec cta[R2_MAX_CTAS_PER_RANK];
@@ -110,7 +125,6 @@ struct LaunchParams {
   int nfaults;
   FaultDev faults[R2_MAXF];
   unsigned int weights[R2_MAXK];
-  unsigned int conn_mask[R2_MAXL];       // static plan: usable outgoing channels
   const char* send[R2_MAXL];
   char* recv[R2_MAXL];
   int recv_reg[R2_MAXL];                 // registration id of recv (real mode)

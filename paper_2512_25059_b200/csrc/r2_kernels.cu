@@ -147,6 +147,7 @@ struct Cta {
   int par;
   bool fault_channel;
   bool own_alive;
+  unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
   RankPtrs me, nx;
   Ctrl* ctrl;
   unsigned int total_items;
@@ -306,6 +307,10 @@ __device__ int wait_word(const Cta& k, Shared& sh, const volatile unsigned int* 
       }
       if (watchdog(k, sh)) {
         sh.cause = STOP_TIMEOUT;
+        // diagnostics: which completion word this CTA gave up on
+        CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
+        rec.wait_idx = (unsigned int)(f - k.me.flags);
+        rec.wait_val = *f;
         return ST_TIMEOUT;
       }
     }
@@ -330,6 +335,8 @@ __device__ int resolve_recv_next(const Cta& k, Shared& sh) {
       if (s != ST_OK) return s;
       if (watchdog(k, sh)) {
         sh.cause = STOP_TIMEOUT;
+        k.ctrl->cta[k.cta_in_rank].wait_idx = 0x40000000u;          // diagnostics: recv descriptor
+        k.ctrl->cta[k.cta_in_rank].wait_val = (unsigned int)ld_relaxed_sys64(d);
         return ST_TIMEOUT;
       }
     }
@@ -556,8 +563,8 @@ __device__ int run_list(Cta& k, Shared& sh) {
               bm = k.me.plan_bits + (size_t)o * p.bits_words;
             }
           epoch = sh.seen_epoch;
-        } else if (!(p.conn_mask[k.l] >> o & 1u)) {
-          mask = p.conn_mask[k.l];
+        } else if (!(k.conn_mask >> o & 1u)) {
+          mask = k.conn_mask;
           if (p.strategy == 0) {
             mode = PLAN_HOT;
             assignee = 0xFFFFFFFFu;
@@ -606,11 +613,14 @@ __device__ int drain(Cta& k, Shared& sh) {
       int st = poll_control(k, sh);
       int cand = 0;
       if (st == ST_OK) {
-        cand = ld_relaxed_sys((volatile unsigned int*)&k.me.misc->delivered) >= k.total_items;
+        const unsigned int dl = ld_relaxed_sys((volatile unsigned int*)&k.me.misc->delivered);
+        cand = dl >= k.total_items;
         if (!cand) {
           if (watchdog(k, sh)) {
             st = ST_TIMEOUT;
             sh.cause = STOP_TIMEOUT;
+            k.ctrl->cta[k.cta_in_rank].wait_idx = 0x80000000u | (dl & 0xFFFFFFu);   // drain: delivered
+            k.ctrl->cta[k.cta_in_rank].wait_val = k.total_items;
           } else {
             __nanosleep(200);
           }
@@ -637,7 +647,11 @@ __device__ int drain(Cta& k, Shared& sh) {
     const int expired = sh.flag == -1;
     __syncthreads();
     if (expired) {
-      if (k.tid == 0) sh.cause = STOP_TIMEOUT;
+      if (k.tid == 0) {
+        sh.cause = STOP_TIMEOUT;
+        k.ctrl->cta[k.cta_in_rank].wait_idx = 0xC0000000u;    // drain: final completion words
+        k.ctrl->cta[k.cta_in_rank].wait_val = 0;
+      }
       return ST_TIMEOUT;
     }
   }
@@ -671,10 +685,36 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
   }
 }
 
+// thread 0, once per CTA on the way out.  The last CTA of the rank resets
+// the per-collective counters (nobody reads them any more in this launch)
+// and publishes done_seq for the host's in-flight window.
+__device__ void last_out(const Cta& k) {
+  const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
+  if (atomicAdd(&k.me.misc->exited, 1u) == per_rank - 1) {
+    k.me.misc->delivered = 0;
+    k.me.misc->copy_next = 0;
+    __threadfence();
+    atomicExch(&k.me.misc->exited, 0u);
+    k.ctrl->done_seq = k.seq;
+  }
+}
+
 template <int DT>
 __device__ void cta_main(Cta& k, Shared& sh) {
   int st;
   unsigned int exit_state = CTA_EXITED;
+  if (k.conn_mask == 0) {
+    // every outgoing channel of this rank is dead: the chain is exhausted
+    // before the collective starts -- abort, the monitor reports it
+    if (k.tid == 0) {
+      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
+      k.ctrl->cta[k.cta_in_rank].cause = STOP_NOBACKUP;
+      __threadfence_system();
+      k.ctrl->cta[k.cta_in_rank].ss = R2_SS(k.seq, CTA_EXITED);
+      last_out(k);
+    }
+    return;
+  }
   for (;;) {
     st = run_list<DT>(k, sh);
     if (st == ST_REPLAN) {
@@ -698,7 +738,10 @@ __device__ void cta_main(Cta& k, Shared& sh) {
       st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
     }
     if (st == ST_STOP && sh.cause == STOP_DEATH) {
-      // bilateral awareness starts at the detecting sender
+      // bilateral awareness starts at the detecting sender; the
+      // surviving CTAs of every rank must start reading the control block
+      const LaunchParams& p = *k.p;
+      for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peers[k.l * p.n + q].alert, k.seq);
       ErrRec& e = k.ctrl->err[k.c];
       if (e.seq != k.seq) {
         e.cause = STOP_DEATH;
@@ -712,15 +755,7 @@ __device__ void cta_main(Cta& k, Shared& sh) {
   }
   if (k.tid == 0) {
     post_state(k, sh, exit_state, st == ST_OK ? 0u : (unsigned int)sh.cause);
-    const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
-    unsigned int v = atomicAdd(&k.me.misc->exited, 1u);
-    if (v == per_rank - 1) {
-      // last CTA of this rank: nobody reads these any more in this launch
-      k.me.misc->delivered = 0;
-      k.me.misc->copy_next = 0;
-      __threadfence();
-      atomicExch(&k.me.misc->exited, 0u);
-    }
+    last_out(k);
   }
 }
 
@@ -743,7 +778,23 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   k.nx = p.peers[k.l * p.n + k.r1];
   k.ctrl = p.ctrl[k.l];
   k.total_items = (unsigned int)(p.steps * p.K * p.m);
-  k.own_alive = (p.conn_mask[k.l] >> k.c) & 1u;
+  // plan-time placement: read the host's health records for this seq;
+  // every CTA of the rank computes the same mask (records for this seq are
+  // never rewritten while it runs, see r2_internal.h)
+  {
+    const unsigned int nk = (unsigned int)(p.n * p.K);
+    const unsigned int* h = k.me.health;
+    unsigned int mask = 0;
+    for (int c = 0; c < p.K; ++c) {
+      const unsigned int a = k.r * p.K + c, b = k.r1 * p.K + c;
+      bool dead = r2_dead_at(h[R2_H_EP_DEAD * nk + a], h[R2_H_EP_REP * nk + a], k.seq) ||
+                  r2_dead_at(h[R2_H_EP_DEAD * nk + b], h[R2_H_EP_REP * nk + b], k.seq) ||
+                  r2_dead_at(h[R2_H_LINK_DEAD * nk + a], h[R2_H_LINK_REP * nk + a], k.seq);
+      if (!dead) mask |= 1u << c;
+    }
+    k.conn_mask = mask;
+  }
+  k.own_alive = (k.conn_mask >> k.c) & 1u;
   k.own_next_key = 0;
   k.fault_channel = false;
   for (int i = 0; i < p.nfaults; ++i)

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <chrono>
 #include <thread>
+#include <tuple>
 
 #include "r2_comm.h"
 
@@ -232,16 +233,22 @@ void on_verdict(r2_comm* c, const Msg& m) {
   vd.channel = m.channel;
   for (int s = 0; s < 4; ++s) vd.outcome[s] = m.outcomes[s];
   std::lock_guard<std::mutex> g(c->mu);
-  for (int e : kill_ep) c->ep_dead[e * K + m.channel] = 1;
-  if (kill_link && m.b == (m.a + 1) % n) c->link_dead[m.a * K + m.channel] = 1;
+  // health records: dead from the next collective on (the running one, if
+  // any, is re-placed dynamically below); mirrored to device memory before
+  // any plan of the running collective is published, so the next kernel
+  // plans around the dead channel from its first chunk
+  const uint32_t from = (m.seq ? m.seq : (uint32_t)c->seq) + 1;
+  for (int e : kill_ep) r2_declare_dead(c, 0, e, m.channel, from);
+  if (kill_link && m.b == (m.a + 1) % n) r2_declare_dead(c, 1, m.a, m.channel, from);
+  r2_push_health(c);
   if (m.seq == 0) return;
   const LaunchInfo* li = launch_of(c, m.seq);
   if (!li) return;
   for (int l = 0; l < c->nlocal; ++l) {
     const int r = c->first_rank + l;
     for (int k = 0; k < K; ++k) {
-      if (!(li->conn_mask[l] >> k & 1u)) continue;       // statically adopted already
-      if (r2_conn_ok(c, r, k)) continue;
+      if (!r2_conn_ok_at(c, r, k, m.seq)) continue;       // statically adopted already
+      if (r2_conn_ok_at(c, r, k, m.seq + 1)) continue;   // not condemned
       auto key = std::make_pair(m.seq, l * K + k);
       if (c->planned.count(key)) continue;
       // a connection this rank detected itself waits for its own round
@@ -357,14 +364,38 @@ bool scan_device_records(r2_comm* c) {
       CtaRec& rec = C->cta[i];
       uint32_t rs, rst;
       rec_ss(rec, &rs, &rst);
-      if (rec.cause == STOP_TIMEOUT && rs != 0 && c->timeout_seq[l] != rs) {
+      const unsigned cause = rec.cause;
+      if ((cause == STOP_TIMEOUT || cause == STOP_NOBACKUP) && rs != 0 && c->timeout_seq[l] != rs) {
         const uint32_t s = rs;
+        const int err = cause == STOP_TIMEOUT ? R2_ERR_TIMEOUT : R2_ERR_NO_BACKUP;
         c->timeout_seq[l] = s;   // report once
-        record_error(c, R2_ERR_TIMEOUT, s);
+        record_error(c, err, s);
+        if (r2_debug) {
+          std::map<std::tuple<uint32_t, uint32_t, uint32_t>, int> hist;
+          std::string line, tos;
+          char buf[160];
+          for (int j = 0; j < K * c->W; ++j) {
+            uint32_t s2, st2;
+            rec_ss(C->cta[j], &s2, &st2);
+            hist[std::make_tuple(s2, st2, (uint32_t)C->cta[j].cause)]++;
+            if (C->cta[j].cause == STOP_TIMEOUT) {
+              snprintf(buf, sizeof(buf), " [cta %d ch%d lane%d seq %u wait %08x val %u]", j, j / c->W, j % c->W, s2,
+                       (unsigned)C->cta[j].wait_idx, (unsigned)C->cta[j].wait_val);
+              tos += buf;
+            }
+          }
+          for (auto& h : hist) {
+            snprintf(buf, sizeof(buf), " %d@(seq %u st %u cause %u)", h.second, std::get<0>(h.first),
+                     std::get<1>(h.first), std::get<2>(h.first));
+            line += buf;
+          }
+          R2LOG("TIMEOUT rank %d done_seq %u ctas:%s timed-out:%s", r, (unsigned)C->done_seq, line.c_str(),
+                tos.c_str());
+        }
         Msg m{};
         m.type = MSG_ABORT;
         m.seq = s;
-        m.error = R2_ERR_TIMEOUT;
+        m.error = err;
         broadcast(c, m);
         busy = true;
         break;
@@ -429,13 +460,15 @@ void publish_plan(r2_comm* c, Replan& rp) {
   // healthy: assignable channels; dead: origins re-placed now (statically
   // dead, or known dead AND quiesced -- a known-dead channel whose CTAs are
   // still draining items below its fault point waits for its own re-plan)
-  uint32_t healthy = 0, dead = 0;
+  uint32_t healthy = 0, dead = 0, static_mask = 0;
   {
     std::lock_guard<std::mutex> g(c->mu);
+    static_mask = r2_conn_mask_at(c, r, rp.seq);          // what the kernel planned with
     for (int k = 0; k < K; ++k) {
-      const bool known_ok = r2_conn_ok(c, r, k) && (li.conn_mask[l] >> k & 1u);
+      const bool stat_ok = static_mask >> k & 1u;
+      const bool known_ok = stat_ok && r2_conn_ok_at(c, r, k, rp.seq + 1);
       if (known_ok && !channel_stopped(c, l, k, rp.seq)) healthy |= 1u << k;
-      if (!(li.conn_mask[l] >> k & 1u) || (!known_ok && channel_quiesced(c, l, k, rp.seq))) dead |= 1u << k;
+      if (!stat_ok || (!known_ok && channel_quiesced(c, l, k, rp.seq))) dead |= 1u << k;
     }
   }
   // what did the stopped channel carry under the previous plan?
@@ -445,9 +478,9 @@ void publish_plan(r2_comm* c, Replan& rp) {
         if ((int)e.origin == o) return (e.mode == PLAN_HOT) ? (int)e.assignee == k : (e.mask >> k & 1u);
       return false;
     }
-    if (li.conn_mask[l] >> o & 1u) return false;
-    if (c->cfg.strategy == R2_HOT_REPAIR) return r2_first_healthy_in_chain(o, li.conn_mask[l], K) == k;
-    return li.conn_mask[l] >> k & 1u;
+    if (static_mask >> o & 1u) return false;
+    if (c->cfg.strategy == R2_HOT_REPAIR) return r2_first_healthy_in_chain(o, static_mask, K) == k;
+    return static_mask >> k & 1u;
   };
   std::vector<PlanEntry> ents;
   std::vector<r2_event_t> evs;
@@ -585,9 +618,8 @@ bool progress_replans(r2_comm* c) {
       bool need_freeze = c->epoch[l] > 0;
       {
         std::lock_guard<std::mutex> g(c->mu);
-        const LaunchInfo* li = launch_of(c, rp.seq);
         const uint32_t full = (c->K >= 32) ? 0xFFFFFFFFu : ((1u << c->K) - 1u);
-        if (li && li->conn_mask[l] != full) need_freeze = true;
+        if (r2_conn_mask_at(c, c->first_rank + l, rp.seq) != full) need_freeze = true;   // static adoption
       }
       if (need_freeze) {
         C->freeze = 1;
