@@ -130,6 +130,8 @@ struct r2_comm {
   // shared with the monitor (mu)
   std::mutex mu;
   std::vector<uint32_t> health;              // host knowledge [4][n*K] seq-indexed (r2_internal.h)
+  struct RepairRec { int r, c; uint32_t seq; };
+  std::vector<RepairRec> repairs_applied;    // REPAIRs already enqueued (closing later deaths)
   cudaStream_t health_stream = nullptr;
   std::vector<r2_event_t> events;
   int last_error = R2_SUCCESS;

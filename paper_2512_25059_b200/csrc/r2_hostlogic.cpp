@@ -128,18 +128,36 @@ uint32_t r2_conn_mask_at(const r2_comm* c, int r, uint32_t q) {
   return m;
 }
 
+// A death opens a new interval from `from_seq` (a collective that has not
+// started on any rank whose plan depends on this record, see on_verdict).
 void r2_declare_dead(r2_comm* c, int kind, int r, int k, uint32_t from_seq) {
   const int i = r * c->K + k;
-  uint32_t* d = c->health.data() + (size_t)(kind == 0 ? R2_H_EP_DEAD : R2_H_LINK_DEAD) * c->n * c->K;
-  const bool already = kind == 0 ? r2_ep_dead_at(c, r, k, from_seq) : r2_link_dead_at(c, r, k, from_seq);
-  if (!already) d[i] = from_seq;
+  const size_t nk = (size_t)c->n * c->K;
+  uint32_t& d = c->health[(kind == 0 ? R2_H_EP_DEAD : R2_H_LINK_DEAD) * nk + i];
+  uint32_t& rs = c->health[(kind == 0 ? R2_H_EP_REP : R2_H_LINK_REP) * nk + i];
+  if (r2_dead_at(d, rs, from_seq)) return;          // already dead then
+  d = from_seq;
+  // a REPAIR already enqueued for a later collective closes this interval
+  uint32_t best = 0;
+  for (const auto& rp : c->repairs_applied)
+    if (rp.r == r && rp.c == k && rp.seq >= from_seq && (!best || rp.seq < best)) best = rp.seq;
+  rs = best;
 }
 
+// A record may only change in ways that leave the view of every collective
+// before `at_seq` untouched (kernels in flight read it): a REPAIR only closes
+// an open death interval (dead since d <= at_seq, not yet repaired); an
+// already repaired or never-dead record keeps its values.
 void r2_declare_repaired(r2_comm* c, int r, int k, uint32_t at_seq) {
   const int i = r * c->K + k;
   const size_t nk = (size_t)c->n * c->K;
-  c->health[R2_H_EP_REP * nk + i] = at_seq;
-  c->health[R2_H_LINK_REP * nk + i] = at_seq;
+  c->repairs_applied.push_back({r, k, at_seq});
+  if (c->repairs_applied.size() > 4096) c->repairs_applied.erase(c->repairs_applied.begin());
+  for (int pair = 0; pair < 2; ++pair) {
+    uint32_t& d = c->health[(pair ? R2_H_LINK_DEAD : R2_H_EP_DEAD) * nk + i];
+    uint32_t& rs = c->health[(pair ? R2_H_LINK_REP : R2_H_EP_REP) * nk + i];
+    if (d != 0 && rs < d && at_seq >= d) rs = at_seq;
+  }
 }
 
 int r2_push_health(r2_comm* c) {

@@ -237,6 +237,34 @@ def test_inplace_with_fault_in_fused_step():
     check_result(out, xs, g, "bfloat16")
 
 
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_periodic_faults_back_to_back(strategy):
+    """Config-5 pattern in miniature: collectives enqueued back to back (no
+    sync), a LINK fault every 12 calls, REPAIR of every (rank, channel) re-armed
+    6 calls later while earlier collectives are still in flight.  Every result
+    bit-exact; health records never change under a running kernel."""
+    n, K, N, calls = 4, 4, 60_000, 72
+    comm = sim_comm(n, K, 2, chunk_bytes=16384, strategy=strategy)
+    pool = [r2inputs.inputs(n, N, "bfloat16", seed=s) for s in range(3)]
+    g = oracle_geom(comm, N, "bfloat16")
+    sends = [to_dev(x, "bfloat16") for x in pool]
+    recvs = [poisoned(n, N, "bfloat16") for _ in range(calls)]
+    rng = np.random.default_rng(17)
+    for f in range(calls // 12):
+        s = 1 + 12 * f
+        comm.inject_fault(at_seq=s, kind="LINK", src_rank=int(rng.integers(n)), channel=int(rng.integers(K)),
+                          step=int(rng.integers(g.steps)), chunk=int(rng.integers(g.m)), byte_offset=32)
+        for r in range(n):
+            for c in range(K):
+                comm.inject_fault(at_seq=s + 6, kind="REPAIR", src_rank=r, channel=c)
+    for i in range(calls):
+        T.allreduce(comm, sends[i % 3], recvs[i], count=N)
+    assert comm.sync() == R.SUCCESS
+    for i in range(calls):
+        check_result(to_np(recvs[i], "bfloat16")[:, :N], pool[i % 3], g, "bfloat16")
+    assert len({e["seq"] for e in comm.events()}) == calls // 12
+
+
 def test_probe_verdicts():
     comm = sim_comm(4, 4, 1)
     v = comm.probe(peer=2, channel=1, rank_local=1)
