@@ -197,7 +197,8 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   if (world < 1 || rank < 0 || rank >= world) return R2_ERR_INVALID_ARG;
   if (cfg.nchannels < 1 || cfg.nchannels > R2_MAXK || cfg.ctas_per_channel < 1 || cfg.ctas_per_channel > R2_MAXW)
     return R2_ERR_INVALID_ARG;
-  if (cfg.threads_per_cta < 32 || cfg.threads_per_cta > 512 || cfg.threads_per_cta % 32) return R2_ERR_INVALID_ARG;
+  // warp 0 controls, warps 1.. move data: at least 2 warps per CTA
+  if (cfg.threads_per_cta < 64 || cfg.threads_per_cta > 512 || cfg.threads_per_cta % 32) return R2_ERR_INVALID_ARG;
   if (cfg.chunk_bytes < 16 || cfg.chunk_bytes % 16 || cfg.max_bytes < 16) return R2_ERR_INVALID_ARG;
   if (cfg.strategy != R2_HOT_REPAIR && cfg.strategy != R2_BALANCE) return R2_ERR_INVALID_ARG;
   if (cfg.sim_ranks < 1 || cfg.sim_ranks > R2_MAXL || (world > 1 && cfg.sim_ranks != 1)) return R2_ERR_INVALID_ARG;

@@ -119,14 +119,70 @@ __device__ __forceinline__ void st_user(char* p, uint4 v, int valid, int E) {
 }
 
 enum { MODE_RS = 0, MODE_FUSED = 1, MODE_AG = 2 };
-enum { ST_OK = 0, ST_STOP = 1, ST_REPLAN = 2, ST_ABORT = 3, ST_TIMEOUT = 4 };
+enum { ST_OK = 0, ST_STOP = 1, ST_REPLAN = 2, ST_ABORT = 3, ST_TIMEOUT = 4, ST_NOTREADY = 5 };
+
+// ---------------------------------------------------------- mbarrier (PTX)
+__device__ __forceinline__ unsigned int smem_u32(const void* p) {
+  return static_cast<unsigned int>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(unsigned long long* b, unsigned int parity) {
+  unsigned int ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned int parity) {
+  unsigned int ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+
+// Warp-specialized pipeline: warp 0 (control) publishes chunk descriptors into
+// a ring of NSLOT shared-memory slots, the other warps move the data; each
+// slot has a `full` (control -> data) and an `empty` (data -> control)
+// mbarrier.  The control warp retires finished chunks in order with ONE
+// fence.acq_rel.sys for all chunks finished since its last retire.
+#define NSLOT 4
+enum { SLOT_GO = 0, SLOT_END = 1 };
+enum { META_ITEM = 0, META_FIRE = 1, META_END = 2 };
+
+struct Slot {                 // read by the data warps
+  int status;
+  int poison;
+  unsigned int nvec, total;   // vectors to move / vectors of the part (poison tail)
+  const char* src;
+  const char* s_in;
+  char* d_rem;
+  char* d_loc;
+  int rem_user, loc_user, rs;
+  unsigned long long e0;
+};
+
+struct Meta {                 // read by the control warp at retirement
+  int kind;
+  int t, o, j;
+  unsigned int parts, epoch, nbytes;
+  int own, fault;
+};
 
 struct Shared {
   int decision;
   int cause;
-  int fire;
-  unsigned int fire_nvec;
-  int poison;
+  int pipe_status;
   unsigned int seen_epoch;
   int dynamic;
   int freeze;
@@ -134,9 +190,14 @@ struct Shared {
   int alerted;
   int flag;
   unsigned int piece;
+  unsigned int pub, fin;      // control: slots published / retired (monotone across pipeline runs)
   char* recv_next;
   unsigned long long first_adopt;
   unsigned long long wait_t0;
+  unsigned long long full[NSLOT];
+  unsigned long long empty[NSLOT];
+  Slot slot[NSLOT];
+  Meta meta[NSLOT];
   PlanEntry ent[R2_MAXK];
 };
 
@@ -203,14 +264,14 @@ __device__ void bal_part(unsigned int V, unsigned int mask, const unsigned int* 
 //   d_rem  : peer scratch (RS, full vectors) or peer recv (fused/AG, masked)
 //   d_loc  : fused only: own stage (in-place, full) or own recv (masked)
 template <int DT>
-__device__ void move(const Cta& k, const char* src, const char* s_in, char* d_rem, bool rem_user, char* d_loc,
-                     bool loc_user, unsigned long long e0, unsigned int nvec) {
-  const LaunchParams& p = *k.p;
+__device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr, const char* src, const char* s_in,
+                     char* d_rem, bool rem_user, char* d_loc, bool loc_user, unsigned long long e0,
+                     unsigned int nvec) {
   const int E = p.elem_bytes, V = p.V;
-  const unsigned int stride = k.nthr;
+  const unsigned int stride = nthr;
   if (e0 + (unsigned long long)nvec * V <= p.N) {
     // fast path: every vector is inside the user buffer
-    unsigned int v = k.tid;
+    unsigned int v = tid;
     for (; v + 3 * stride < nvec; v += 4 * stride) {
       uint4 a[4];
 #pragma unroll
@@ -238,7 +299,7 @@ __device__ void move(const Cta& k, const char* src, const char* s_in, char* d_re
     return;
   }
   // tail path: vectors straddling / beyond N
-  for (unsigned int v = k.tid; v < nvec; v += stride) {
+  for (unsigned int v = tid; v < nvec; v += stride) {
     long long ev = (long long)(e0 + (unsigned long long)v * V);
     long long left = (long long)p.N - ev;
     int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
@@ -293,58 +354,21 @@ __device__ __forceinline__ bool watchdog(const Cta& k, Shared& sh) {
   return now - sh.wait_t0 > k.p->watchdog_ns;
 }
 
-// thread 0: wait until *f >= seq with periodic control polls
-__device__ int wait_word(const Cta& k, Shared& sh, const volatile unsigned int* f, bool check_death) {
-  sh.wait_t0 = 0;
-  unsigned int it = 0;
-  while ((int)(ld_acquire_sys(f) - k.seq) < 0) {
-    if ((++it & 31u) == 0) {
-      int s = poll_control(k, sh);
-      if (s != ST_OK) return s;
-      if (check_death && conn_phys_dead(k)) {
-        sh.cause = STOP_DEATH;
-        return ST_STOP;
-      }
-      if (watchdog(k, sh)) {
-        sh.cause = STOP_TIMEOUT;
-        // diagnostics: which completion word this CTA gave up on
-        CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
-        rec.wait_idx = (unsigned int)(f - k.me.flags);
-        rec.wait_val = *f;
-        return ST_TIMEOUT;
-      }
-    }
-  }
-  return ST_OK;
-}
-
-// thread 0: peer's recv pointer for this seq (real mode: published descriptor)
-__device__ int resolve_recv_next(const Cta& k, Shared& sh) {
+// control lane: peer's recv pointer for this seq, without blocking (real
+// mode: the descriptor the downstream rank publishes at kernel start)
+__device__ bool try_recv_next(const Cta& k, Shared& sh) {
   const LaunchParams& p = *k.p;
-  if (sh.recv_next) return ST_OK;
+  if (sh.recv_next) return true;
   if (p.sim) {
     sh.recv_next = p.recv[k.r1 - p.first_rank];
-    return ST_OK;
+    return true;
   }
   const volatile unsigned long long* d = k.nx.desc + k.par * 4;
-  sh.wait_t0 = 0;
-  unsigned int it = 0;
-  while ((unsigned int)ld_relaxed_sys64(d) != k.seq) {
-    if ((++it & 31u) == 0) {
-      int s = poll_control(k, sh);
-      if (s != ST_OK) return s;
-      if (watchdog(k, sh)) {
-        sh.cause = STOP_TIMEOUT;
-        k.ctrl->cta[k.cta_in_rank].wait_idx = 0x40000000u;          // diagnostics: recv descriptor
-        k.ctrl->cta[k.cta_in_rank].wait_val = (unsigned int)ld_relaxed_sys64(d);
-        return ST_TIMEOUT;
-      }
-    }
-  }
+  if ((unsigned int)ld_relaxed_sys64(d) != k.seq) return false;
   fence_sys();
   unsigned long long reg = ld_relaxed_sys64(d + 1), off = ld_relaxed_sys64(d + 2);
   sh.recv_next = (char*)(p.regtab[reg * p.n + k.r1] + off);
-  return ST_OK;
+  return true;
 }
 
 // thread 0: fire an armed fault ("Failures may occur mid-chunk").
@@ -375,11 +399,11 @@ __device__ void fire_fault(const Cta& k, const FaultDev& f, int t, int o, int j)
   __threadfence_system();
 }
 
-// thread 0: item delivered -> release + completion word (+ Balance counter)
+// control lane: item delivered -> completion word (+ Balance counter).  The
+// caller has issued the release fence (one for every chunk retired together).
 __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, unsigned int parts,
                               unsigned int epoch, bool own, unsigned int nbytes) {
   const LaunchParams& p = *k.p;
-  fence_sys();
   bool last = true;
   const size_t fi = fidx(p, t, o, j);
   if (parts > 1) {
@@ -412,96 +436,323 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
   }
 }
 
-// ------------------------------------------------------------------ an item
-template <int DT>
-__device__ int do_item(Cta& k, Shared& sh, int t, int o, int j, unsigned int lo, unsigned int hi,
-                       unsigned int parts, unsigned int epoch, bool own) {
+// ------------------------------------------------------------ work list
+// The merged work list of one CTA in (step, origin, chunk) order: its own
+// chunks (j = w, w+W, ...) and the chunks it adopts for dead origins (static
+// plan: plan-time placement from the health records; dynamic plan: the
+// monitor's residual bitmaps).  Resumable iterator of the control lane.
+struct Iter {
+  int t, o, j;
+};
+struct ItemRef {
+  int t, o, j;
+  unsigned int lo, hi, parts, epoch;
+  bool own;
+};
+
+__device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out) {
   const LaunchParams& p = *k.p;
-  const int n = p.n;
-  if (k.tid == 0) {
-    int st = ST_OK;
-    sh.fire = 0;
-    const unsigned long long key = keyof(t, o, j);
-    // deterministic fault rule: channel dead from the armed key on (C-6)
-    for (int i = 0; i < p.nfaults && st == ST_OK; ++i) {
-      const FaultDev& f = p.faults[i];
-      if ((int)f.rank != k.r || (int)f.channel != k.c || f.kind > 2) continue;
-      unsigned long long kf = keyof(f.t, f.origin, f.j);
-      // own-origin faults: deterministic "dead from k* on" for every lane of
-      // the channel; adopted-item faults fire when (and if) carried
-      if (key > kf && (int)f.origin == k.c) {
-        st = ST_STOP;
-        sh.cause = STOP_FAULT_TABLE;
-      } else if (key == kf) {
-        sh.fire = 1 + i;
-        unsigned long long bv = f.b / 16;
-        sh.fire_nvec = (unsigned int)(bv < (hi - lo) ? bv : (hi - lo));
-        sh.poison = f.poison;
+  while (it.t < p.steps) {
+    const int t = it.t, o = it.o;
+    const bool own = (o == k.c) && k.own_alive;
+    unsigned int mode = PLAN_NONE, mask = 0, assignee = 0, epoch = 0;
+    const unsigned int* bm = nullptr;
+    bool usable = true;
+    if (!own) {
+      if (sh.freeze) {
+        usable = false;
+      } else if (sh.dynamic) {
+        for (int e = 0; e < sh.nent; ++e)
+          if ((int)sh.ent[e].origin == o) {
+            mode = sh.ent[e].mode;
+            mask = sh.ent[e].mask;
+            assignee = sh.ent[e].assignee;
+            bm = k.me.plan_bits + (size_t)o * p.bits_words;
+          }
+        epoch = sh.seen_epoch;
+      } else if (!(k.conn_mask >> o & 1u)) {
+        mask = k.conn_mask;
+        if (p.strategy == 0) {
+          mode = PLAN_HOT;
+          assignee = 0xFFFFFFFFu;
+          for (int d = 1; d < p.K; ++d)
+            if (mask >> ((o + d) % p.K) & 1u) {
+              assignee = (unsigned int)((o + d) % p.K);
+              break;
+            }
+        } else {
+          mode = PLAN_BAL;
+        }
+      }
+      if (mode == PLAN_NONE) usable = false;
+      else if (mode == PLAN_HOT && assignee != (unsigned int)k.c) usable = false;
+      else if (mode == PLAN_BAL && !(mask >> k.c & 1u)) usable = false;
+    }
+    if (usable) {
+      for (; it.j < p.m; it.j += p.W) {
+        const int j = it.j;
+        const unsigned long long key = keyof(t, o, j);
+        if (own && key < k.own_next_key) continue;
+        const int q = t * p.m + j;
+        if (bm && !(ld_relaxed_sys(bm + (q >> 5)) >> (q & 31) & 1u)) continue;
+        const unsigned int Vj =
+            (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
+        unsigned int lo = 0, hi = Vj, parts = 1;
+        if (!own && mode == PLAN_BAL) {
+          bal_part(Vj, mask, p.weights, p.K, k.c, lo, hi, parts);
+          if (hi == lo) continue;
+        }
+        out.t = t;
+        out.o = o;
+        out.j = j;
+        out.lo = lo;
+        out.hi = hi;
+        out.parts = parts;
+        out.epoch = epoch;
+        out.own = own;
+        it.j += p.W;
+        return true;
       }
     }
-    if (st == ST_OK) st = poll_control(k, sh);
-    if (st == ST_OK && conn_phys_dead(k)) {
-      st = ST_STOP;
-      sh.cause = STOP_DEATH;
+    it.o++;
+    it.j = k.w;
+    if (it.o == p.K) {
+      it.o = 0;
+      it.t++;
     }
-    if (st == ST_OK && t > 0) st = wait_word(k, sh, k.me.flags + fidx(p, t - 1, o, j), true);
-    if (st == ST_OK && t >= n - 1) st = resolve_recv_next(k, sh);
-    sh.decision = st;
   }
-  __syncthreads();
-  // copy the broadcast into registers: thread 0 may rewrite `sh` as soon as
-  // everybody has passed the next barrier
-  const int st = sh.decision;
-  const int fire = sh.fire;
-  const unsigned int fire_nvec = sh.fire_nvec;
-  const int poison = sh.poison;
-  char* const recv_next = sh.recv_next;
-  if (st != ST_OK) {
-    __syncthreads();
-    return st;
-  }
+  return false;
+}
 
-  // addresses
+// ------------------------------------------------------------ control lane
+// Decide one chunk (fault table, control block, emulated death, input
+// arrived?) and, when ready, publish its descriptor into the next slot.
+// Returns ST_OK (published; *fired if it carries an armed fault),
+// ST_NOTREADY, or a terminal status (cause in sh.cause).
+__device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try, bool* fired) {
+  const LaunchParams& p = *k.p;
+  const int n = p.n;
+  int fire = 0;
+  unsigned int fire_nvec = 0;
+  int poison = 0;
+  const unsigned long long key = keyof(it.t, it.o, it.j);
+  for (int i = 0; i < p.nfaults; ++i) {
+    const FaultDev& f = p.faults[i];
+    if ((int)f.rank != k.r || (int)f.channel != k.c || f.kind > 2) continue;
+    const unsigned long long kf = keyof(f.t, f.origin, f.j);
+    // own-origin faults: deterministic "dead from k* on" for every lane of the
+    // channel (reading R-1); adopted-chunk faults fire when (and if) carried
+    if (key > kf && (int)f.origin == k.c) {
+      sh.cause = STOP_FAULT_TABLE;
+      return ST_STOP;
+    }
+    if (key == kf) {
+      fire = 1 + i;
+      const unsigned long long bv = f.b / 16;
+      fire_nvec = (unsigned int)(bv < (it.hi - it.lo) ? bv : (it.hi - it.lo));
+      poison = f.poison;
+    }
+  }
+  if (first_try) {
+    const int st = poll_control(k, sh);
+    if (st != ST_OK) return st;
+    if (conn_phys_dead(k)) {
+      sh.cause = STOP_DEATH;
+      return ST_STOP;
+    }
+  }
+  if (it.t > 0 && (int)(ld_acquire_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0) return ST_NOTREADY;
+  if (it.t >= n - 1 && !try_recv_next(k, sh)) return ST_NOTREADY;
+
   const int E = p.elem_bytes, V = p.V;
-  const int s = (t <= n - 2) ? ((k.r - 1 - t) % n + n) % n : ((k.r - (t - n + 1)) % n + n) % n;
-  const unsigned long long off = (unsigned long long)o * p.slice + (unsigned long long)j * p.chunk +
-                                 (unsigned long long)lo * V;   // shard-local element
-  const unsigned long long e0 = (unsigned long long)s * p.shard + off;
-  const unsigned int nvec = fire ? fire_nvec : (hi - lo);
-  if (t <= n - 2) {
-    const char* s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
-    move<DT>(k, p.send[k.l] + e0 * E, s_in, scratch_slot(k.nx, p, k.par, t) + off * E, false, nullptr,
-             false, e0, nvec);
-  } else if (t == n - 1) {
-    char* d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
-    move<DT>(k, p.send[k.l] + e0 * E, scratch_slot(k.me, p, k.par, n - 2) + off * E, recv_next + e0 * E,
-             true, d_loc, !p.inplace, e0, nvec);
-  } else {
-    move<DT>(k, p.recv[k.l] + e0 * E, nullptr, recv_next + e0 * E, true, nullptr, false, e0, nvec);
+  const int t = it.t;
+  const int s_ = (t <= n - 2) ? ((k.r - 1 - t) % n + n) % n : ((k.r - (t - n + 1)) % n + n) % n;
+  const unsigned long long off =
+      (unsigned long long)it.o * p.slice + (unsigned long long)it.j * p.chunk + (unsigned long long)it.lo * V;
+  const unsigned long long e0 = (unsigned long long)s_ * p.shard + off;
+  const unsigned int u = sh.pub % NSLOT;
+  Slot& d = sh.slot[u];
+  Meta& m = sh.meta[u];
+  d.status = SLOT_GO;
+  d.nvec = fire ? fire_nvec : (it.hi - it.lo);
+  d.total = it.hi - it.lo;
+  d.poison = fire && poison;
+  d.e0 = e0;
+  d.rs = t <= n - 2;
+  if (t <= n - 2) {                                   // reduce-scatter hop
+    d.src = p.send[k.l] + e0 * E;
+    d.s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
+    d.d_rem = scratch_slot(k.nx, p, k.par, t) + off * E;
+    d.rem_user = 0;
+    d.d_loc = nullptr;
+    d.loc_user = 0;
+  } else if (t == n - 1) {                            // final add + first all-gather send
+    d.src = p.send[k.l] + e0 * E;
+    d.s_in = scratch_slot(k.me, p, k.par, n - 2) + off * E;
+    d.d_rem = sh.recv_next + e0 * E;
+    d.rem_user = 1;
+    d.d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
+    d.loc_user = !p.inplace;
+  } else {                                            // all-gather forward
+    d.src = p.recv[k.l] + e0 * E;
+    d.s_in = nullptr;
+    d.d_rem = sh.recv_next + e0 * E;
+    d.rem_user = 1;
+    d.d_loc = nullptr;
+    d.loc_user = 0;
   }
-  if (fire && poison) {
-    // poison the rest of the faulted part at the peer (reading C-6)
-    char* dst = (t <= n - 2) ? scratch_slot(k.nx, p, k.par, t) + off * E : recv_next + e0 * E;
-    const unsigned int total = hi - lo;
-    for (unsigned int v = nvec + k.tid; v < total; v += k.nthr) {
-      long long ev = (long long)(e0 + (unsigned long long)v * V);
-      long long left = (long long)p.N - ev;
-      int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
-      if (t <= n - 2) st_v4(dst + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
-      else st_user(dst + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, E);
+  m.kind = fire ? META_FIRE : META_ITEM;
+  m.t = t;
+  m.o = it.o;
+  m.j = it.j;
+  m.parts = it.parts;
+  m.epoch = it.epoch;
+  m.nbytes = (it.hi - it.lo) * 16u;
+  m.own = it.own;
+  m.fault = fire - 1;
+  mbar_arrive(&sh.full[u]);
+  sh.pub++;
+  if (it.own) k.own_next_key = key + 1;
+  *fired = fire != 0;
+  return ST_OK;
+}
+
+// Control lane (thread 0): run the work list through the slot ring until it
+// is exhausted or a stop / re-plan / abort / timeout is decided; every
+// published chunk is retired before returning, then an END slot releases
+// the data warps.  Returns the status (also in sh.pipe_status).
+__device__ int control_run(Cta& k, Shared& sh) {
+  const LaunchParams& p = *k.p;
+  Iter it{0, 0, k.w};
+  ItemRef cur;
+  bool have = iter_next(k, sh, it, cur);
+  bool first_try = true;
+  int pending = ST_OK;
+  unsigned int idle = 0;
+  unsigned long long t_idle = 0;
+  for (;;) {
+    bool progress = false;
+    // 1. retire finished chunks in order: ONE release fence for all of them
+    unsigned int nd = 0;
+    while (sh.fin + nd != sh.pub) {
+      const unsigned int u = sh.fin + nd;
+      if (!mbar_test(&sh.empty[u % NSLOT], (u / NSLOT) & 1u)) break;
+      ++nd;
+    }
+    if (nd) {
+      bool any = false;
+      for (unsigned int i = 0; i < nd; ++i) any |= sh.meta[(sh.fin + i) % NSLOT].kind != META_END;
+      if (any) fence_sys();
+      for (unsigned int i = 0; i < nd; ++i) {
+        const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
+        if (m.kind == META_ITEM) {
+          complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes);
+        } else if (m.kind == META_FIRE) {
+          atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
+          fire_fault(k, p.faults[m.fault], m.t, m.o, m.j);
+        }
+      }
+      sh.fin += nd;
+      progress = true;
+    }
+    // 2. publish the next chunk when a slot is free and its input has arrived
+    if (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
+      bool fired = false;
+      const int st = try_publish(k, sh, cur, first_try, &fired);
+      first_try = false;
+      if (st == ST_OK) {
+        progress = true;
+        first_try = true;
+        if (fired) {
+          pending = ST_STOP;
+          sh.cause = STOP_FAULT_FIRED;
+          have = false;
+        } else {
+          have = iter_next(k, sh, it, cur);
+        }
+      } else if (st != ST_NOTREADY) {
+        pending = st;
+        have = false;
+      }
+    }
+    // 3. done: everything published is retired -> END releases the data warps
+    if ((!have || pending != ST_OK) && sh.fin == sh.pub) {
+      const unsigned int u = sh.pub % NSLOT;
+      sh.slot[u].status = SLOT_END;
+      sh.meta[u].kind = META_END;
+      sh.pipe_status = pending;
+      mbar_arrive(&sh.full[u]);
+      sh.pub++;
+      return pending;
+    }
+    // 4. idle: periodic control polls, emulated death, watchdog
+    if (progress) {
+      idle = 0;
+      t_idle = 0;
+    } else if ((++idle & 31u) == 0) {
+      if (pending == ST_OK && have) {
+        int st = poll_control(k, sh);
+        if (st == ST_OK && conn_phys_dead(k)) {
+          st = ST_STOP;
+          sh.cause = STOP_DEATH;
+        }
+        if (st != ST_OK) {
+          pending = st;
+          have = false;
+          continue;
+        }
+        const unsigned long long now = gtimer();
+        if (t_idle == 0) {
+          t_idle = now;
+        } else if (now - t_idle > p.watchdog_ns) {
+          pending = ST_TIMEOUT;
+          sh.cause = STOP_TIMEOUT;
+          CtaRec& rec = k.ctrl->cta[k.cta_in_rank];     // diagnostics: the input we gave up on
+          if (cur.t > 0) {
+            const size_t fi = fidx(p, cur.t - 1, cur.o, cur.j);
+            rec.wait_idx = (unsigned int)fi;
+            rec.wait_val = k.me.flags[fi];
+          } else {
+            rec.wait_idx = 0x40000000u;
+            rec.wait_val = 0;
+          }
+          have = false;
+        }
+      }
     }
   }
-  __syncthreads();
-  if (k.tid == 0) {
-    if (fire) {
-      atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nvec * 16ull);
-      fire_fault(k, p.faults[fire - 1], t, o, j);
-      sh.cause = STOP_FAULT_FIRED;
-    } else {
-      complete_item(k, sh, t, o, j, parts, epoch, own, (hi - lo) * 16u);
+}
+
+// Data warps: move the published chunks (16-byte vectors straight into the
+// peer's memory over NVLink), then signal the slot empty.
+template <int DT>
+__device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
+  const LaunchParams& p = *k.p;
+  const unsigned int dtid = k.tid - 32, dn = k.nthr - 32, lane = k.tid & 31u;
+  for (;;) {
+    const unsigned int u = dcount % NSLOT, ph = (dcount / NSLOT) & 1u;
+    mbar_wait(&sh.full[u], ph);
+    ++dcount;
+    const Slot d = sh.slot[u];
+    if (d.status == SLOT_END) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.empty[u]);
+      return;
     }
+    move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec);
+    if (d.poison) {
+      // poison the rest of the faulted part at the peer (reading C-6)
+      for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {
+        const long long ev = (long long)(d.e0 + (unsigned long long)v * p.V);
+        const long long left = (long long)p.N - ev;
+        const int valid = left <= 0 ? 0 : (left >= p.V ? p.V : (int)left);
+        if (d.rs) st_v4(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+        else st_user(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, p.elem_bytes);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[u]);
   }
-  return fire ? ST_STOP : ST_OK;
 }
 
 // thread 0 writes this CTA's record
@@ -541,64 +792,6 @@ __device__ void load_plan(Cta& k, Shared& sh) {
     k.ctrl->cta[k.cta_in_rank].ack = R2_SS(k.seq, sh.seen_epoch);
   }
   __syncthreads();
-}
-
-// all threads: the merged work list, in (step, origin, chunk) order
-template <int DT>
-__device__ int run_list(Cta& k, Shared& sh) {
-  const LaunchParams& p = *k.p;
-  for (int t = 0; t < p.steps; ++t) {
-    for (int o = 0; o < p.K; ++o) {
-      const bool own = (o == k.c) && k.own_alive;
-      unsigned int mode = PLAN_NONE, mask = 0, assignee = 0, epoch = 0;
-      const unsigned int* bm = nullptr;
-      if (!own) {
-        if (sh.freeze) continue;
-        if (sh.dynamic) {
-          for (int e = 0; e < sh.nent; ++e)
-            if ((int)sh.ent[e].origin == o) {
-              mode = sh.ent[e].mode;
-              mask = sh.ent[e].mask;
-              assignee = sh.ent[e].assignee;
-              bm = k.me.plan_bits + (size_t)o * p.bits_words;
-            }
-          epoch = sh.seen_epoch;
-        } else if (!(k.conn_mask >> o & 1u)) {
-          mask = k.conn_mask;
-          if (p.strategy == 0) {
-            mode = PLAN_HOT;
-            assignee = 0xFFFFFFFFu;
-            for (int d = 1; d < p.K; ++d)
-              if (mask >> ((o + d) % p.K) & 1u) {
-                assignee = (unsigned int)((o + d) % p.K);
-                break;
-              }
-          } else {
-            mode = PLAN_BAL;
-          }
-        }
-        if (mode == PLAN_NONE) continue;
-        if (mode == PLAN_HOT && assignee != (unsigned int)k.c) continue;
-        if (mode == PLAN_BAL && !(mask >> k.c & 1u)) continue;
-      }
-      for (int j = k.w; j < p.m; j += p.W) {
-        const unsigned long long key = keyof(t, o, j);
-        if (own && key < k.own_next_key) continue;
-        const int q = t * p.m + j;
-        if (bm && !(ld_relaxed_sys(bm + (q >> 5)) >> (q & 31) & 1u)) continue;
-        const unsigned int Vj = (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
-        unsigned int lo = 0, hi = Vj, parts = 1;
-        if (!own && mode == PLAN_BAL) {
-          bal_part(Vj, mask, p.weights, p.K, k.c, lo, hi, parts);
-          if (hi == lo) continue;
-        }
-        int st = do_item<DT>(k, sh, t, o, j, lo, hi, parts, epoch, own);
-        if (st != ST_OK) return st;
-        if (own) k.own_next_key = key + 1;
-      }
-    }
-  }
-  return ST_OK;
 }
 
 // all threads: wait for the whole rank to finish (delivered + final flags)
@@ -715,8 +908,18 @@ __device__ void cta_main(Cta& k, Shared& sh) {
     }
     return;
   }
+  unsigned int dcount = 0;   // data warps: slots consumed (monotone across pipeline runs)
   for (;;) {
-    st = run_list<DT>(k, sh);
+    // warp-specialized work list: thread 0 controls, warps 1.. move data
+    if (k.tid < 32) {
+      if (k.tid == 0) control_run(k, sh);
+      __syncwarp();
+    } else {
+      data_run<DT>(k, sh, dcount);
+    }
+    __syncthreads();
+    st = sh.pipe_status;
+    __syncthreads();
     if (st == ST_REPLAN) {
       load_plan(k, sh);
       continue;
@@ -804,7 +1007,13 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   if (k.tid == 0) {
     sh.decision = 0;
     sh.cause = 0;
-    sh.fire = 0;
+    sh.pipe_status = 0;
+    sh.pub = 0;
+    sh.fin = 0;
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(&sh.full[s], 1);                          // the control lane's publish
+      mbar_init(&sh.empty[s], (k.nthr >> 5) - 1);         // one arrival per data warp
+    }
     sh.seen_epoch = 0;
     sh.dynamic = 0;
     sh.freeze = 0;
