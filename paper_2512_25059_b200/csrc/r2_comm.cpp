@@ -306,6 +306,22 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   c->plan_seq.assign(c->nlocal, 0);
   c->cur_plan.assign(c->nlocal, {});
   if (cudaStreamCreateWithFlags(&c->mon_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(R2_ERR_CUDA);
+  for (int i = 0; i < r2_comm::kProbeStreams; ++i)
+    if (cudaStreamCreateWithFlags(&c->probe_stream[i], cudaStreamNonBlocking) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+  {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, c->health.size() * sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+    c->health_pinned = (uint32_t*)h;
+    const int steps_cap = c->n > 1 ? 2 * c->n - 2 : 1;
+    if (cudaHostAlloc(&h, (size_t)steps_cap * c->K * c->lay.m_cap * 4, cudaHostAllocDefault) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+    c->flags_pinned = (unsigned int*)h;
+    if (cudaHostAlloc(&h, (size_t)c->K * c->lay.bits_words * 4, cudaHostAllocDefault) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+    c->bits_pinned = (unsigned int*)h;
+  }
   if (c->n > 1) {
     // pre-load the kernels (see r2_warmup): a healthy self-probe
     const RankPtrs& me = c->peers_host[c->first_rank];
@@ -697,6 +713,11 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   if (c->host_stage) cudaFree(c->host_stage);
   if (c->mon_stream) cudaStreamDestroy(c->mon_stream);
   if (c->health_stream) cudaStreamDestroy(c->health_stream);
+  for (int i = 0; i < r2_comm::kProbeStreams; ++i)
+    if (c->probe_stream[i]) cudaStreamDestroy(c->probe_stream[i]);
+  if (c->health_pinned) cudaFreeHost(c->health_pinned);
+  if (c->flags_pinned) cudaFreeHost(c->flags_pinned);
+  if (c->bits_pinned) cudaFreeHost(c->bits_pinned);
   delete c;
   return R2_SUCCESS;
 }

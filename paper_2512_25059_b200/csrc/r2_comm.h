@@ -143,6 +143,12 @@ struct r2_comm {
   std::thread mon;
   std::atomic<bool> stop{false};
   cudaStream_t mon_stream = nullptr;
+  static const int kProbeStreams = 4;        // the probes of a round run concurrently
+  cudaStream_t probe_stream[kProbeStreams] = {};
+  int probe_stream_next = 0;
+  uint32_t* health_pinned = nullptr;         // pinned staging of the health records
+  unsigned int* flags_pinned = nullptr;      // rollback: receiver's completion words
+  unsigned int* bits_pinned = nullptr;       // plan: residual bitmaps
   std::mutex qmu;                            // local message queue (sim + self)
   std::deque<Msg> localq;
   std::vector<uint32_t> handled_err;         // [nlocal*K] last handled err seq

@@ -162,9 +162,11 @@ void r2_declare_repaired(r2_comm* c, int r, int k, uint32_t at_seq) {
 
 int r2_push_health(r2_comm* c) {
   const size_t bytes = c->health.size() * sizeof(uint32_t);
+  memcpy(c->health_pinned, c->health.data(), bytes);     // pinned: true async DMA, no staging
   for (int l = 0; l < c->nlocal; ++l) {
     const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
-    if (cudaMemcpyAsync(me.health, c->health.data(), bytes, cudaMemcpyHostToDevice, c->health_stream) != cudaSuccess)
+    if (cudaMemcpyAsync(me.health, c->health_pinned, bytes, cudaMemcpyHostToDevice, c->health_stream) !=
+        cudaSuccess)
       return -1;
   }
   return cudaStreamSynchronize(c->health_stream) == cudaSuccess ? 0 : -1;

@@ -270,24 +270,30 @@ __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr,
   const int E = p.elem_bytes, V = p.V;
   const unsigned int stride = nthr;
   if (e0 + (unsigned long long)nvec * V <= p.N) {
-    // fast path: every vector is inside the user buffer
+    // fast path: every vector is inside the user buffer.  UNR vectors per
+    // thread per iteration: all loads issued before any use (memory-level
+    // parallelism is what bounds this HBM/NVLink-bound loop)
+#ifndef R2_UNR
+#define R2_UNR 8   // measured: 8 -> 0.956, 4 -> 0.923 of the HBM roof (N=1, profiles/r01_summary.md)
+#endif
+    constexpr int UNR = R2_UNR;
     unsigned int v = tid;
-    for (; v + 3 * stride < nvec; v += 4 * stride) {
-      uint4 a[4];
+    for (; v + (UNR - 1) * stride < nvec; v += UNR * stride) {
+      uint4 a[UNR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) a[u] = ld_cg(src + (size_t)(v + u * stride) * 16);
+      for (int u = 0; u < UNR; ++u) a[u] = ld_cg(src + (size_t)(v + u * stride) * 16);
       if (s_in) {
-        uint4 b[4];
+        uint4 b[UNR];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = ld_cg(s_in + (size_t)(v + u * stride) * 16);
+        for (int u = 0; u < UNR; ++u) b[u] = ld_cg(s_in + (size_t)(v + u * stride) * 16);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = vadd<DT>(b[u], a[u]);
+        for (int u = 0; u < UNR; ++u) a[u] = vadd<DT>(b[u], a[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) st_v4(d_rem + (size_t)(v + u * stride) * 16, a[u]);
+      for (int u = 0; u < UNR; ++u) st_v4(d_rem + (size_t)(v + u * stride) * 16, a[u]);
       if (d_loc) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) st_v4(d_loc + (size_t)(v + u * stride) * 16, a[u]);
+        for (int u = 0; u < UNR; ++u) st_v4(d_loc + (size_t)(v + u * stride) * 16, a[u]);
       }
     }
     for (; v < nvec; v += stride) {

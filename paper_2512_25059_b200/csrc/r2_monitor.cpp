@@ -43,6 +43,12 @@ int aux_of(int a, int b, int n) {
 }
 
 void broadcast(r2_comm* c, Msg m) {
+  // one monitor serves every simulated rank: a single delivery suffices (the
+  // handlers act on all local ranks)
+  if (c->sim) {
+    r2_send_msg(c, c->first_rank, m);
+    return;
+  }
   for (int d = 0; d < c->n; ++d) r2_send_msg(c, d, m);
 }
 
@@ -73,7 +79,9 @@ void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int 
   if (pp.token == 0) pp.token = ++c->probe_token;
   pp.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
   pp.result = c->probe_res_dev + idx;
-  int rc = r2_launch_probe(pp, c->mon_stream);
+  cudaStream_t ps = c->probe_stream[c->probe_stream_next];
+  c->probe_stream_next = (c->probe_stream_next + 1) % r2_comm::kProbeStreams;
+  int rc = r2_launch_probe(pp, ps);
   R2LOG("probe launch %d->%d ch%d slot%d round %08x rc=%d", prober, target, channel, slot, round_id, rc);
   PendingProbe pr{prober, target, channel, slot, l, owner, round_id, seq, c->probe_res_host + idx, idx};
   if (rc != 0) c->probe_res_host[idx] = R2_PROBE_NOT_RUN;
@@ -241,6 +249,7 @@ void on_verdict(r2_comm* c, const Msg& m) {
   for (int e : kill_ep) r2_declare_dead(c, 0, e, m.channel, from);
   if (kill_link && m.b == (m.a + 1) % n) r2_declare_dead(c, 1, m.a, m.channel, from);
   r2_push_health(c);
+  R2LOG("verdict seq %u applied: health records pushed", m.seq);
   if (m.seq == 0) return;
   const LaunchInfo* li = launch_of(c, m.seq);
   if (!li) return;
@@ -451,10 +460,12 @@ void publish_plan(r2_comm* c, Replan& rp) {
   }
   const int m = li.m, steps = li.steps;
   // rollback: read the receiver's completion words (reading C-4)
-  std::vector<unsigned int> flags((size_t)steps * K * m);
+  const unsigned int* flags = c->flags_pinned;
   const RankPtrs& nx = c->peers_host[l * c->n + r1];
-  cudaMemcpyAsync(flags.data(), nx.flags, flags.size() * 4, cudaMemcpyDeviceToHost, c->mon_stream);
+  R2LOG("replan seq %u rank %d ch%d: quiesced, reading flags", rp.seq, r, rp.channel);
+  cudaMemcpyAsync(c->flags_pinned, nx.flags, (size_t)steps * K * m * 4, cudaMemcpyDeviceToHost, c->mon_stream);
   cudaStreamSynchronize(c->mon_stream);
+  R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
   auto done = [&](int t, int o, int j) { return (int)(flags[((size_t)t * K + o) * m + j] - rp.seq) >= 0; };
 
   // healthy: assignable channels; dead: origins re-placed now (statically
@@ -570,7 +581,8 @@ void publish_plan(r2_comm* c, Replan& rp) {
   // publish: entries, unfreeze, new epoch (device reloads and acks)
   // residual bitmaps -> device memory first (read by the CTAs after the epoch)
   unsigned int* dbits = c->peers_host[l * c->n + r].plan_bits;
-  cudaMemcpyAsync(dbits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, c->mon_stream);
+  memcpy(c->bits_pinned, bits.data(), bits.size() * 4);
+  cudaMemcpyAsync(dbits, c->bits_pinned, bits.size() * 4, cudaMemcpyHostToDevice, c->mon_stream);
   cudaStreamSynchronize(c->mon_stream);
   for (size_t i = 0; i < ents.size(); ++i) memcpy((void*)&C->entries[i], &ents[i], sizeof(PlanEntry));
   C->nentries = (unsigned)ents.size();
@@ -614,6 +626,7 @@ bool progress_replans(r2_comm* c) {
         ++i;
         continue;
       }
+      R2LOG("replan seq %u rank %d ch%d: channel quiesced", rp.seq, c->first_rank + l, rp.channel);
       // freeze adopted work when other channels may hold parts of it
       bool need_freeze = c->epoch[l] > 0;
       {

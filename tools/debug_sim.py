@@ -19,7 +19,8 @@ def main():
     dtype, chunk = a.get("dtype", "bfloat16"), a.get("chunk", 16384)
     faults = a.get("faults", [])
     strategy = a.get("strategy", "BALANCE")
-    comm = sim_comm(n, K, W, chunk, strategy=strategy, watchdog_ms=a.get("watchdog_ms", 3000))
+    comm = sim_comm(n, K, W, chunk, strategy=strategy, watchdog_ms=a.get("watchdog_ms", 3000),
+                    max_bytes=max(16 << 20, N * (2 if dtype == "bfloat16" else 4)))
     for f in faults:
         comm.inject_fault(at_seq=1, **f)
     xs = r2inputs.inputs(n, N, dtype)
