@@ -99,7 +99,7 @@ typedef struct {
  *   max_bytes         largest allreduce payload per rank (scratch sizing;
  *                     default 1 GiB)
  *   strategy          R2_BALANCE
- *   probe_timeout_us  200 (reading C-13)
+ *   probe_timeout_us  50 (reading C-13)
  *   watchdog_ms       3000: a kernel waiting longer aborts with R2_ERR_TIMEOUT
  *   channel_w         K integer weights (NULL = equal) for Balance
  *   sim_ranks         world == 1 only: k >= 1 simulated ranks on one GPU

@@ -50,8 +50,7 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
   L.desc = take(8 * 8);
   L.misc = take(sizeof(MiscDev));
   L.stage = take(L.slot_bytes);
-  L.bits_words = (int)(((size_t)steps * L.m_cap + 31) / 32);
-  L.plan_bits = take((size_t)K * L.bits_words * 4);
+  L.dctrl = take(sizeof(DevCtrl));
   L.health = take((size_t)4 * n * K * 4);
   L.total = align_up(off, 4096);
   return L;
@@ -69,7 +68,7 @@ RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
   p.desc = (unsigned long long*)(base + L.desc);
   p.misc = (MiscDev*)(base + L.misc);
   p.stage = base + L.stage;
-  p.plan_bits = (unsigned int*)(base + L.plan_bits);
+  p.dctrl = (DevCtrl*)(base + L.dctrl);
   p.health = (unsigned int*)(base + L.health);
   return p;
 }
@@ -180,7 +179,7 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->chunk_bytes = 512 * 1024;
   cfg->max_bytes = (size_t)1 << 30;
   cfg->strategy = R2_BALANCE;
-  cfg->probe_timeout_us = 200;
+  cfg->probe_timeout_us = 50;
   cfg->watchdog_ms = 3000;
   cfg->use_channel_w = 0;
   for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
@@ -259,6 +258,12 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     void* d = nullptr;
     if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(R2_ERR_CUDA);
     c->probe_res_dev = (int*)d;
+    if (cudaHostAlloc(&h, sizeof(unsigned long long) * r2_comm::kProbeSlots, cudaHostAllocMapped) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+    c->probe_t0_host = (volatile unsigned long long*)h;
+    memset(h, 0, sizeof(unsigned long long) * r2_comm::kProbeSlots);
+    if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(R2_ERR_CUDA);
+    c->probe_t0_dev = (unsigned long long*)d;
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(R2_ERR_CUDA);
 
@@ -318,9 +323,6 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     if (cudaHostAlloc(&h, (size_t)steps_cap * c->K * c->lay.m_cap * 4, cudaHostAllocDefault) != cudaSuccess)
       return fail(R2_ERR_CUDA);
     c->flags_pinned = (unsigned int*)h;
-    if (cudaHostAlloc(&h, (size_t)c->K * c->lay.bits_words * 4, cudaHostAllocDefault) != cudaSuccess)
-      return fail(R2_ERR_CUDA);
-    c->bits_pinned = (unsigned int*)h;
   }
   if (c->n > 1) {
     // pre-load the kernels (see r2_warmup): a healthy self-probe
@@ -337,6 +339,25 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     pp.timeout_ns = 1000000ull;
     pp.result = c->probe_res_dev + (r2_comm::kProbeSlots - 1);
     if (r2_warmup(pp, c->mon_stream) != 0) return fail(R2_ERR_CUDA);
+    c->probe_res_host[r2_comm::kProbeSlots - 1] = -1;
+    // host CLOCK_MONOTONIC <-> device %globaltimer offset (failover timelines):
+    // best of a few probe launches, midpoint of the host window
+    pp.t_start = c->probe_t0_dev + (r2_comm::kProbeSlots - 1);
+    long long best_w = -1;
+    for (int i = 0; i < 5; ++i) {
+      c->probe_t0_host[r2_comm::kProbeSlots - 1] = 0;
+      const uint64_t h0 = r2_now_ns();
+      if (r2_launch_probe(pp, c->mon_stream) != 0) return fail(R2_ERR_CUDA);
+      while (c->probe_t0_host[r2_comm::kProbeSlots - 1] == 0) {
+      }
+      const uint64_t h1 = r2_now_ns();
+      const long long w = (long long)(h1 - h0);
+      if (best_w < 0 || w < best_w) {
+        best_w = w;
+        c->clk_offset = (long long)c->probe_t0_host[r2_comm::kProbeSlots - 1] - (long long)((h0 + h1) / 2);
+      }
+    }
+    cudaStreamSynchronize(c->mon_stream);
     c->probe_res_host[r2_comm::kProbeSlots - 1] = -1;
   }
   if (c->has_oob && c->oob.barrier(c->oob.ctx)) return fail(R2_ERR_BOOTSTRAP);
@@ -453,7 +474,6 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   p.slice = g.slice;
   p.chunk = g.chunk;
   p.slot_bytes = c->lay.slot_bytes;
-  p.bits_words = c->lay.bits_words;
   p.watchdog_ns = (unsigned long long)c->cfg.watchdog_ms * 1000000ull;
   for (int k = 0; k < c->K; ++k) p.weights[k] = c->weights[k];
   p.peers = c->peers_dev;
@@ -708,6 +728,7 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   for (char* a : c->arena) cudaFree(a);
   for (Ctrl* h : c->ctrl_host) cudaFreeHost(h);
   if (c->probe_res_host) cudaFreeHost((void*)c->probe_res_host);
+  if (c->probe_t0_host) cudaFreeHost((void*)c->probe_t0_host);
   if (c->peers_dev) cudaFree(c->peers_dev);
   if (c->regtab_dev) cudaFree(c->regtab_dev);
   if (c->host_stage) cudaFree(c->host_stage);
@@ -717,7 +738,6 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
     if (c->probe_stream[i]) cudaStreamDestroy(c->probe_stream[i]);
   if (c->health_pinned) cudaFreeHost(c->health_pinned);
   if (c->flags_pinned) cudaFreeHost(c->flags_pinned);
-  if (c->bits_pinned) cudaFreeHost(c->bits_pinned);
   delete c;
   return R2_SUCCESS;
 }

@@ -69,6 +69,7 @@ struct Replan {                              // a dead outgoing connection to re
   r2_verdict_t verdict;
   int stage;                                 // 0 quiesce, 1 freeze-wait, 2 done
   uint32_t freeze_epoch;
+  bool froze;                                // adopted work was frozen: rollback reads completion words
   uint64_t t_detect, t_verdict;
   uint64_t t_fire_dev;
 };
@@ -113,6 +114,9 @@ struct r2_comm {
   // probe result slots (host-mapped)
   volatile int* probe_res_host = nullptr;
   int* probe_res_dev = nullptr;
+  volatile unsigned long long* probe_t0_host = nullptr;   // probe start, device clock
+  long long clk_offset = 0;                  // device %globaltimer - host CLOCK_MONOTONIC (ns)
+  unsigned long long* probe_t0_dev = nullptr;
   int probe_res_next = 0;
   static const int kProbeSlots = 256;
 
@@ -148,7 +152,6 @@ struct r2_comm {
   int probe_stream_next = 0;
   uint32_t* health_pinned = nullptr;         // pinned staging of the health records
   unsigned int* flags_pinned = nullptr;      // rollback: receiver's completion words
-  unsigned int* bits_pinned = nullptr;       // plan: residual bitmaps
   std::mutex qmu;                            // local message queue (sim + self)
   std::deque<Msg> localq;
   std::vector<uint32_t> handled_err;         // [nlocal*K] last handled err seq
@@ -204,3 +207,4 @@ bool r2_link_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
 void r2_declare_dead(r2_comm* comm, int kind, int r, int c, uint32_t from_seq);   // kind 0 ep, 1 link
 void r2_declare_repaired(r2_comm* comm, int r, int c, uint32_t at_seq);
 int r2_push_health(r2_comm* comm);                                     // mirror to every local arena
+cudaError_t r2_spin_sync(cudaStream_t s);

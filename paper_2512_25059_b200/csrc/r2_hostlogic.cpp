@@ -169,7 +169,16 @@ int r2_push_health(r2_comm* c) {
         cudaSuccess)
       return -1;
   }
-  return cudaStreamSynchronize(c->health_stream) == cudaSuccess ? 0 : -1;
+  return r2_spin_sync(c->health_stream) == cudaSuccess ? 0 : -1;
+}
+
+// Busy-wait for a stream (the monitor is on the failover critical path; a
+// blocking synchronize can take 100+ us to wake up under load).
+cudaError_t r2_spin_sync(cudaStream_t s) {
+  cudaError_t e;
+  while ((e = cudaStreamQuery(s)) == cudaErrorNotReady) {
+  }
+  return e;
 }
 
 extern "C" const char* r2_strerror(r2_result_t r) {

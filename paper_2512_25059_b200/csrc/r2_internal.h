@@ -23,7 +23,6 @@
 #define R2_MAXW 16
 #define R2_MAXF 8
 #define R2_MAX_REGS 64
-#define R2_BITMAP_WORDS 64            // 2048 stream positions per origin
 #define R2_MAX_CTAS_PER_RANK (R2_MAXK * R2_MAXW)
 
 enum { R2D_INT32 = 0, R2D_FLOAT32 = 1, R2D_BF16 = 2 };
@@ -45,6 +44,21 @@ struct MiscDev {
   unsigned long long first_retx_ns;   // min over adopters (debug)
 };
 
+struct PlanEntry {           // dynamic re-placement of one origin channel
+  unsigned int origin, mode, assignee, mask;   // residual: chunks of origin without a completion word
+};
+
+// Device-resident mirror of the plan fields of Ctrl, one per rank arena.
+// The CTAs poll THIS (an L2 hit) instead of host memory: thousands of PCIe
+// reads per microsecond from every CTA of every GPU saturate the host path
+// (measured: ~90 us per poll under load).  The monitor pushes updates with a
+// one-thread kernel on its own stream (r2_launch_ctrl_push): body first, then
+// (after a fence) the word that publishes it.
+struct DevCtrl {
+  unsigned int plan_seq, epoch, freeze, abort, stop_mask, nentries, pad0, pad1;
+  PlanEntry entries[R2_MAXK];
+};
+
 struct RankPtrs {            // one rank's arena as seen from some process
   char* scratch;
   unsigned int* flags;
@@ -56,7 +70,7 @@ struct RankPtrs {            // one rank's arena as seen from some process
   unsigned long long* desc;
   MiscDev* misc;
   char* stage;
-  unsigned int* plan_bits;   // [K][bits_words] residual bitmaps of the dynamic plan
+  DevCtrl* dctrl;            // plan/stop/abort mirror polled by the CTAs
   unsigned int* health;      // [4][n*K] host health records: ep dead/repair seq, link dead/repair seq
 };
 
@@ -75,22 +89,22 @@ inline __host__ __device__ bool r2_dead_at(unsigned int dseq, unsigned int rseq,
 #endif
 
 struct ArenaLayout {
-  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, plan_bits, health, total;
+  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, dctrl, health, total;
   size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
   int m_cap;
-  int bits_words;             // 32-bit words per origin bitmap: ceil(steps * m_cap / 32)
 };
 
 // ------------------------------------------------------------------ control
-struct PlanEntry {           // dynamic re-placement of one origin channel
-  unsigned int origin, mode, assignee, mask;   // residual bitmap: arena plan_bits[origin]
-};
+
 
 struct CtaRec {                       // written by one CTA, read by the monitor
   volatile unsigned long long ss;    // seq << 32 | state   (one store: never torn)
   volatile unsigned long long ack;   // seq << 32 | acknowledged plan epoch
   volatile unsigned int cause, adopt_tag, wait_idx, wait_val;  // adopt_tag = seq<<8 | epoch; watchdog diagnostics
   volatile unsigned long long t_stop, t_first_adopt;
+  volatile unsigned long long t_apply, t_pub_adopt, t_prev_poll;
+  volatile unsigned int npoll, apply_src;   // diagnostics: plan applied / first adopted chunk published
+  volatile unsigned long long stop_key;  // own chunks with key >= stop_key are not complete (set with the state)
 };
 #define R2_SS(seq, state) (((unsigned long long)(seq) << 32) | (unsigned long long)(state))
 
@@ -120,7 +134,6 @@ struct LaunchParams {
   int dtype, elem_bytes, V, inplace, strategy, sim;
   unsigned long long N, Np, shard, slice, chunk;   // elements
   size_t slot_bytes;
-  int bits_words;
   unsigned long long watchdog_ns;
   int nfaults;
   FaultDev faults[R2_MAXF];
@@ -142,6 +155,7 @@ struct ProbeParams {
   unsigned int token;
   unsigned long long timeout_ns;
   volatile int* result;                  // host-mapped: r2_probe_outcome_t
+  volatile unsigned long long* t_start;  // host-mapped: %globaltimer at probe start (failover timeline)
 };
 
 // host-side launchers implemented in r2_kernels.cu
@@ -153,6 +167,9 @@ int r2_launch_probe(const ProbeParams& p, void* stream);
 int r2_kernel_smem_bytes();
 int r2_max_coop_ctas(int threads);
 int r2_warmup(const ProbeParams& p, void* stream);
+// mode 0: a new collective takes over the block (body, fence, plan_seq);
+// mode 1: update within the collective (body, fence, epoch)
+int r2_launch_ctrl_push(DevCtrl* dst, const DevCtrl& v, int mode, void* stream);
 #ifdef __cplusplus
 }
 #endif

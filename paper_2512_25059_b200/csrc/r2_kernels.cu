@@ -191,9 +191,12 @@ struct Shared {
   int flag;
   unsigned int piece;
   unsigned int pub, fin;      // control: slots published / retired (monotone across pipeline runs)
+  unsigned long long stop_key;  // first own chunk that will not complete (recorded at a stop)
   char* recv_next;
   unsigned long long first_adopt;
   unsigned long long wait_t0;
+  unsigned long long t_poll, t_prev_poll;   // diagnostics
+  unsigned int npoll;
   unsigned long long full[NSLOT];
   unsigned long long empty[NSLOT];
   Slot slot[NSLOT];
@@ -325,12 +328,15 @@ __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr,
 // (set on every rank by a firing fault) and, once alerted, the host-mapped
 // control block (abort, stop mask, plan epoch).
 __device__ int poll_control(const Cta& k, Shared& sh) {
+  sh.t_prev_poll = sh.t_poll;
+  sh.t_poll = gtimer();
+  sh.npoll++;
   if (ld_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq) == k.seq) return ST_ABORT;
   if (!sh.alerted) {
     if (ld_relaxed_sys(k.me.alert) == k.seq) sh.alerted = 1;
   }
   if (sh.alerted) {
-    Ctrl* C = k.ctrl;
+    DevCtrl* C = k.me.dctrl;
     if (ld_relaxed_sys(&C->plan_seq) == k.seq) {
       if (ld_relaxed_sys(&C->abort)) {
         sh.cause = STOP_ABORT;
@@ -462,7 +468,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
     const int t = it.t, o = it.o;
     const bool own = (o == k.c) && k.own_alive;
     unsigned int mode = PLAN_NONE, mask = 0, assignee = 0, epoch = 0;
-    const unsigned int* bm = nullptr;
+    bool dyn = false;
     bool usable = true;
     if (!own) {
       if (sh.freeze) {
@@ -473,7 +479,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
             mode = sh.ent[e].mode;
             mask = sh.ent[e].mask;
             assignee = sh.ent[e].assignee;
-            bm = k.me.plan_bits + (size_t)o * p.bits_words;
+            dyn = true;
           }
         epoch = sh.seen_epoch;
       } else if (!(k.conn_mask >> o & 1u)) {
@@ -499,8 +505,10 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         const int j = it.j;
         const unsigned long long key = keyof(t, o, j);
         if (own && key < k.own_next_key) continue;
-        const int q = t * p.m + j;
-        if (bm && !(ld_relaxed_sys(bm + (q >> 5)) >> (q & 31) & 1u)) continue;
+        // re-placed chunks: exactly those without a completion (reading C-7);
+        // the origin's own lanes have quiesced and no part of an older plan
+        // is in flight (freeze), so the receiver's flags are stable evidence
+        if (dyn && (int)(ld_relaxed_sys(k.nx.flags + fidx(p, t, o, j)) - k.seq) >= 0) continue;
         const unsigned int Vj =
             (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
         unsigned int lo = 0, hi = Vj, parts = 1;
@@ -623,10 +631,32 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   return ST_OK;
 }
 
+// Control lane: apply a new plan epoch in place (no pipeline drain: chunks
+// already published have their inputs and complete on their own).  A freeze
+// is acknowledged once no adopted chunk of the old plan is in flight.
+__device__ void apply_plan(const Cta& k, Shared& sh) {
+  DevCtrl* C = k.me.dctrl;
+  const unsigned int e = ld_acquire_sys(&C->epoch);
+  sh.seen_epoch = e;
+  sh.freeze = (int)ld_relaxed_sys(&C->freeze);
+  sh.nent = (int)ld_relaxed_sys(&C->nentries);
+  sh.first_adopt = 0;
+  if (!sh.freeze) {
+    const int words = (int)(sizeof(PlanEntry) / 4);
+    for (int i = 0; i < sh.nent * words; ++i)
+      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)C->entries) + i);
+    sh.dynamic = 1;
+    k.ctrl->cta[k.cta_in_rank].t_apply = gtimer();
+    k.ctrl->cta[k.cta_in_rank].t_prev_poll = sh.t_prev_poll;
+    k.ctrl->cta[k.cta_in_rank].npoll = sh.npoll;
+    k.ctrl->cta[k.cta_in_rank].apply_src = 1;
+  }
+}
+
 // Control lane (thread 0): run the work list through the slot ring until it
-// is exhausted or a stop / re-plan / abort / timeout is decided; every
-// published chunk is retired before returning, then an END slot releases
-// the data warps.  Returns the status (also in sh.pipe_status).
+// is exhausted or a stop / abort / timeout is decided; every published chunk
+// is retired before returning, then an END slot releases the data warps.
+// Returns the status (also in sh.pipe_status).
 __device__ int control_run(Cta& k, Shared& sh) {
   const LaunchParams& p = *k.p;
   Iter it{0, 0, k.w};
@@ -636,6 +666,9 @@ __device__ int control_run(Cta& k, Shared& sh) {
   int pending = ST_OK;
   unsigned int idle = 0;
   unsigned long long t_idle = 0;
+  unsigned long long fired_key = ~0ull;   // own chunk that carried a fired fault
+  unsigned int last_adopt_pub = 0;        // 1 + slot index of the newest published adopted chunk
+  unsigned int ack_epoch = 0;             // freeze epoch still to acknowledge
   for (;;) {
     bool progress = false;
     // 1. retire finished chunks in order: ONE release fence for all of them
@@ -661,15 +694,34 @@ __device__ int control_run(Cta& k, Shared& sh) {
       sh.fin += nd;
       progress = true;
     }
+    // 1b. acknowledge a freeze once no adopted chunk is in flight
+    if (ack_epoch && sh.fin >= last_adopt_pub) {
+      __threadfence_system();            // completion words before the acknowledgement
+      k.ctrl->cta[k.cta_in_rank].ack = R2_SS(k.seq, ack_epoch);
+      ack_epoch = 0;
+    }
     // 2. publish the next chunk when a slot is free and its input has arrived
     if (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
       bool fired = false;
-      const int st = try_publish(k, sh, cur, first_try, &fired);
+      int st = try_publish(k, sh, cur, first_try, &fired);
       first_try = false;
+      if (st == ST_REPLAN) {
+        apply_plan(k, sh);
+        if (sh.freeze) ack_epoch = sh.seen_epoch;
+        it = Iter{0, 0, k.w};             // rescan: own chunks skip by key, re-placed ones by flag
+        have = iter_next(k, sh, it, cur);
+        first_try = true;
+        continue;
+      }
       if (st == ST_OK) {
         progress = true;
         first_try = true;
+        if (!cur.own) {
+          if (!last_adopt_pub) k.ctrl->cta[k.cta_in_rank].t_pub_adopt = gtimer();
+          last_adopt_pub = sh.pub;
+        }
         if (fired) {
+          if (cur.own) fired_key = keyof(cur.t, cur.o, cur.j);
           pending = ST_STOP;
           sh.cause = STOP_FAULT_FIRED;
           have = false;
@@ -682,31 +734,41 @@ __device__ int control_run(Cta& k, Shared& sh) {
       }
     }
     // 3. done: everything published is retired -> END releases the data warps
-    if ((!have || pending != ST_OK) && sh.fin == sh.pub) {
+    if ((!have || pending != ST_OK) && sh.fin == sh.pub && !ack_epoch) {
       const unsigned int u = sh.pub % NSLOT;
       sh.slot[u].status = SLOT_END;
       sh.meta[u].kind = META_END;
       sh.pipe_status = pending;
+      sh.stop_key = fired_key != ~0ull ? fired_key : k.own_next_key;
       mbar_arrive(&sh.full[u]);
       sh.pub++;
       return pending;
     }
-    // 4. idle: periodic control polls, emulated death, watchdog
+    // 4. idle: periodic control polls (new plan, stop, abort), emulated death,
+    //    watchdog while waiting for an input
     if (progress) {
       idle = 0;
       t_idle = 0;
-    } else if ((++idle & 31u) == 0) {
-      if (pending == ST_OK && have) {
-        int st = poll_control(k, sh);
-        if (st == ST_OK && conn_phys_dead(k)) {
-          st = ST_STOP;
-          sh.cause = STOP_DEATH;
-        }
-        if (st != ST_OK) {
-          pending = st;
-          have = false;
-          continue;
-        }
+    } else if ((++idle & 31u) == 0 && pending == ST_OK) {
+      int st = poll_control(k, sh);
+      if (st == ST_REPLAN) {
+        apply_plan(k, sh);
+        if (sh.freeze) ack_epoch = sh.seen_epoch;
+        it = Iter{0, 0, k.w};
+        have = iter_next(k, sh, it, cur);
+        first_try = true;
+        continue;
+      }
+      if (st == ST_OK && have && conn_phys_dead(k)) {
+        st = ST_STOP;
+        sh.cause = STOP_DEATH;
+      }
+      if (st != ST_OK) {
+        pending = st;
+        have = false;
+        continue;
+      }
+      if (have) {
         const unsigned long long now = gtimer();
         if (t_idle == 0) {
           t_idle = now;
@@ -768,6 +830,9 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
 __device__ void post_state(const Cta& k, const Shared& sh, unsigned int state, unsigned int cause) {
   CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
   if (cause) rec.cause = cause;
+  // own chunks with key >= stop_key are not complete (every published chunk
+  // was retired before the state changes; a fired chunk never completes)
+  rec.stop_key = state == CTA_STOPPED ? sh.stop_key : k.own_next_key;
   if (sh.alerted || state == CTA_STOPPED) {
     rec.t_stop = gtimer();
     __threadfence_system();
@@ -778,7 +843,7 @@ __device__ void post_state(const Cta& k, const Shared& sh, unsigned int state, u
 // all threads: pull the dynamic plan from the control block
 __device__ void load_plan(Cta& k, Shared& sh) {
   if (k.tid == 0) {
-    Ctrl* C = k.ctrl;
+    DevCtrl* C = k.me.dctrl;
     unsigned int e = ld_acquire_sys(&C->epoch);
     sh.seen_epoch = e;
     sh.freeze = (int)ld_relaxed_sys(&C->freeze);
@@ -789,8 +854,14 @@ __device__ void load_plan(Cta& k, Shared& sh) {
   if (!sh.freeze) {
     const int words = (int)(sizeof(PlanEntry) / 4);
     for (int i = k.tid; i < sh.nent * words; i += k.nthr)
-      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)k.ctrl->entries) + i);
-    if (k.tid == 0) sh.dynamic = 1;
+      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)k.me.dctrl->entries) + i);
+    if (k.tid == 0) {
+      sh.dynamic = 1;
+      k.ctrl->cta[k.cta_in_rank].t_apply = gtimer();
+      k.ctrl->cta[k.cta_in_rank].t_prev_poll = sh.t_prev_poll;
+      k.ctrl->cta[k.cta_in_rank].npoll = sh.npoll;
+      k.ctrl->cta[k.cta_in_rank].apply_src = 2;
+    }
   }
   __syncthreads();
   if (k.tid == 0) {
@@ -1028,6 +1099,8 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     sh.recv_next = nullptr;
     sh.first_adopt = 0;
     sh.wait_t0 = 0;
+    sh.t_poll = sh.t_prev_poll = 0;
+    sh.npoll = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;
     rec.ss = R2_SS(k.seq, CTA_RUNNING);
@@ -1055,6 +1128,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
 // timeout) if the target's endpoint or a link between them is dead.
 __global__ void r2_probe_kernel(const __grid_constant__ ProbeParams p) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (p.t_start) *p.t_start = gtimer();
   int res;
   const int K = p.K, c = p.channel;
   if (ld_relaxed_sys(p.ep_dead + p.prober * K + c)) {
@@ -1101,11 +1175,35 @@ int r2_kernel_smem_bytes() { return (int)sizeof(Shared); }
 // allreduce kernel -- which itself waits for the probe verdict (deadlock
 // until the watchdog).  A warm-up launch of the probe kernel (self-probe of a
 // healthy mailbox) and an attribute query of the allreduce kernel load them.
+// one thread: install a plan/stop/abort update into the device mirror
+__global__ void r2_ctrl_push_kernel(DevCtrl* dst, const __grid_constant__ DevCtrl v, int mode) {
+  volatile unsigned int* d = (volatile unsigned int*)dst;
+  const unsigned int* s = (const unsigned int*)&v;
+  const int words = (int)(sizeof(DevCtrl) / 4);
+  for (int i = 2; i < words; ++i) d[i] = s[i];          // body: freeze .. entries
+  __threadfence();
+  if (mode == 0) {
+    d[1] = v.epoch;
+    __threadfence();
+    d[0] = v.plan_seq;
+  } else {
+    d[1] = v.epoch;
+  }
+  __threadfence();
+}
+
+int r2_launch_ctrl_push(DevCtrl* dst, const DevCtrl& v, int mode, void* stream) {
+  r2_ctrl_push_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst, v, mode);
+  return (int)cudaGetLastError();
+}
+
 int r2_warmup(const ProbeParams& p, void* stream) {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, r2_allreduce_kernel);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncGetAttributes(&a, r2_probe_kernel);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaFuncGetAttributes(&a, r2_ctrl_push_kernel);
   if (e != cudaSuccess) return (int)e;
   r2_probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   e = cudaGetLastError();
@@ -1113,10 +1211,12 @@ int r2_warmup(const ProbeParams& p, void* stream) {
   return (int)cudaStreamSynchronize((cudaStream_t)stream);
 }
 
+// The cooperative grid leaves two SMs free: the probe-flag kernels and the
+// control-block pushes of the monitor must run while a collective is stuck.
 int r2_max_coop_ctas(int threads) {
   int dev = 0, nsm = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, r2_allreduce_kernel, threads, 0);
-  return nsm * per;
+  return (nsm - 2) * per;
 }

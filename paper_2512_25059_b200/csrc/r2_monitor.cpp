@@ -79,6 +79,8 @@ void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int 
   if (pp.token == 0) pp.token = ++c->probe_token;
   pp.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
   pp.result = c->probe_res_dev + idx;
+  pp.t_start = c->probe_t0_dev + idx;
+  c->probe_t0_host[idx] = 0;
   cudaStream_t ps = c->probe_stream[c->probe_stream_next];
   c->probe_stream_next = (c->probe_stream_next + 1) % r2_comm::kProbeStreams;
   int rc = r2_launch_probe(pp, ps);
@@ -169,7 +171,8 @@ bool progress_probes(r2_comm* c) {
     busy = true;
     PendingProbe done = pr;
     c->probes.erase(c->probes.begin() + i);
-    R2LOG("probe result %d->%d ch%d slot%d = %d", done.prober, done.target, done.channel, done.slot, v);
+    R2LOG("probe result %d->%d ch%d slot%d = %d (device start %llu)", done.prober, done.target, done.channel,
+          done.slot, v, (unsigned long long)c->probe_t0_host[done.res_index]);
     if (is_local(c, done.round_owner)) {
       round_result(c, done.round_id, done.slot, v);
     } else {
@@ -187,6 +190,24 @@ bool progress_probes(r2_comm* c) {
 }
 
 // ------------------------------------------------------------------ ctrl
+// The host-mapped Ctrl keeps the host's copy of the plan fields; the CTAs
+// poll the device mirror (DevCtrl, r2_internal.h) that this installs.
+void push_ctrl(r2_comm* c, int l, int mode) {
+  const Ctrl* C = c->ctrl_host[l];
+  DevCtrl v;
+  memset(&v, 0, sizeof(v));
+  v.plan_seq = C->plan_seq;
+  v.epoch = C->epoch;
+  v.freeze = C->freeze;
+  v.abort = C->abort;
+  v.stop_mask = C->stop_mask;
+  v.nentries = C->nentries;
+  memcpy(v.entries, (const void*)C->entries, sizeof(v.entries));
+  const int r = c->first_rank + l;
+  int rc = r2_launch_ctrl_push(c->peers_host[l * c->n + r].dctrl, v, mode, c->mon_stream);
+  if (rc != 0) R2LOG("ctrl push failed rank %d: %d", r, rc);
+}
+
 void ctrl_init_for(r2_comm* c, int l, uint32_t seq) {
   if (c->plan_seq[l] == seq) return;
   Ctrl* C = c->ctrl_host[l];
@@ -198,6 +219,7 @@ void ctrl_init_for(r2_comm* c, int l, uint32_t seq) {
   std::atomic_thread_fence(std::memory_order_seq_cst);
   C->plan_seq = seq;
   std::atomic_thread_fence(std::memory_order_seq_cst);
+  push_ctrl(c, l, 0);
   c->plan_seq[l] = seq;
   c->epoch[l] = 0;
   c->cur_plan[l].clear();
@@ -208,6 +230,7 @@ void set_abort(r2_comm* c, int l, uint32_t seq) {
   Ctrl* C = c->ctrl_host[l];
   C->abort = 1;
   std::atomic_thread_fence(std::memory_order_seq_cst);
+  push_ctrl(c, l, 1);
 }
 
 void record_error(r2_comm* c, int err, uint32_t seq) {
@@ -344,7 +367,8 @@ bool scan_device_records(r2_comm* c) {
       std::atomic_thread_fence(std::memory_order_acquire);
       c->handled_err[l * K + k] = s;
       busy = true;
-      R2LOG("detect seq %u rank %d ch%d cause %u origin %u q %u", s, r, k, e.cause, e.origin, e.q);
+      R2LOG("detect seq %u rank %d ch%d cause %u origin %u q %u (fire -> host detect %.1f us)", s, r, k, e.cause,
+            e.origin, e.q, ((double)(long long)r2_now_ns() - ((double)(long long)e.t_fire - (double)c->clk_offset)) / 1e3);
       const uint64_t now = r2_now_ns();
       {
         std::lock_guard<std::mutex> g(c->mu);
@@ -459,15 +483,6 @@ void publish_plan(r2_comm* c, Replan& rp) {
     li = *p;
   }
   const int m = li.m, steps = li.steps;
-  // rollback: read the receiver's completion words (reading C-4)
-  const unsigned int* flags = c->flags_pinned;
-  const RankPtrs& nx = c->peers_host[l * c->n + r1];
-  R2LOG("replan seq %u rank %d ch%d: quiesced, reading flags", rp.seq, r, rp.channel);
-  cudaMemcpyAsync(c->flags_pinned, nx.flags, (size_t)steps * K * m * 4, cudaMemcpyDeviceToHost, c->mon_stream);
-  cudaStreamSynchronize(c->mon_stream);
-  R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
-  auto done = [&](int t, int o, int j) { return (int)(flags[((size_t)t * K + o) * m + j] - rp.seq) >= 0; };
-
   // healthy: assignable channels; dead: origins re-placed now (statically
   // dead, or known dead AND quiesced -- a known-dead channel whose CTAs are
   // still draining items below its fault point waits for its own re-plan)
@@ -482,6 +497,34 @@ void publish_plan(r2_comm* c, Replan& rp) {
       if (!stat_ok || (!known_ok && channel_quiesced(c, l, k, rp.seq))) dead |= 1u << k;
     }
   }
+  // Rollback: which chunks of each re-placed origin have a completion?
+  // First failure of the collective (nothing adopted yet): the stopped
+  // channel's lanes record the first own chunk that will not complete, so the
+  // ledger follows without touching device memory.  Otherwise (an adopter
+  // failed / static adoption): read the receiver's completion words.
+  const bool from_keys = !rp.froze && dead == (1u << rp.channel);
+  const unsigned int* flags = c->flags_pinned;
+  std::vector<unsigned long long> lane_key(c->W, ~0ull);   // a drained lane completed all its own chunks
+  if (from_keys)
+    for (int w = 0; w < c->W; ++w) {
+      const CtaRec& rec = C->cta[rp.channel * c->W + w];
+      uint32_t s, st;
+      rec_ss(rec, &s, &st);
+      if (st == CTA_STOPPED) lane_key[w] = rec.stop_key;   // fenced before the state (post_state)
+    }
+  if (!from_keys) {
+    const RankPtrs& nx = c->peers_host[l * c->n + r1];
+    cudaMemcpyAsync(c->flags_pinned, nx.flags, (size_t)steps * K * m * 4, cudaMemcpyDeviceToHost, c->mon_stream);
+    r2_spin_sync(c->mon_stream);
+    R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
+  }
+  auto done = [&](int t, int o, int j) {
+    if (from_keys) {
+      const unsigned long long key = ((unsigned long long)t << 40) | ((unsigned long long)o << 32) | (unsigned)j;
+      return key < lane_key[j % c->W];
+    }
+    return (int)(flags[((size_t)t * K + o) * m + j] - rp.seq) >= 0;
+  };
   // what did the stopped channel carry under the previous plan?
   auto carried_by = [&](int k, int o) -> bool {
     if (c->epoch[l] > 0) {
@@ -497,8 +540,6 @@ void publish_plan(r2_comm* c, Replan& rp) {
   std::vector<r2_event_t> evs;
   bool nobackup = false;
   const uint64_t now = r2_now_ns();
-  const int bw = c->lay.bits_words;
-  std::vector<unsigned int> bits((size_t)K * bw, 0u);
   for (int o = 0; o < K; ++o) {
     if (!(dead >> o & 1u)) continue;
     PlanEntry pe;
@@ -506,16 +547,11 @@ void publish_plan(r2_comm* c, Replan& rp) {
     pe.origin = o;
     std::vector<uint8_t> comp((size_t)steps * m);
     int nres = 0;
-    unsigned int* bm = bits.data() + (size_t)o * bw;
     for (int t = 0; t < steps; ++t)
       for (int j = 0; j < m; ++j) {
         bool d = done(t, o, j);
         comp[(size_t)t * m + j] = d;
-        if (!d) {
-          int q = t * m + j;
-          bm[q >> 5] |= 1u << (q & 31);
-          nres++;
-        }
+        if (!d) nres++;
       }
     int resume = 0, floor = 0;
     r2_rollback(comp.data(), steps * m, &resume, &floor);
@@ -578,12 +614,8 @@ void publish_plan(r2_comm* c, Replan& rp) {
     }
     return;
   }
-  // publish: entries, unfreeze, new epoch (device reloads and acks)
-  // residual bitmaps -> device memory first (read by the CTAs after the epoch)
-  unsigned int* dbits = c->peers_host[l * c->n + r].plan_bits;
-  memcpy(c->bits_pinned, bits.data(), bits.size() * 4);
-  cudaMemcpyAsync(dbits, c->bits_pinned, bits.size() * 4, cudaMemcpyHostToDevice, c->mon_stream);
-  cudaStreamSynchronize(c->mon_stream);
+  // publish: entries, unfreeze, new epoch.  The adopters re-place exactly the
+  // chunks without a completion word (checked on the device, reading C-7).
   for (size_t i = 0; i < ents.size(); ++i) memcpy((void*)&C->entries[i], &ents[i], sizeof(PlanEntry));
   C->nentries = (unsigned)ents.size();
   C->freeze = 0;
@@ -591,6 +623,7 @@ void publish_plan(r2_comm* c, Replan& rp) {
   c->epoch[l]++;
   C->epoch = c->epoch[l];
   std::atomic_thread_fence(std::memory_order_seq_cst);
+  push_ctrl(c, l, 1);
   c->cur_plan[l] = ents;
   std::lock_guard<std::mutex> g(c->mu);
   for (auto& ev : evs) {
@@ -621,6 +654,7 @@ bool progress_replans(r2_comm* c) {
       if (!fault_channel && !(C->stop_mask >> rp.channel & 1u)) {
         C->stop_mask = C->stop_mask | (1u << rp.channel);
         std::atomic_thread_fence(std::memory_order_seq_cst);
+        push_ctrl(c, l, 1);
       }
       if (!channel_quiesced(c, l, rp.channel, rp.seq)) {
         ++i;
@@ -640,7 +674,9 @@ bool progress_replans(r2_comm* c) {
         c->epoch[l]++;
         C->epoch = c->epoch[l];
         std::atomic_thread_fence(std::memory_order_seq_cst);
+        push_ctrl(c, l, 1);
         rp.freeze_epoch = c->epoch[l];
+        rp.froze = true;
         rp.stage = 1;
         busy = true;
         ++i;
@@ -656,7 +692,8 @@ bool progress_replans(r2_comm* c) {
       rp.stage = 2;
     }
     publish_plan(c, rp);
-    R2LOG("plan published seq %u rank %d ch%d epoch %u", rp.seq, c->first_rank + l, rp.channel, c->epoch[l]);
+    R2LOG("plan published seq %u rank %d ch%d epoch %u (device clock %lld)", rp.seq, c->first_rank + l, rp.channel,
+          c->epoch[l], (long long)r2_now_ns() + c->clk_offset);
     busy = true;
     c->replans.erase(c->replans.begin() + i);
   }
@@ -688,6 +725,28 @@ bool progress_timings(r2_comm* c) {
       ev.failover_ms = (double)(long long)(best - et.t_fire_dev) / 1e6;
     }
     if (all_done) {
+      if (r2_debug) {
+        unsigned long long a0 = ~0ull, a1 = 0, p0 = ~0ull, p1 = 0, d0 = ~0ull, d1 = 0;
+        for (int k = 0; k < c->K * c->W; ++k) {
+          CtaRec& rec = C->cta[k];
+          if (rec.t_apply) { a0 = std::min(a0, (unsigned long long)rec.t_apply); a1 = std::max(a1, (unsigned long long)rec.t_apply); }
+          if (rec.t_pub_adopt) { p0 = std::min(p0, (unsigned long long)rec.t_pub_adopt); p1 = std::max(p1, (unsigned long long)rec.t_pub_adopt); }
+          if (rec.adopt_tag == tag && rec.t_first_adopt) { d0 = std::min(d0, (unsigned long long)rec.t_first_adopt); d1 = std::max(d1, (unsigned long long)rec.t_first_adopt); }
+        }
+        const long long f = (long long)et.t_fire_dev;
+        std::string ln;
+        for (int k = 0; k < c->K * c->W; ++k) {
+          CtaRec& rec = C->cta[k];
+          char b[96];
+          snprintf(b, sizeof b, " %d:%c%.0f/%.0f/%u", k, rec.apply_src == 1 ? 'R' : 'D', ((long long)rec.t_apply - f) / 1e3,
+                   ((long long)rec.t_prev_poll - f) / 1e3, (unsigned)rec.npoll);
+          ln += b;
+        }
+        R2LOG("apply(us)/prev-poll(us)/npoll per CTA:%s", ln.c_str());
+        R2LOG("timeline seq %u l %d (us after fire): apply %.1f..%.1f  adopt-publish %.1f..%.1f  adopt-done %.1f..%.1f",
+              et.seq, et.l, ((long long)a0 - f) / 1e3, ((long long)a1 - f) / 1e3, ((long long)p0 - f) / 1e3,
+              ((long long)p1 - f) / 1e3, ((long long)d0 - f) / 1e3, ((long long)d1 - f) / 1e3);
+      }
       c->timings.erase(c->timings.begin() + i);
       busy = true;
     } else {

@@ -15,7 +15,8 @@ def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     S = int(os.environ.get("BYTES", 256 << 20))
-    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=16, max_bytes=S))
+    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=16, max_bytes=S,
+                                            strategy=os.environ.get("STRATEGY", "BALANCE")))
     x = torch.randn(S // 2, device="cuda").to(torch.bfloat16)
     y = torch.empty_like(x)
     T.register(comm, y)
@@ -33,7 +34,9 @@ def main():
     e1.synchronize()
     rc = comm.sync()
     evs = comm.events()
-    print(f"[rank {rank}] rc {rc} faulted call {e0.elapsed_time(e1):.3f} ms events "
+    fire = [e["t_fire_dev_ns"] for e in evs]
+    retx = [e["t_first_retx_dev_ns"] for e in evs]
+    print(f"[rank {rank}] rc {rc} faulted call {e0.elapsed_time(e1):.3f} ms fire {fire} retx {retx} events "
           f"{[(e['rank'], e['origin'], e['verdict'], e['resume'], round(e['failover_ms'], 3)) for e in evs]}",
           file=sys.stderr, flush=True)
     dist.barrier()
