@@ -431,6 +431,20 @@ def run_multi(a):
     return res, rank
 
 
+def ncu_traffic(a, n_ranks, W):
+    """DRAM bytes per launch from the committed ncu --set full capture of this
+    exact workload (profiles/r01_ncu_traffic.json), else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
+    if not (n_ranks == 8 and a.bytes == 256 * MIB and a.channels == 8 and W == 2 and a.chunk == 512 * 1024):
+        return None, None
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_launch"], d["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def report(a, res, n_gpus, n_ranks, mode):
     P = peaks()
     S, K = a.bytes, a.channels
@@ -440,8 +454,9 @@ def report(a, res, n_gpus, n_ranks, mode):
     if mode == "sim":
         hbm = (5 * n_ranks - 4) * S
         peak = P.get("hbm_gbs", 6650.0)
+        traffic, tsrc = ncu_traffic(a, n_ranks, res["W"])
         roof = {"bound": "hbm", "achieved": hbm / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                "frac": hbm / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                "frac": hbm / (ms * 1e-3) / 1e9 / peak, "traffic": traffic, "traffic_source": tsrc,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in P else "fallback 6.65 TB/s",
                 "algorithmic_bytes_per_launch": hbm,
                 "per_unit": "(5k-4) x S HBM bytes per simulated allreduce (SURVEY §8(d)), k=%d" % n_ranks}
@@ -450,7 +465,10 @@ def report(a, res, n_gpus, n_ranks, mode):
         peak = 770.0
         roof = {"bound": "nvlink", "achieved": nv / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": nv / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                "traffic_note": "no ncu on multi-rank runs (one-GPU rule); see the N=1 capture",
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)",
+                "sm_store_peak_gbs": 697.0,
+                "sm_store_peak_source": "profiles/r01_p2p_store_n4.log: SM/TMA peer-store ceiling (copy engine 760)",
                 "frac_of_nominal_900": nv / (ms * 1e-3) / 1e9 / 900.0,
                 "algorithmic_bytes_per_launch": nv, "per_unit": "2(n-1)/n x S NVLink bytes per GPU"}
     line = {

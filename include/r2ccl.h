@@ -269,6 +269,16 @@ r2_result_t r2_get_event(r2_comm_t comm, int idx, r2_event_t* out);
  */
 r2_result_t r2_sync(r2_comm_t comm);
 
+/*
+ * r2_trace -- diagnostics.  Returns the device-clock (%globaltimer, ns)
+ * timeline of the collectives launched since the previous r2_trace call on
+ * local rank `rank_local` (64 slots: first CTA start, per-step first publish
+ * and last retire, control end, drain end, exit; 0 / ~0 = not reached) and
+ * re-arms it.  Recording is enabled by the environment variable R2_TRACE=1 at
+ * r2_init; otherwise INVALID_ARG.  Synchronizes the device.
+ */
+r2_result_t r2_trace(r2_comm_t comm, int rank_local, uint64_t out[64]);
+
 /* r2_finalize -- collective.  Stops the monitor, unmaps peers, frees all. */
 r2_result_t r2_finalize(r2_comm_t comm);
 

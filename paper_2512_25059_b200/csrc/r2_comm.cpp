@@ -217,6 +217,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   c->K = cfg.nchannels;
   c->W = cfg.ctas_per_channel;
   c->threads = cfg.threads_per_cta;
+  c->trace = getenv("R2_TRACE") ? atoi(getenv("R2_TRACE")) : 0;
   for (int k = 0; k < c->K; ++k) c->weights[k] = cfg.use_channel_w ? (unsigned)std::max(cfg.channel_w[k], 1) : 1u;
   if (oob) {
     c->oob = *oob;
@@ -475,6 +476,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   p.chunk = g.chunk;
   p.slot_bytes = c->lay.slot_bytes;
   p.watchdog_ns = (unsigned long long)c->cfg.watchdog_ms * 1000000ull;
+  p.trace = c->trace;
   for (int k = 0; k < c->K; ++k) p.weights[k] = c->weights[k];
   p.peers = c->peers_dev;
   p.regtab = c->regtab_dev;
@@ -637,6 +639,19 @@ extern "C" r2_result_t r2_sync(r2_comm_t c) {
     std::this_thread::sleep_for(std::chrono::microseconds(200));
   }
   return (r2_result_t)take_async_error(c);
+}
+
+extern "C" r2_result_t r2_trace(r2_comm_t c, int rank_local, uint64_t out[64]) {
+  if (!c || !out || !c->trace || c->n < 2 || rank_local < 0 || rank_local >= c->nlocal) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return R2_ERR_CUDA;
+  const RankPtrs& me = c->peers_host[rank_local * c->n + c->first_rank + rank_local];
+  unsigned long long* dev = me.misc->trace;
+  if (cudaMemcpy(out, dev, sizeof(unsigned long long) * R2_TRACE_SLOTS, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return R2_ERR_CUDA;
+  unsigned long long arm[R2_TRACE_SLOTS];
+  for (int i = 0; i < R2_TRACE_SLOTS; ++i) arm[i] = (i == 0 || i == 2 || (i >= 32 && i < 60)) ? ~0ull : 0ull;
+  if (cudaMemcpy(dev, arm, sizeof(arm), cudaMemcpyHostToDevice) != cudaSuccess) return R2_ERR_CUDA;
+  return R2_SUCCESS;
 }
 
 extern "C" r2_result_t r2_probe(r2_comm_t c, int rank_local, int peer, int channel, r2_verdict_t* out) {

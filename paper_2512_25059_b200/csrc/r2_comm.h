@@ -95,6 +95,7 @@ struct r2_comm {
   bool sim = false;
   r2_config_t cfg{};
   int K = 8, W = 4, threads = 512;
+  int trace = 0;                             // R2_TRACE=1: record the device timeline (r2_trace)
   unsigned int weights[R2_MAXK]{};
   ArenaLayout lay{};
   r2_oob_t oob{};

@@ -35,6 +35,11 @@ enum { STOP_NONE = 0, STOP_FAULT_FIRED = 1, STOP_FAULT_TABLE = 2, STOP_DEATH = 3
 // plan entry modes
 enum { PLAN_NONE = 0, PLAN_HOT = 1, PLAN_BAL = 2 };
 
+// r2_trace slots: [0] first CTA start (min), [1] last CTA init done (max),
+// [2] first publish (min), [4+t] last own chunk of step t retired (max),
+// [32+t] first own chunk of step t published (min), [60] last control END,
+// [61] last drain done, [62] last CTA exit (max)
+#define R2_TRACE_SLOTS 64
 struct MiscDev {
   unsigned int delivered;     // items whose flag this rank set in this collective
   unsigned int exited;        // CTAs that left the kernel
@@ -42,6 +47,7 @@ struct MiscDev {
   unsigned int abort_seq;     // == seq: a CTA of this rank timed out, all stop
   unsigned long long bytes[R2_MAXK];  // cumulative bytes pushed per carrier channel
   unsigned long long first_retx_ns;   // min over adopters (debug)
+  unsigned long long trace[R2_TRACE_SLOTS];  // %globaltimer timeline when LaunchParams.trace (r2_trace)
 };
 
 struct PlanEntry {           // dynamic re-placement of one origin channel
@@ -135,6 +141,7 @@ struct LaunchParams {
   unsigned long long N, Np, shard, slice, chunk;   // elements
   size_t slot_bytes;
   unsigned long long watchdog_ns;
+  int trace;                             // record the r2_trace timeline
   int nfaults;
   FaultDev faults[R2_MAXF];
   unsigned int weights[R2_MAXK];

@@ -58,6 +58,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// r2_trace timeline (LaunchParams.trace): slot layout in r2_internal.h
+#define TRACE_MIN(k, i) \
+  do { if ((k).p->trace) atomicMin(&(k).me.misc->trace[(i)], gtimer()); } while (0)
+#define TRACE_MAX(k, i) \
+  do { if ((k).p->trace) atomicMax(&(k).me.misc->trace[(i)], gtimer()); } while (0)
 __device__ __forceinline__ uint4 ld_cg(const void* p) {
   uint4 v;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -626,7 +631,11 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   m.fault = fire - 1;
   mbar_arrive(&sh.full[u]);
   sh.pub++;
-  if (it.own) k.own_next_key = key + 1;
+  if (it.own) {
+    k.own_next_key = key + 1;
+    if (t < 28) TRACE_MIN(k, 32 + t);
+    TRACE_MIN(k, 2);
+  }
   *fired = fire != 0;
   return ST_OK;
 }
@@ -686,6 +695,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
         const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
         if (m.kind == META_ITEM) {
           complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes);
+          if (m.own && m.t < 28) TRACE_MAX(k, 4 + m.t);
         } else if (m.kind == META_FIRE) {
           atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
           fire_fault(k, p.faults[m.fault], m.t, m.o, m.j);
@@ -740,6 +750,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
       sh.meta[u].kind = META_END;
       sh.pipe_status = pending;
       sh.stop_key = fired_key != ~0ull ? fired_key : k.own_next_key;
+      TRACE_MAX(k, 60);
       mbar_arrive(&sh.full[u]);
       sh.pub++;
       return pending;
@@ -911,7 +922,10 @@ __device__ int drain(Cta& k, Shared& sh) {
     const unsigned int* fin = k.me.flags + fidx(p, p.steps - 1, 0, 0);
     for (int i = k.tid; i < nf; i += k.nthr)
       if ((int)(ld_acquire_sys(fin + i) - k.seq) < 0) ok = 0;
-    if (__syncthreads_and(ok)) return ST_OK;
+    if (__syncthreads_and(ok)) {
+      if (k.tid == 0) TRACE_MAX(k, 61);
+      return ST_OK;
+    }
     if (k.tid == 0) sh.flag = watchdog(k, sh) ? -1 : 0;
     __syncthreads();
     const int expired = sh.flag == -1;
@@ -960,6 +974,7 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
 // and publishes done_seq for the host's in-flight window.
 __device__ void last_out(const Cta& k) {
   const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
+  TRACE_MAX(k, 62);
   if (atomicAdd(&k.me.misc->exited, 1u) == per_rank - 1) {
     k.me.misc->delivered = 0;
     k.me.misc->copy_next = 0;
@@ -1058,6 +1073,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   k.nx = p.peers[k.l * p.n + k.r1];
   k.ctrl = p.ctrl[k.l];
   k.total_items = (unsigned int)(p.steps * p.K * p.m);
+  if (k.tid == 0) TRACE_MIN(k, 0);
   // plan-time placement: read the host's health records for this seq;
   // every CTA of the rank computes the same mask (records for this seq are
   // never rewritten while it runs, see r2_internal.h)
@@ -1115,6 +1131,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     }
   }
   __syncthreads();
+  if (k.tid == 0) TRACE_MAX(k, 1);
   if (p.dtype == R2D_INT32) cta_main<R2D_INT32>(k, sh);
   else if (p.dtype == R2D_FLOAT32) cta_main<R2D_FLOAT32>(k, sh);
   else cta_main<R2D_BF16>(k, sh);

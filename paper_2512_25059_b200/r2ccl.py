@@ -126,6 +126,7 @@ EXPORTS = {
     "r2_get_event": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Event)]),
     "r2_sync": (C.c_int, [C.c_void_p]),
     "r2_finalize": (C.c_int, [C.c_void_p]),
+    "r2_trace": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
     "r2_strerror": (C.c_char_p, [C.c_int]),
     "r2_triangulate": (C.c_int, [C.POINTER(C.c_int), C.c_int]),
     "r2_balance_shares": (C.c_int, [C.c_uint64, C.POINTER(C.c_int), C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
