@@ -16,6 +16,17 @@ P:94 ring AllReduce = ReduceScatter then AllGather; reading C-3 (chunking).
   (r-(t-n+1)) mod n during AG.
 * effective chunk: min(configured chunk, ceil(slice / W) rounded up to a
   vector) so that W workers per channel all get chunks (reading C-3).
+
+Standalone ReduceScatter / AllGather: the two
+halves of the same ring.  N is then the per-rank shard count (recvcount /
+sendcount); the user buffers hold n shards at stride N; each shard is padded
+to roundup(N, K*V) for the channel split (padding read as 0, never written).
+  * ReduceScatter: steps t = 0..n-1; t <= n-2 are the AllReduce's RS hops,
+    t = n-1 is the owner's final add, written to its own output only (a
+    LOCAL item: no connection is used; its completion word is in the owner's
+    own memory -- reading R-5).
+  * AllGather: steps t = 0..n-2 = the AllReduce's steps n-1..2n-3 (the owner
+    sends its own shard at t = 0, then the ring forwards).
 """
 from __future__ import annotations
 
@@ -26,11 +37,18 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1) -> int:
+ALLREDUCE, REDUCE_SCATTER, ALL_GATHER = "allreduce", "reduce_scatter", "all_gather"
+
+
+def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1,
+                          op: str = ALLREDUCE) -> int:
     """Chunk size actually used (reading C-3); multiple of 16 bytes."""
     V = 16 // elem_bytes
-    Np = ceil_div(max(N, 1), n * K * V) * n * K * V
-    slice_bytes = Np // (n * K) * elem_bytes
+    if op == ALLREDUCE:
+        Np = ceil_div(max(N, 1), n * K * V) * n * K * V
+        slice_bytes = Np // (n * K) * elem_bytes
+    else:
+        slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
     per_worker = ceil_div(ceil_div(slice_bytes, W), 16) * 16
     return max(16, min(chunk_bytes, per_worker))
 
@@ -42,6 +60,7 @@ class Geometry:
     N: int
     elem_bytes: int
     chunk_bytes: int          # the effective chunk (multiple of 16)
+    op: str = ALLREDUCE       # N = per-shard count for REDUCE_SCATTER / ALL_GATHER
 
     @property
     def V(self) -> int:
@@ -49,16 +68,47 @@ class Geometry:
 
     @property
     def Np(self) -> int:
+        if self.op != ALLREDUCE:
+            return self.n * self.shard
         q = self.n * self.K * self.V
         return ceil_div(self.N, q) * q
 
     @property
     def shard(self) -> int:
+        """Padded shard length (the channel split)."""
+        if self.op != ALLREDUCE:
+            q = self.K * self.V
+            return ceil_div(self.N, q) * q
         return self.Np // self.n
 
     @property
+    def stride(self) -> int:
+        """Distance between shards in the user buffers."""
+        return self.shard if self.op == ALLREDUCE else self.N
+
+    @property
+    def total(self) -> int:
+        """Elements of the n-shard user buffer (AllReduce: N)."""
+        return self.N if self.op == ALLREDUCE else self.n * self.N
+
+    def shard_limit(self, s: int) -> int:
+        """One past the last valid global element of shard s."""
+        if self.op == ALLREDUCE:
+            return min(self.N, (s + 1) * self.shard)
+        return s * self.N + self.N
+
+    @property
+    def t0(self) -> int:
+        """AllReduce step that op-step 0 corresponds to."""
+        return self.n - 1 if self.op == ALL_GATHER else 0
+
+    def local(self, t: int) -> bool:
+        """True for the ReduceScatter's final add (no connection used)."""
+        return self.op == REDUCE_SCATTER and t == self.n - 1
+
+    @property
     def slice(self) -> int:
-        return self.Np // (self.n * self.K)
+        return self.shard // self.K
 
     @property
     def chunk(self) -> int:
@@ -70,7 +120,7 @@ class Geometry:
 
     @property
     def steps(self) -> int:
-        return 2 * self.n - 2
+        return {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1}[self.op]
 
     def item_len(self, j: int) -> int:
         """Elements in chunk j of a channel slice."""
@@ -80,15 +130,16 @@ class Geometry:
         return self.item_len(j) // self.V
 
     def shard_sent(self, r: int, t: int) -> int:
-        """Shard that rank r sends at step t (§8 header)."""
+        """Shard that rank r sends at (op-)step t (§8 header)."""
         n = self.n
-        if t <= n - 2:
-            return (r - 1 - t) % n
-        return (r - (t - n + 1)) % n
+        ta = t + self.t0
+        if ta <= n - 2:
+            return (r - 1 - ta) % n
+        return (r - (ta - n + 1)) % n
 
     def item_base(self, r: int, t: int, c: int, j: int) -> int:
-        """Global element offset of item (t, c, j) sent by rank r."""
-        return self.shard_sent(r, t) * self.shard + c * self.slice + j * self.chunk
+        """Global element offset (in the n-shard buffer) of item (t, c, j) of rank r."""
+        return self.shard_sent(r, t) * self.stride + c * self.slice + j * self.chunk
 
     def q(self, t: int, j: int) -> int:
         return t * self.m + j

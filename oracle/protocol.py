@@ -35,6 +35,16 @@ dependency-respecting interleaving must yield identical buffers.
 In-place calls (send == recv): the owner's final sum for its own shard is
 staged and copied to recv at the end, so that a retransmitted final-add chunk
 never reads an already-overwritten input (reading C-7).
+
+Standalone ReduceScatter / AllGather (SURVEY §8(f) f1, P:78, P:94,
+P:353/572 "R²CCL-Balance on AllGather, ReduceScatter"): the same workers,
+flags, faults, rollback and re-placement over the op's steps
+(oracle/geometry.py).  The ReduceScatter's final add is a LOCAL item: it uses
+no connection, so no fault fires on it, its completion word is kept by the
+owner itself, and a stopped worker's unfinished local items are re-placed
+with the rest of its residual (reading R-5).  In-place ReduceScatter
+(recv = own shard of send) needs no staging: the final add is the only
+writer of the own shard and a local item is never torn by a fault.
 """
 from __future__ import annotations
 
@@ -45,7 +55,7 @@ import numpy as np
 from . import balance as _bal
 from . import ledger as _led
 from . import triangulation as _tri
-from .geometry import Geometry
+from .geometry import ALL_GATHER, ALLREDUCE, REDUCE_SCATTER, Geometry
 from .semantic import hop_add, np_dtype
 
 HOT_REPAIR = "HOT_REPAIR"
@@ -90,7 +100,7 @@ class Task:
 
 @dataclass
 class SimResult:
-    y: list                      # per rank result buffer (N elements)
+    y: list                      # per rank result buffer (AllReduce N, ReduceScatter N, AllGather n*N elements)
     events: list                 # failover records (one per re-planned origin)
     detections: list             # triangulation rounds
     bytes_sent: np.ndarray       # [rank, channel] bytes pushed to the peer
@@ -107,6 +117,7 @@ class Simulator:
         self.g, self.dtype = geom, dtype
         self.n, self.K, self.m, self.V = geom.n, geom.K, geom.m, geom.V
         self.N = geom.N
+        self.op = geom.op
         n, K = self.n, self.K
         self.strategy = strategy
         self.weights = {c: 1 for c in range(K)} if weights is None else dict(enumerate(weights))
@@ -114,15 +125,34 @@ class Simulator:
         self.inplace = inplace
         dt = np_dtype(dtype)
         self.dt = dt
-        # buffers
-        if inplace:
-            self.recv = [np.array(x, dtype=dt, copy=True) for x in xs]
-            self.x = self.recv
-            self.stage = [np.zeros(geom.shard, dtype=dt) for _ in range(n)]
+        # buffers: x[r] is the op's input, recv[r] its output (in-place: views
+        # of one buffer, NCCL's convention: RS recv = own shard of send, AG
+        # send = own shard of recv)
+        self.stage = None
+        if self.op == ALLREDUCE:
+            if inplace:
+                self.recv = [np.array(x, dtype=dt, copy=True) for x in xs]
+                self.x = self.recv
+                self.stage = [np.zeros(geom.shard, dtype=dt) for _ in range(n)]
+            else:
+                self.x = [np.asarray(x, dtype=dt) for x in xs]
+                self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
+        elif self.op == REDUCE_SCATTER:
+            self.x = [np.array(x, dtype=dt, copy=True) for x in xs]         # n*N elements
+            if inplace:
+                self.recv = [self.x[r][r * self.N:(r + 1) * self.N] for r in range(n)]
+            else:
+                self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
+        elif self.op == ALL_GATHER:
+            self.recv = [self._poisoned(n * self.N, poison) for _ in range(n)]
+            if inplace:
+                for r in range(n):
+                    self.recv[r][r * self.N:(r + 1) * self.N] = xs[r]
+                self.x = [self.recv[r][r * self.N:(r + 1) * self.N] for r in range(n)]
+            else:
+                self.x = [np.asarray(x, dtype=dt) for x in xs]              # N elements: the own shard
         else:
-            self.x = [np.asarray(x, dtype=dt) for x in xs]
-            self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
-            self.stage = None
+            raise ValueError(self.op)
         self.scratch = [[self._poisoned(geom.shard, poison) for _ in range(max(n - 1, 0))] for _ in range(n)]
         # completion flags live in the receiver's memory: (recv_rank, t, c, j)
         self.flags: set = set()
@@ -180,24 +210,30 @@ class Simulator:
         r1 = (r + 1) % self.n
         return self.ep_dead[r][c] or self.ep_dead[r1][c] or self.link_dead[r][c]
 
-    def xread(self, r, lo, hi):
+    def xread(self, r, lo, hi, lim, base=0):
+        """Input elements [lo, hi) (global n-shard index, valid below lim; the
+        AllGather's input holds only the own shard: base = its global start)."""
         out = np.zeros(hi - lo, dtype=self.dt)
-        top = min(hi, self.N)
+        top = min(hi, lim)
         if top > lo:
-            out[: top - lo] = self.x[r][lo:top]
+            out[: top - lo] = self.x[r][lo - base:top - base]
         return out
 
-    def rread(self, r, lo, hi):
+    def rread(self, r, lo, hi, lim):
         out = np.zeros(hi - lo, dtype=self.dt)
-        top = min(hi, self.N)
+        top = min(hi, lim)
         if top > lo:
             out[: top - lo] = self.recv[r][lo:top]
         return out
 
-    def rwrite(self, r, lo, vals):
-        top = min(lo + len(vals), self.N)
+    def rwrite(self, r, lo, vals, lim, base=0):
+        top = min(lo + len(vals), lim)
         if top > lo:
-            self.recv[r][lo:top] = vals[: top - lo]
+            self.recv[r][lo - base:top - base] = vals[: top - lo]
+
+    def holder(self, r, t) -> int:
+        """Rank whose memory keeps the completion word of r's item at step t."""
+        return r if self.g.local(t) else (r + 1) % self.n
 
     def ready(self, r, task: Task) -> bool:
         return task.t == 0 or (r, task.t - 1, task.origin, task.j) in self.flags
@@ -207,31 +243,42 @@ class Simulator:
         """Execute vectors [lo, hi) of item (task.t, task.origin, task.j) sent by r."""
         g, n, V = self.g, self.n, self.V
         t = task.t
+        ta = t + g.t0                                     # the AllReduce step it corresponds to
         s = g.shard_sent(r, t)
         e0 = g.item_base(r, t, task.origin, task.j) + lo * V
         e1 = e0 + (hi - lo) * V
-        o0, o1 = e0 - s * g.shard, e1 - s * g.shard
+        o0, o1 = e0 - s * g.stride, e1 - s * g.stride    # offsets inside the shard
+        lim = g.shard_limit(s)
         r1 = (r + 1) % n
-        if t <= n - 2:                                    # reduce-scatter hop
-            val = self.xread(r, e0, e1)
+        if ta <= n - 2:                                   # reduce-scatter hop
+            val = self.xread(r, e0, e1, lim)
             if t > 0:
                 val = hop_add(self.scratch[r][t - 1][o0:o1], val, self.dtype)
             self.scratch[r1][t][o0:o1] = val
-        elif t == n - 1:                                  # final add + first all-gather send
-            val = hop_add(self.scratch[r][n - 2][o0:o1], self.xread(r, e0, e1), self.dtype)
+        elif ta == n - 1 and self.op == ALLREDUCE:        # final add + first all-gather send
+            val = hop_add(self.scratch[r][n - 2][o0:o1], self.xread(r, e0, e1, lim), self.dtype)
             if self.inplace:
                 self.stage[r][o0:o1] = val
             else:
-                self.rwrite(r, e0, val)
-            self.rwrite(r1, e0, val)
+                self.rwrite(r, e0, val, lim)
+            self.rwrite(r1, e0, val, lim)
+        elif ta == n - 1 and self.op == REDUCE_SCATTER:   # final add into the own output (LOCAL)
+            val = hop_add(self.scratch[r][n - 2][o0:o1], self.xread(r, e0, e1, lim), self.dtype)
+            self.rwrite(r, e0, val, lim, base=s * g.stride)
+        elif ta == n - 1:                                 # all-gather: the owner sends its shard
+            val = self.xread(r, e0, e1, lim, base=s * g.stride)
+            if not self.inplace:
+                self.rwrite(r, e0, val, lim)
+            self.rwrite(r1, e0, val, lim)
         else:                                             # all-gather forward
-            self.rwrite(r1, e0, self.rread(r, e0, e1))
+            self.rwrite(r1, e0, self.rread(r, e0, e1, lim), lim)
 
     def _run_task(self, w, task: Task):
         r, c = w
         g = self.g
-        # armed fault?
-        for f in self.faults:
+        local = g.local(task.t)
+        # armed fault? (a LOCAL item uses no connection: nothing to fire on)
+        for f in ([] if local else self.faults):
             if (f.rank, f.channel, f.org, f.t, f.j) == (r, c, task.origin, task.t, task.j) and f not in self.fired:
                 bvec = min(max(f.b, 0) // 16, task.hi - task.lo)
                 if bvec > 0:
@@ -249,7 +296,8 @@ class Simulator:
                 self._stop(w)
                 return
         self._move(r, task, task.lo, task.hi)
-        self.bytes_sent[r, c] += (task.hi - task.lo) * 16
+        if not local:
+            self.bytes_sent[r, c] += (task.hi - task.lo) * 16
         self.queue[w].pop(0)
         key = (r, task.t, task.origin, task.j)
         if task.parts == 1:
@@ -262,7 +310,7 @@ class Simulator:
             self.counters[key] = (task.epoch, cnt)
             done = cnt == task.parts
         if done:
-            self.flags.add(((r + 1) % self.n, task.t, task.origin, task.j))
+            self.flags.add((self.holder(r, task.t), task.t, task.origin, task.j))
 
     def _stop(self, w):
         self.state[w] = "stopped"
@@ -270,8 +318,7 @@ class Simulator:
 
     # ------------------------------------------------------------ host side
     def _completed(self, r, origin):
-        r1 = (self.n + r + 1) % self.n
-        return [(r1, t, origin, j) in self.flags for t in range(self.g.steps) for j in range(self.m)]
+        return [(self.holder(r, t), t, origin, j) in self.flags for t in range(self.g.steps) for j in range(self.m)]
 
     def _assign(self, r, origin, items, record):
         """Place residual items of (r -> r+1, origin) on healthy channels."""
@@ -376,14 +423,14 @@ class Simulator:
         if self.error is None:
             missing = [(r, t, c, j) for r in range(self.n) for t in range(self.g.steps)
                        for c in range(self.K) for j in range(self.m)
-                       if ((r + 1) % self.n, t, c, j) not in self.flags]
+                       if (self.holder(r, t), t, c, j) not in self.flags]
             if missing:
                 raise RuntimeError(f"deadlock: {len(missing)} items undelivered, e.g. {missing[:4]}")
-            if self.inplace:
+            if self.stage is not None:
                 g = self.g
                 for r in range(self.n):
                     lo = r * g.shard
-                    self.rwrite(r, lo, self.stage[r])
+                    self.rwrite(r, lo, self.stage[r], g.N)
         health = {"dead_endpoints": sorted((r, c) for r in range(self.n) for c in range(self.K) if self.known_ep_dead[r][c]),
                   "dead_links": sorted((r, c) for r in range(self.n) for c in range(self.K) if self.known_link_dead[r][c])}
         return SimResult(self.recv, self.events, self.detections, self.bytes_sent, self.error, health,
@@ -391,12 +438,9 @@ class Simulator:
 
 
 def simulate(xs, geom: Geometry, dtype: str, **kw) -> SimResult:
-    """Run the Layer-2 protocol simulation for one allreduce."""
-    if geom.n == 1:
-        y = [np.array(xs[0], copy=True)]
-        return SimResult(y, [], [], np.zeros((1, geom.K), dtype=np.int64), None,
+    """Run the Layer-2 protocol simulation for one collective (geom.op)."""
+    if geom.n == 1 or geom.N == 0:
+        y = [np.array(x, copy=True) for x in xs]
+        return SimResult(y, [], [], np.zeros((geom.n, geom.K), dtype=np.int64), None,
                          {"dead_endpoints": [], "dead_links": []}, 0, 0, [])
-    if geom.N == 0:
-        return SimResult([np.array(x, copy=True) for x in xs], [], [], np.zeros((geom.n, geom.K), dtype=np.int64),
-                         None, {"dead_endpoints": [], "dead_links": []}, 0, 0, [])
     return Simulator(xs, geom, dtype, **kw).run()

@@ -1,4 +1,5 @@
-"""Layer 1 of the oracle: WHAT the fault-tolerant allreduce computes.
+"""Layer 1 of the oracle: WHAT the fault-tolerant collectives compute
+(AllReduce; standalone ReduceScatter / AllGather at the end of the file).
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
@@ -106,6 +107,31 @@ def allreduce(xs: list[np.ndarray], shard_elems: int, dtype: str) -> np.ndarray:
             continue
         y[lo:hi] = ring_fold([x[lo:hi] for x in xs], s, dtype)
     return y
+
+
+def reduce_scatter(xs: list[np.ndarray], recvcount: int, dtype: str) -> list[np.ndarray]:
+    """Standalone ReduceScatter ("a ReduceScatter retains only a 1/n
+    shard"; P:94 the first half of the ring AllReduce).
+
+    Rank r's input holds n*recvcount elements (shard s = [s*recvcount,
+    (s+1)*recvcount)); rank r keeps shard r, reduced with the same ring fold
+    as the AllReduce's reduce-scatter half: fold(x_{r+1}, ..., x_{r-1}, x_r).
+    Returns the n output shards (rank r's is element r).
+    """
+    n = len(xs)
+    out = []
+    for r in range(n):
+        lo, hi = r * recvcount, (r + 1) * recvcount
+        out.append(ring_fold([np.asarray(x)[lo:hi] for x in xs], r, dtype))
+    return out
+
+
+def all_gather(shards: list[np.ndarray]) -> np.ndarray:
+    """Standalone AllGather (P:78 "an AllGather must receive the same amount";
+    P:94 the second half of the ring AllReduce): every rank ends with the
+    concatenation shard_0 | shard_1 | ... | shard_{n-1}.  A pure copy: the bits
+    of every shard are preserved."""
+    return np.concatenate([np.asarray(s) for s in shards]) if shards else np.empty(0)
 
 
 def exact_sum_f64(xs: list[np.ndarray], dtype: str) -> np.ndarray:
