@@ -49,6 +49,9 @@ typedef enum {
 
 typedef enum { R2_INT32 = 0, R2_FLOAT32 = 1, R2_BFLOAT16 = 2 } r2_dtype_t;
 
+/* Collectives on the ring (SURVEY §8(f) f1 for the standalone halves). */
+typedef enum { R2_OP_ALLREDUCE = 0, R2_OP_REDUCE_SCATTER = 1, R2_OP_ALL_GATHER = 2 } r2_op_t;
+
 /* Single-failure strategies (P:57 HotRepair; P:73 R²CCL-Balance). */
 typedef enum { R2_HOT_REPAIR = 0, R2_BALANCE = 1 } r2_strategy_t;
 
@@ -231,6 +234,34 @@ r2_result_t r2_allreduce(r2_comm_t comm, const void* send, void* recv, size_t co
                          r2_dtype_t dt, void* stream);
 
 /*
+ * r2_reduce_scatter -- collective, asynchronous ("a
+ * ReduceScatter retains only a 1/n shard"; P:353/572 Balance on RS).  send
+ * holds n * recvcount elements (shard s at element s * recvcount); rank r's
+ * recv receives recvcount elements: shard r reduced with the AllReduce's
+ * ring fold, fold(x_{r+1}, ..., x_{r-1}, x_r) per element, per-hop rounding as
+ * r2_allreduce.  In-place: recv == send + r * recvcount.  recv needs no
+ * registration (peers write only into library scratch).  Same fault handling
+ * (rollback, failover chain / Balance; the owner's final add is a LOCAL item
+ * that uses no connection, reading R-5).  Sim mode: send rows of n * recvcount
+ * elements and recv rows of recvcount elements, each row 16-byte aligned.
+ * Errors: as r2_allreduce.
+ */
+r2_result_t r2_reduce_scatter(r2_comm_t comm, const void* send, void* recv, size_t recvcount,
+                              r2_dtype_t dt, void* stream);
+
+/*
+ * r2_all_gather -- collective, asynchronous (f1; "an AllGather must
+ * receive the same amount").  send holds sendcount elements; every rank's
+ * recv receives n * sendcount elements, rank s's input at element
+ * s * sendcount (bits preserved).  In-place: send == recv + r * sendcount.
+ * recv must lie in a registered range (peers write into it).  Sim mode: send
+ * rows of sendcount and recv rows of n * sendcount elements, 16-byte aligned.
+ * Errors: as r2_allreduce.
+ */
+r2_result_t r2_all_gather(r2_comm_t comm, const void* send, void* recv, size_t sendcount,
+                          r2_dtype_t dt, void* stream);
+
+/*
  * r2_allreduce_host -- as r2_allreduce, but send/recv are HOST buffers (pinned
  * memory recommended).  Enqueues H2D copy into a library-owned registered
  * device buffer, the allreduce and the D2H copy on `stream`; the caller
@@ -303,13 +334,23 @@ void r2_failover_chain(int c, int K, int* out);
 /* Rollback on a completion ledger. */
 void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
 
-/* Geometry of one allreduce (SURVEY §8 header, reading C-3). */
+/* Geometry of one collective (SURVEY §8 header, reading C-3).
+ * AllReduce: N = count, shards of Np/n at stride shard.
+ * ReduceScatter / AllGather (f1): N = n * count (the n-shard user buffer),
+ * shard = roundup(count, K*V) (the channel split), stride = count (shard
+ * distance in the user buffers); steps n (RS: t = n-1 is the owner's LOCAL
+ * final add, local_step = n-1) / n-1 (AG: op-step t is AllReduce step
+ * t + t0, t0 = n-1). */
 typedef struct {
   uint64_t N, Np, shard, slice, chunk; /* elements */
   int n, K, W, V, m, steps;
+  uint64_t stride;                     /* elements between shards in the user buffers */
+  int t0, local_step;                  /* AllReduce step of op-step 0; LOCAL step or -1 */
 } r2_geometry_t;
 r2_result_t r2_geometry(uint64_t count, r2_dtype_t dt, int n, int K, int W,
                         size_t chunk_bytes, r2_geometry_t* out);
+r2_result_t r2_geometry_op(r2_op_t op, uint64_t count, r2_dtype_t dt, int n, int K, int W,
+                           size_t chunk_bytes, r2_geometry_t* out);
 
 /* POSIX shared-memory OOB for ranks of one node.  `name` must be identical
  * on all ranks and unique per communicator (e.g. from the launcher's store).

@@ -439,8 +439,11 @@ extern "C" r2_result_t r2_inject_fault(r2_comm_t c, const r2_fault_t* f) {
   return R2_SUCCESS;
 }
 
-static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, size_t count, r2_dtype_t dt,
-                                     void* stream) {
+// One ring collective (AllReduce, or the standalone ReduceScatter / AllGather
+// halves of SURVEY §8(f) f1).  `count`: AllReduce elements; RS recvcount; AG
+// sendcount.
+static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                                void* stream) {
   const int E = elem_bytes(dt);
   if (c->n == 1) {
     if (send != recv) CK(cudaMemcpyAsync(recv, send, count * E, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -448,7 +451,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
     return R2_SUCCESS;
   }
   r2_geometry_t g;
-  r2_result_t e = r2_geometry(count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
+  r2_result_t e = r2_geometry_op(op, count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
   if (e != R2_SUCCESS) return e;
   if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
   const uint32_t seq = (uint32_t)(c->seq + 1);
@@ -466,7 +469,19 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   p.dtype = dt == R2_INT32 ? R2D_INT32 : (dt == R2_FLOAT32 ? R2D_FLOAT32 : R2D_BF16);
   p.elem_bytes = E;
   p.V = g.V;
-  p.inplace = send == recv;
+  p.op = op;
+  p.t0 = g.t0;
+  p.local_step = g.local_step;
+  p.fin_step = op == R2_OP_REDUCE_SCATTER ? c->n - 2 : g.steps - 1;
+  p.peer_recv = op != R2_OP_REDUCE_SCATTER;
+  p.sstride = g.stride;
+  p.slen = op == R2_OP_ALLREDUCE ? g.shard : count;
+  // in-place (NCCL's convention for RS / AG: recv / send is the own shard)
+  const size_t shard_bytes = count * (size_t)E;
+  p.inplace = op == R2_OP_ALLREDUCE && send == recv;
+  if (op == R2_OP_ALL_GATHER && !c->sim)
+    p.ag_inplace = (const char*)send == (const char*)recv + (size_t)c->rank * shard_bytes;
+  if (c->sim && op != R2_OP_ALLREDUCE && (send == recv)) return R2_ERR_INVALID_ARG;   // sim: out-of-place only
   p.strategy = c->cfg.strategy;
   p.sim = c->sim;
   p.N = g.N;
@@ -481,18 +496,21 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
   p.peers = c->peers_dev;
   p.regtab = c->regtab_dev;
 
-  // recv publication (real mode) / rank buffers (sim mode)
-  const size_t stride = align_up(count * E, 16);   // sim mode: 16-B aligned rank rows
+  // recv publication (real mode) / rank buffers (sim mode: 16-B aligned rows)
+  const size_t full = align_up((size_t)g.N * E, 16), part = align_up(count * E, 16);
+  const size_t sstride = op == R2_OP_ALL_GATHER ? part : full;       // sim row strides
+  const size_t rstride = op == R2_OP_REDUCE_SCATTER ? part : full;
   for (int l = 0; l < c->nlocal; ++l) {
-    p.send[l] = (const char*)send + (size_t)l * stride;
-    p.recv[l] = (char*)recv + (size_t)l * stride;
+    p.send[l] = (const char*)send + (size_t)l * sstride;
+    p.recv[l] = (char*)recv + (size_t)l * rstride;
     p.ctrl[l] = c->ctrl_dev[l];
   }
-  if (!c->sim) {
+  if (!c->sim && p.peer_recv) {
+    const size_t rbytes = (size_t)g.N * E;
     int found = -1;
     for (size_t i = 0; i < c->regs.size(); ++i) {
       const Reg& rg = c->regs[i];
-      if (rg.active && (char*)recv >= rg.dptr && (char*)recv + count * E <= rg.dptr + rg.bytes) {
+      if (rg.active && (char*)recv >= rg.dptr && (char*)recv + rbytes <= rg.dptr + rg.bytes) {
         found = (int)i;
         break;
       }
@@ -510,7 +528,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
       repairs.push_back({f.src_rank, f.channel});
       continue;
     }
-    if (f.step >= g.steps || f.chunk >= g.m) continue;   // no such item: never fires
+    if (f.step >= g.steps || f.chunk >= g.m || f.step == g.local_step) continue;   // no such send: never fires
     if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
     FaultDev& d = p.faults[p.nfaults++];
     d.rank = f.src_rank;
@@ -542,6 +560,7 @@ static r2_result_t enqueue_allreduce(r2_comm* c, const void* send, void* recv, s
 
   LaunchInfo li{};
   li.seq = seq;
+  li.local_step = g.local_step;
   li.m = g.m;
   li.steps = g.steps;
   li.V = g.V;
@@ -584,7 +603,41 @@ extern "C" r2_result_t r2_allreduce(r2_comm_t c, const void* send, void* recv, s
   if (!send || !recv || ((uintptr_t)send & 15) || ((uintptr_t)recv & 15)) return R2_ERR_INVALID_ARG;
   if (count * (size_t)elem_bytes(dt) > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
-  return enqueue_allreduce(c, send, recv, count, dt, stream);
+  return enqueue_coll(c, R2_OP_ALLREDUCE, send, recv, count, dt, stream);
+}
+
+// ReduceScatter / AllGather (f1).  The shard stride count * elem need not be
+// a multiple of 16 bytes: the kernel then uses element-wise user accesses.
+static r2_result_t rs_ag(r2_comm_t c, r2_op_t op, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                         void* stream) {
+  if (!c) return R2_ERR_INVALID_ARG;
+  int ae = take_async_error(c);
+  if (ae != R2_SUCCESS) return (r2_result_t)ae;
+  if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
+  if (count == 0) return R2_SUCCESS;
+  if (!send || !recv) return R2_ERR_INVALID_ARG;
+  const size_t E = (size_t)elem_bytes(dt);
+  // the n-shard buffer is 16-byte aligned; the one-shard buffer only needs
+  // element alignment when it is the own shard of the other (in place)
+  const void* big = op == R2_OP_REDUCE_SCATTER ? send : (const void*)recv;
+  if ((uintptr_t)big & 15) return R2_ERR_INVALID_ARG;
+  const void* small = op == R2_OP_REDUCE_SCATTER ? (const void*)recv : send;
+  const bool own_shard = !c->sim && (const char*)small == (const char*)big + (size_t)c->rank * count * E;
+  if (!own_shard && ((uintptr_t)small & 15)) return R2_ERR_INVALID_ARG;
+  if ((uintptr_t)small % E) return R2_ERR_INVALID_ARG;
+  if ((size_t)c->n * count * E > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  return enqueue_coll(c, op, send, recv, count, dt, stream);
+}
+
+extern "C" r2_result_t r2_reduce_scatter(r2_comm_t c, const void* send, void* recv, size_t recvcount, r2_dtype_t dt,
+                                         void* stream) {
+  return rs_ag(c, R2_OP_REDUCE_SCATTER, send, recv, recvcount, dt, stream);
+}
+
+extern "C" r2_result_t r2_all_gather(r2_comm_t c, const void* send, void* recv, size_t sendcount, r2_dtype_t dt,
+                                     void* stream) {
+  return rs_ag(c, R2_OP_ALL_GATHER, send, recv, sendcount, dt, stream);
 }
 
 extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* recv, size_t count, r2_dtype_t dt,
@@ -613,7 +666,7 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
     for (int l = 0; l < c->nlocal; ++l)
       CK(cudaMemcpyAsync(c->host_stage + l * stride, (const char*)send + l * stride, bytes, cudaMemcpyHostToDevice, s));
   }
-  r2_result_t e = enqueue_allreduce(c, c->host_stage, c->host_stage, count, dt, stream);
+  r2_result_t e = enqueue_coll(c, R2_OP_ALLREDUCE, c->host_stage, c->host_stage, count, dt, stream);
   if (e != R2_SUCCESS) return e;
   if (stride == bytes || c->nlocal == 1) {
     CK(cudaMemcpyAsync(recv, c->host_stage, bytes * c->nlocal, cudaMemcpyDeviceToHost, s));

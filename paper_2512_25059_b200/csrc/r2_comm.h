@@ -49,6 +49,7 @@ struct Reg {
 
 struct LaunchInfo {                          // what the monitor needs about a seq
   uint32_t seq;
+  int local_step;                            // ReduceScatter's LOCAL step (own completion words) or -1
   int m, steps, V;
   unsigned long long slice, chunk;
   int nfaults;

@@ -138,7 +138,14 @@ struct LaunchParams {
   unsigned int seq;
   int n, K, W, m, steps, nlocal, first_rank;
   int dtype, elem_bytes, V, inplace, strategy, sim;
-  unsigned long long N, Np, shard, slice, chunk;   // elements
+  int op;                                // r2_op_t
+  int t0;                                // AllReduce step of op-step 0 (AllGather: n-1)
+  int local_step;                        // op-step of LOCAL items (ReduceScatter: n-1) or -1
+  int fin_step;                          // last op-step with incoming completion words
+  int peer_recv;                         // some step writes the downstream rank's recv
+  int ag_inplace;                        // AllGather with send == own shard of recv
+  unsigned long long N, Np, shard, slice, chunk;   // elements (N: the whole user buffer)
+  unsigned long long sstride, slen;      // shard stride in the user buffers / valid elements per shard
   size_t slot_bytes;
   unsigned long long watchdog_ns;
   int trace;                             // record the r2_trace timeline

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/r2ccl.h"
 #include "r2_internal.h"
 
 namespace {
@@ -98,8 +99,8 @@ __device__ __forceinline__ uint4 vadd(uint4 a, uint4 b) {
 }
 
 // masked (tail) user-buffer access: lanes >= valid read as 0 / are not written
-__device__ __forceinline__ uint4 ld_user(const char* p, int valid, int E) {
-  if (valid >= 16 / E) return ld_cg(p);
+__device__ __forceinline__ uint4 ld_user(const char* p, int valid, int E, bool aligned = true) {
+  if (aligned && valid >= 16 / E) return ld_cg(p);
   unsigned int w[4] = {0, 0, 0, 0};
   if (valid > 0) {
     if (E == 4) {
@@ -113,8 +114,8 @@ __device__ __forceinline__ uint4 ld_user(const char* p, int valid, int E) {
   }
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
-__device__ __forceinline__ void st_user(char* p, uint4 v, int valid, int E) {
-  if (valid >= 16 / E) { st_v4(p, v); return; }
+__device__ __forceinline__ void st_user(char* p, uint4 v, int valid, int E, bool aligned = true) {
+  if (aligned && valid >= 16 / E) { st_v4(p, v); return; }
   unsigned int w[4] = {v.x, v.y, v.z, v.w};
   if (E == 4) {
     for (int i = 0; i < valid; ++i) ((volatile unsigned int*)p)[i] = w[i];
@@ -174,14 +175,17 @@ struct Slot {                 // read by the data warps
   char* d_rem;
   char* d_loc;
   int rem_user, loc_user, rs;
+  int aligned;                // every user-buffer pointer 16-byte aligned (ReduceScatter /
+                              // AllGather shards at a ragged stride may not be)
   unsigned long long e0;
+  unsigned long long lim;     // one past the last valid element of the item's shard
 };
 
 struct Meta {                 // read by the control warp at retirement
   int kind;
   int t, o, j;
   unsigned int parts, epoch, nbytes;
-  int own, fault;
+  int own, fault, local;
 };
 
 struct Shared {
@@ -271,13 +275,16 @@ __device__ void bal_part(unsigned int V, unsigned int mask, const unsigned int* 
 //   s_in   : scratch partial (RS t>0, fused) or null
 //   d_rem  : peer scratch (RS, full vectors) or peer recv (fused/AG, masked)
 //   d_loc  : fused only: own stage (in-place, full) or own recv (masked)
+//   (d_rem null: the ReduceScatter's LOCAL final add)
+//   lim    : one past the last valid element of the shard; aligned: user
+//            pointers 16-byte aligned (else element-wise user accesses)
 template <int DT>
 __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr, const char* src, const char* s_in,
                      char* d_rem, bool rem_user, char* d_loc, bool loc_user, unsigned long long e0,
-                     unsigned int nvec) {
+                     unsigned int nvec, unsigned long long lim, bool aligned) {
   const int E = p.elem_bytes, V = p.V;
   const unsigned int stride = nthr;
-  if (e0 + (unsigned long long)nvec * V <= p.N) {
+  if (aligned && d_rem && e0 + (unsigned long long)nvec * V <= lim) {
     // fast path: every vector is inside the user buffer.  UNR vectors per
     // thread per iteration: all loads issued before any use (memory-level
     // parallelism is what bounds this HBM/NVLink-bound loop)
@@ -312,17 +319,20 @@ __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr,
     }
     return;
   }
-  // tail path: vectors straddling / beyond N
+  // tail path: vectors straddling / beyond the shard's end, unaligned user
+  // buffers, or a LOCAL item (no remote destination)
   for (unsigned int v = tid; v < nvec; v += stride) {
     long long ev = (long long)(e0 + (unsigned long long)v * V);
-    long long left = (long long)p.N - ev;
+    long long left = (long long)lim - ev;
     int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
-    uint4 a = ld_user(src + (size_t)v * 16, valid, E);
+    uint4 a = ld_user(src + (size_t)v * 16, valid, E, aligned);
     if (s_in) a = vadd<DT>(ld_cg(s_in + (size_t)v * 16), a);
-    if (rem_user) st_user(d_rem + (size_t)v * 16, a, valid, E);
-    else st_v4(d_rem + (size_t)v * 16, a);
+    if (d_rem) {
+      if (rem_user) st_user(d_rem + (size_t)v * 16, a, valid, E, aligned);
+      else st_v4(d_rem + (size_t)v * 16, a);
+    }
     if (d_loc) {
-      if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E);
+      if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E, aligned);
       else st_v4(d_loc + (size_t)v * 16, a);
     }
   }
@@ -419,7 +429,7 @@ __device__ void fire_fault(const Cta& k, const FaultDev& f, int t, int o, int j)
 // control lane: item delivered -> completion word (+ Balance counter).  The
 // caller has issued the release fence (one for every chunk retired together).
 __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, unsigned int parts,
-                              unsigned int epoch, bool own, unsigned int nbytes) {
+                              unsigned int epoch, bool own, unsigned int nbytes, bool local) {
   const LaunchParams& p = *k.p;
   bool last = true;
   const size_t fi = fidx(p, t, o, j);
@@ -439,10 +449,12 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
     if (last) fence_sys();
   }
   if (last) {
-    st_relaxed_sys(k.nx.flags + fi, k.seq);
+    // the completion word lives with its consumer: the receiver, or this rank
+    // itself for a LOCAL item (ReduceScatter's final add, reading R-5)
+    st_relaxed_sys((local ? k.me.flags : k.nx.flags) + fi, k.seq);
     atomicAdd(&k.me.misc->delivered, 1u);
   }
-  atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nbytes);
+  if (!local) atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nbytes);
   if (!own && sh.first_adopt == 0) {
     // failover latency endpoint: first retransmitted chunk's flag
     sh.first_adopt = gtimer();
@@ -513,7 +525,8 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         // re-placed chunks: exactly those without a completion (reading C-7);
         // the origin's own lanes have quiesced and no part of an older plan
         // is in flight (freeze), so the receiver's flags are stable evidence
-        if (dyn && (int)(ld_relaxed_sys(k.nx.flags + fidx(p, t, o, j)) - k.seq) >= 0) continue;
+        if (dyn && (int)(ld_relaxed_sys((t == p.local_step ? k.me.flags : k.nx.flags) + fidx(p, t, o, j)) - k.seq) >= 0)
+          continue;
         const unsigned int Vj =
             (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
         unsigned int lo = 0, hi = Vj, parts = 1;
@@ -581,14 +594,17 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     }
   }
   if (it.t > 0 && (int)(ld_acquire_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0) return ST_NOTREADY;
-  if (it.t >= n - 1 && !try_recv_next(k, sh)) return ST_NOTREADY;
+  const int t = it.t;
+  const int ta = t + p.t0;                            // the AllReduce step this op-step is
+  const bool local = t == p.local_step;
+  if (ta >= n - 1 && !local && !try_recv_next(k, sh)) return ST_NOTREADY;
 
   const int E = p.elem_bytes, V = p.V;
-  const int t = it.t;
-  const int s_ = (t <= n - 2) ? ((k.r - 1 - t) % n + n) % n : ((k.r - (t - n + 1)) % n + n) % n;
+  const int s_ = (ta <= n - 2) ? ((k.r - 1 - ta) % n + n) % n : ((k.r - (ta - n + 1)) % n + n) % n;
   const unsigned long long off =
       (unsigned long long)it.o * p.slice + (unsigned long long)it.j * p.chunk + (unsigned long long)it.lo * V;
-  const unsigned long long e0 = (unsigned long long)s_ * p.shard + off;
+  const unsigned long long sbase = (unsigned long long)s_ * p.sstride;
+  const unsigned long long e0 = sbase + off;
   const unsigned int u = sh.pub % NSLOT;
   Slot& d = sh.slot[u];
   Meta& m = sh.meta[u];
@@ -597,21 +613,36 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   d.total = it.hi - it.lo;
   d.poison = fire && poison;
   d.e0 = e0;
-  d.rs = t <= n - 2;
-  if (t <= n - 2) {                                   // reduce-scatter hop
+  d.lim = sbase + p.slen < p.N ? sbase + p.slen : p.N;
+  d.rs = ta <= n - 2;
+  if (ta <= n - 2) {                                  // reduce-scatter hop
     d.src = p.send[k.l] + e0 * E;
     d.s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
     d.d_rem = scratch_slot(k.nx, p, k.par, t) + off * E;
     d.rem_user = 0;
     d.d_loc = nullptr;
     d.loc_user = 0;
-  } else if (t == n - 1) {                            // final add + first all-gather send
+  } else if (ta == n - 1 && p.op == R2_OP_ALLREDUCE) {   // final add + first all-gather send
     d.src = p.send[k.l] + e0 * E;
     d.s_in = scratch_slot(k.me, p, k.par, n - 2) + off * E;
     d.d_rem = sh.recv_next + e0 * E;
     d.rem_user = 1;
     d.d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
     d.loc_user = !p.inplace;
+  } else if (ta == n - 1 && p.op == R2_OP_REDUCE_SCATTER) {   // final add into the own output (LOCAL)
+    d.src = p.send[k.l] + e0 * E;
+    d.s_in = scratch_slot(k.me, p, k.par, n - 2) + off * E;
+    d.d_rem = nullptr;
+    d.rem_user = 0;
+    d.d_loc = p.recv[k.l] + off * E;
+    d.loc_user = 1;
+  } else if (ta == n - 1) {                           // all-gather: the owner sends its own shard
+    d.src = p.send[k.l] + off * E;
+    d.s_in = nullptr;
+    d.d_rem = sh.recv_next + e0 * E;
+    d.rem_user = 1;
+    d.d_loc = p.ag_inplace ? nullptr : (p.recv[k.l] + e0 * E);
+    d.loc_user = 1;
   } else {                                            // all-gather forward
     d.src = p.recv[k.l] + e0 * E;
     d.s_in = nullptr;
@@ -620,7 +651,10 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     d.d_loc = nullptr;
     d.loc_user = 0;
   }
+  d.aligned = ((((unsigned long long)d.src) | (d.rem_user ? (unsigned long long)d.d_rem : 0ull) |
+                (d.loc_user ? (unsigned long long)d.d_loc : 0ull)) & 15ull) == 0;
   m.kind = fire ? META_FIRE : META_ITEM;
+  m.local = local;
   m.t = t;
   m.o = it.o;
   m.j = it.j;
@@ -694,7 +728,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
       for (unsigned int i = 0; i < nd; ++i) {
         const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
         if (m.kind == META_ITEM) {
-          complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes);
+          complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes, m.local != 0);
           if (m.own && m.t < 28) TRACE_MAX(k, 4 + m.t);
         } else if (m.kind == META_FIRE) {
           atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
@@ -818,15 +852,16 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
       if (lane == 0) mbar_arrive(&sh.empty[u]);
       return;
     }
-    move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec);
-    if (d.poison) {
+    move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
+             d.aligned != 0);
+    if (d.poison && d.d_rem) {
       // poison the rest of the faulted part at the peer (reading C-6)
       for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {
         const long long ev = (long long)(d.e0 + (unsigned long long)v * p.V);
-        const long long left = (long long)p.N - ev;
+        const long long left = (long long)d.lim - ev;
         const int valid = left <= 0 ? 0 : (left >= p.V ? p.V : (int)left);
         if (d.rs) st_v4(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
-        else st_user(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, p.elem_bytes);
+        else st_user(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, p.elem_bytes, d.aligned != 0);
       }
     }
     __syncwarp();
@@ -919,7 +954,7 @@ __device__ int drain(Cta& k, Shared& sh) {
     // all final incoming completion words present?
     int ok = 1;
     const int nf = p.K * p.m;
-    const unsigned int* fin = k.me.flags + fidx(p, p.steps - 1, 0, 0);
+    const unsigned int* fin = k.me.flags + fidx(p, p.fin_step, 0, 0);
     for (int i = k.tid; i < nf; i += k.nthr)
       if ((int)(ld_acquire_sys(fin + i) - k.seq) < 0) ok = 0;
     if (__syncthreads_and(ok)) {
@@ -944,7 +979,7 @@ __device__ int drain(Cta& k, Shared& sh) {
 // in-place: copy the staged own shard into recv (pieces grabbed atomically)
 __device__ void copy_stage(Cta& k, Shared& sh) {
   const LaunchParams& p = *k.p;
-  const unsigned long long shard_vec = p.shard / p.V;
+  const unsigned long long shard_vec = p.shard / p.V;   // AllReduce only (sstride == shard)
   const unsigned int PIECE = 4096;
   const unsigned long long npieces = (shard_vec + PIECE - 1) / PIECE;
   __threadfence();
@@ -1120,7 +1155,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;
     rec.ss = R2_SS(k.seq, CTA_RUNNING);
-    if (!p.sim && k.cta_in_rank == 0) {
+    if (!p.sim && p.peer_recv && k.cta_in_rank == 0) {
       // publish our recv (registration id, offset) for the upstream rank
       volatile unsigned long long* d = k.me.desc + k.par * 4;
       d[1] = (unsigned long long)p.recv_reg[k.l];

@@ -516,6 +516,13 @@ void publish_plan(r2_comm* c, Replan& rp) {
   if (!from_keys) {
     const RankPtrs& nx = c->peers_host[l * c->n + r1];
     cudaMemcpyAsync(c->flags_pinned, nx.flags, (size_t)steps * K * m * 4, cudaMemcpyDeviceToHost, c->mon_stream);
+    if (li.local_step >= 0) {
+      // LOCAL items keep their completion words in this rank's own memory
+      // (reading R-5); the receiver has no words at that step
+      const size_t o = (size_t)li.local_step * K * m;
+      cudaMemcpyAsync(c->flags_pinned + o, c->peers_host[l * c->n + r].flags + o, (size_t)K * m * 4,
+                      cudaMemcpyDeviceToHost, c->mon_stream);
+    }
     r2_spin_sync(c->mon_stream);
     R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
   }

@@ -98,7 +98,8 @@ class Status(C.Structure):
 class Geometry(C.Structure):
     _fields_ = [("N", C.c_uint64), ("Np", C.c_uint64), ("shard", C.c_uint64), ("slice", C.c_uint64),
                 ("chunk", C.c_uint64), ("n", C.c_int), ("K", C.c_int), ("W", C.c_int), ("V", C.c_int),
-                ("m", C.c_int), ("steps", C.c_int)]
+                ("m", C.c_int), ("steps", C.c_int), ("stride", C.c_uint64), ("t0", C.c_int),
+                ("local_step", C.c_int)]
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
@@ -133,6 +134,10 @@ EXPORTS = {
     "r2_failover_chain": (None, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "r2_rollback": (None, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "r2_geometry": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, C.POINTER(Geometry)]),
+    "r2_geometry_op": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t,
+                                 C.POINTER(Geometry)]),
+    "r2_reduce_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
+    "r2_all_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "r2_oob_shm_open": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(Oob)]),
     "r2_oob_shm_close": (C.c_int, [C.POINTER(Oob)]),
 }
@@ -209,9 +214,13 @@ def rollback(completed) -> tuple:
     return r.value, f.value
 
 
-def geometry(count: int, dtype: int, n: int, K: int, W: int, chunk_bytes: int) -> Geometry:
+OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER = 0, 1, 2
+OPS = {"allreduce": OP_ALLREDUCE, "reduce_scatter": OP_REDUCE_SCATTER, "all_gather": OP_ALL_GATHER}
+
+
+def geometry(count: int, dtype: int, n: int, K: int, W: int, chunk_bytes: int, op: int = OP_ALLREDUCE) -> Geometry:
     g = Geometry()
-    _check(lib().r2_geometry(count, dtype, n, K, W, chunk_bytes, C.byref(g)), "r2_geometry")
+    _check(lib().r2_geometry_op(op, count, dtype, n, K, W, chunk_bytes, C.byref(g)), "r2_geometry_op")
     return g
 
 
@@ -287,6 +296,14 @@ class Comm:
     def allreduce(self, send_ptr: int, recv_ptr: int, count: int, dtype: int, stream: int = 0):
         _check(lib().r2_allreduce(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), count, dtype,
                                   C.c_void_p(stream)), "r2_allreduce")
+
+    def reduce_scatter(self, send_ptr: int, recv_ptr: int, recvcount: int, dtype: int, stream: int = 0):
+        _check(lib().r2_reduce_scatter(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), recvcount, dtype,
+                                       C.c_void_p(stream)), "r2_reduce_scatter")
+
+    def all_gather(self, send_ptr: int, recv_ptr: int, sendcount: int, dtype: int, stream: int = 0):
+        _check(lib().r2_all_gather(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), sendcount, dtype,
+                                   C.c_void_p(stream)), "r2_all_gather")
 
     def allreduce_host(self, send_ptr: int, recv_ptr: int, count: int, dtype: int, stream: int = 0):
         _check(lib().r2_allreduce_host(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), count, dtype,

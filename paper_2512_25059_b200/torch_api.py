@@ -83,6 +83,63 @@ def allreduce(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor | None = None
     return recv
 
 
+def _rows_ok(comm: R.Comm, t: torch.Tensor, count: int) -> None:
+    """Sim mode: a [k, row] tensor whose rows are roundup(count * elem, 16) bytes."""
+    if t.dim() != 2 or t.shape[0] != comm.n:
+        raise ValueError(f"sim mode expects a [{comm.n}, row] tensor")
+    if t.shape[1] * t.element_size() != -(-count * t.element_size() // 16) * 16:
+        raise ValueError("sim-mode rows must be roundup(count * elem, 16) bytes long")
+
+
+def _check_pair(send: torch.Tensor, recv: torch.Tensor) -> None:
+    if not (send.is_cuda and recv.is_cuda):
+        raise ValueError("device tensors required")
+    if not (send.is_contiguous() and recv.is_contiguous()):
+        raise ValueError("contiguous tensors required")
+    if send.dtype != recv.dtype:
+        raise ValueError("send/recv must match in dtype")
+
+
+def reduce_scatter(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None,
+                   recvcount: int | None = None) -> torch.Tensor:
+    """Sum-ReduceScatter (r2_reduce_scatter): send holds n shards of recvcount
+    elements, recv receives this rank's reduced shard.  In-place: recv is the
+    own shard of send (a view).  Sim mode: send [k, rowS], recv [k, rowR]."""
+    _check_pair(send, recv)
+    n = comm.n
+    if comm.sim:
+        recvcount = recvcount if recvcount is not None else recv.shape[1]
+        _rows_ok(comm, send, n * recvcount)
+        _rows_ok(comm, recv, recvcount)
+    else:
+        recvcount = recv.numel() if recvcount is None else recvcount
+        if send.numel() < n * recvcount or recv.numel() < recvcount:
+            raise ValueError("send must hold n * recvcount and recv recvcount elements")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    comm.reduce_scatter(send.data_ptr(), recv.data_ptr(), recvcount, r2_dtype(send), s.cuda_stream)
+    return recv
+
+
+def all_gather(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None,
+               sendcount: int | None = None) -> torch.Tensor:
+    """AllGather (r2_all_gather): every rank's recv receives the n inputs in
+    rank order; recv must be registered.  In-place: send is the own shard of
+    recv (a view).  Sim mode: send [k, rowS], recv [k, rowR]."""
+    _check_pair(send, recv)
+    n = comm.n
+    if comm.sim:
+        sendcount = sendcount if sendcount is not None else send.shape[1]
+        _rows_ok(comm, send, sendcount)
+        _rows_ok(comm, recv, n * sendcount)
+    else:
+        sendcount = send.numel() if sendcount is None else sendcount
+        if recv.numel() < n * sendcount:
+            raise ValueError("recv must hold n * sendcount elements")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    comm.all_gather(send.data_ptr(), recv.data_ptr(), sendcount, r2_dtype(send), s.cuda_stream)
+    return recv
+
+
 def allreduce_host(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None,
                    count: int | None = None) -> torch.Tensor:
     """Host (ideally pinned) tensors: H2D, allreduce, D2H on `stream`."""

@@ -76,6 +76,61 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     return out
 
 
+def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", inplace=False, seed=0):
+    """Standalone ReduceScatter / AllGather (f1) over the real NVLink path."""
+    n = world
+    xs = r2inputs.inputs(n, n * count if op == "reduce_scatter" else count, dtype, seed=seed)
+    E = r2inputs.elem_bytes(dtype)
+    if op == "reduce_scatter":
+        send = dev_tensor(xs[rank], dtype)
+        recv = send[rank * count:(rank + 1) * count] if inplace else torch.empty(count, dtype=TD[dtype], device="cuda")
+        want = OS.reduce_scatter(xs, count, dtype)[rank]
+    else:
+        recv = torch.empty(n * count, dtype=TD[dtype], device="cuda")
+        if inplace:
+            recv[rank * count:(rank + 1) * count] = dev_tensor(xs[rank], dtype)
+            send = recv[rank * count:(rank + 1) * count]
+        else:
+            send = dev_tensor(xs[rank], dtype)
+        want = OS.all_gather(xs)
+        T.register(comm, recv)
+    if not inplace:
+        recv.view(torch.uint8).fill_(0xFF)
+    st = comm.status()
+    health = {"dead_links": st["dead_links"], "dead_endpoints": st["dead_endpoints"]}
+    seq = st["seq"] + 1
+    for f in faults:
+        comm.inject_fault(at_seq=seq, **f)
+    ne = len(comm.events())
+    if op == "reduce_scatter":
+        T.reduce_scatter(comm, send, recv, recvcount=count)
+    else:
+        T.all_gather(comm, send, recv, sendcount=count)
+    rc = comm.sync()
+    ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), np.asarray(want).view(np.uint8))
+    evs = [norm_event(e) for e in comm.events()[ne:]]
+    all_evs = [None] * world
+    dist.all_gather_object(all_evs, evs)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok))
+    out = {"op": op, "N": count, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc,
+           "inplace": inplace, "ok": all(oks)}
+    if faults:
+        cfg = comm.cfg
+        g = Geometry(world, cfg.nchannels, count, E, effective_chunk_bytes(
+            count, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel, op), op)
+        got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, health=health,
+                          faults=[OP.Fault(f["kind"], f["src_rank"], f["channel"], f["step"], f["chunk"],
+                                           f.get("byte_offset", 0)) for f in faults])
+        want_ev = sorted((norm_event(e) for e in res.events),
+                         key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        out["events_equal"] = got == want_ev
+        out["events"] = got
+        out["want"] = want_ev
+    return out
+
+
 def main():
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
@@ -94,6 +149,14 @@ def main():
             f = dict(kind="LINK", src_rank=world - 1, channel=1, step=max(0, world - 2), chunk=1,
                      byte_offset=12345, poison=1)
             results.append(case(comm, rank, world, 1 << 20, "bfloat16", [f], strategy, seed=11))
+            # standalone ReduceScatter / AllGather: healthy (ragged, in-place) and one LINK fault
+            for op in ("reduce_scatter", "all_gather"):
+                if strategy == "BALANCE":
+                    for dtype, count in (("bfloat16", 100_003), ("float32", 1 << 18), ("int32", 777)):
+                        results.append(case_op(comm, rank, world, op, count, dtype, seed=count))
+                    results.append(case_op(comm, rank, world, op, 65_537, "bfloat16", inplace=True, seed=3))
+                fo = dict(kind="LINK", src_rank=0, channel=2, step=0, chunk=1, byte_offset=4096, poison=1)
+                results.append(case_op(comm, rank, world, op, 1 << 18, "bfloat16", [fo], strategy, seed=17))
             # degraded steady state (channel 1 of rank world-1 now dead): static plan
             results.append(case(comm, rank, world, 1 << 20, "float32", seed=12))
             comm.finalize()

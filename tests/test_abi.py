@@ -97,6 +97,25 @@ def test_geometry_matches_oracle():
             (og.Np, og.shard, og.slice, og.chunk, og.m, og.steps, og.V)
 
 
+@pytest.mark.parametrize("op", ["reduce_scatter", "all_gather"])
+def test_geometry_op_matches_oracle(op):
+    """ReduceScatter / AllGather geometry (f1): shard padding, stride, steps,
+    AllGather's step offset and the ReduceScatter's LOCAL step."""
+    rng = np.random.default_rng(7)
+    for _ in range(2000):
+        dt = ["int32", "float32", "bfloat16"][int(rng.integers(3))]
+        E = r2inputs.elem_bytes(dt)
+        n, K, W = int(rng.integers(2, 9)), int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        count = int(rng.integers(1, 1 << 20))
+        chunk = int(rng.integers(1, 1 << 16)) * 16
+        g = R.geometry(count, R.DTYPE_NAMES[dt], n, K, W, chunk, R.OPS[op])
+        og = Geometry(n, K, count, E, effective_chunk_bytes(count, n, K, E, chunk, W, op), op)
+        assert (g.N, g.Np, g.shard, g.slice, g.chunk, g.m, g.steps, g.stride, g.t0) == \
+            (og.total, og.Np, og.shard, og.slice, og.chunk, og.m, og.steps, og.stride, og.t0)
+        assert g.local_step == (n - 1 if op == "reduce_scatter" else -1)
+        assert all(og.local(t) == (t == g.local_step) for t in range(og.steps))
+
+
 # ------------------------------------------------------------ OOB, 2 procs
 
 def _oob_worker(rank, world, port, out):
