@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-coll", action="store_true", help="skip the standalone ReduceScatter / AllGather section")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--per-step", action="store_true", help="debug: per-step CUDA-event times to stderr")
     ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling period (ms)")
@@ -243,6 +244,57 @@ def fault_scenario(make_comm, run_step, healthy_ms, S, n, K, geom_m, strategy, g
     return out
 
 
+def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, reduce_max, pg):
+    """standalone ReduceScatter / AllGather on the same S-byte
+    n-shard buffers, healthy and with one channel of one rank dead (Balance;
+    the paper reports 85-89 % of normal throughput), NCCL beside.
+    busbw = (n-1)/n * S / t (nccl-tests convention for RS/AG)."""
+    import torch
+    import torch.distributed as dist
+    n = world
+    cnt = S // 2 // n
+    steps = max(5, min(a.steps, 50))
+    shard = recv[:cnt]
+    out = {}
+    busbw = lambda ms: (n - 1) / n * S / (ms * 1e-3) / 1e9  # noqa: E731
+    for strategy in ("BALANCE",):
+        for degraded in (False, True):
+            c = T.comm_from_env(R.config_default(nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads,
+                                                 chunk_bytes=a.chunk, max_bytes=S, strategy=strategy))
+            T.register(c, recv)
+            if degraded:   # the config-3 LINK fault, then the steady state with the channel dead
+                c.inject_fault(at_seq=1, kind="LINK", src_rank=3 % n, channel=5 % K, step=0, chunk=0,
+                               byte_offset=4096)
+            ops = {"reduce_scatter": lambda: T.reduce_scatter(c, send, shard, recvcount=cnt),
+                   "all_gather": lambda: T.all_gather(c, send[:cnt], recv, sendcount=cnt)}
+            for name, fn in ops.items():
+                for _ in range(3):
+                    fn()
+                barrier()
+                ms = reduce_max(timed(fn, steps, stream))
+                d = out.setdefault(name, {})
+                d["degraded_busbw" if degraded else "busbw"] = busbw(ms)
+                d["degraded_ms" if degraded else "ms"] = ms
+            assert c.sync() == R.SUCCESS
+            c.finalize()
+    for name, d in out.items():
+        d["degraded_over_healthy"] = d["degraded_busbw"] / d["busbw"]
+        d["degraded_over_bound"] = d["degraded_busbw"] / (d["busbw"] * (K - 1) / K)
+    if pg is not None:
+        rs_out = torch.empty(cnt, dtype=send.dtype, device="cuda")
+        ag_out = torch.empty(n * cnt, dtype=send.dtype, device="cuda")
+        nc = {"reduce_scatter": lambda: dist.reduce_scatter_tensor(rs_out, send[:n * cnt], group=pg),
+              "all_gather": lambda: dist.all_gather_into_tensor(ag_out, send[:cnt], group=pg)}
+        for name, fn in nc.items():
+            for _ in range(3):
+                fn()
+            barrier()
+            out[name]["nccl_busbw"] = busbw(reduce_max(timed(fn, steps, stream)))
+    out["note"] = ("S-byte n-shard buffer per rank (RS input / AG output), bf16; degraded = one LINK fault "
+                   "(rank 3 % n, ch 5), Balance; bound (K-1)/K of healthy")
+    return out
+
+
 def run_sim(a):
     """N = 1: k simulated ranks on one B200."""
     import torch
@@ -421,6 +473,9 @@ def run_multi(a):
                        "nvls": "disabled (NCCL_NVLS_ENABLE=0; the paper disabled SHARP)",
                        "version": ".".join(map(str, torch.cuda.nccl.version()))}
     comm.finalize()
+    if not a.no_coll and world >= 2:
+        res["collectives"] = coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, reduce_max,
+                                          pg if not a.no_nccl else None)
     if not a.no_fault and world >= 2:
         res["fault"] = []
         for strat in ("BALANCE", "HOT_REPAIR"):
@@ -495,6 +550,8 @@ def report(a, res, n_gpus, n_ranks, mode):
                        "result_equal_device_path": e["equal"], "api": "r2_allreduce_host (C ABI, pinned host buffers)"}
     if "nccl" in res:
         line["nccl_same_box"] = res["nccl"]
+    if "collectives" in res:
+        line["collectives"] = res["collectives"]
     if "fault" in res:
         line["fault"] = res["fault"]
     return line
