@@ -40,6 +40,16 @@ __device__ __forceinline__ unsigned int ld_acquire_sys(const volatile unsigned i
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const volatile unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Completion words are polled with RELAXED loads: the sender's
+// fence.acq_rel.sys before the word guarantees its payload is already
+// performed in this GPU's memory, and the payload is read through L2
+// (ld.global.cg), so no receiver-side sys-scope acquire is needed -- it cost
+// ~1.5 us per poll (tools/pingpong.cu, profiles/r01_pingpong.log).
 __device__ __forceinline__ unsigned int ld_relaxed_sys(const volatile unsigned int* p) {
   unsigned int v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -361,7 +371,7 @@ __device__ int poll_control(const Cta& k, Shared& sh) {
         sh.cause = STOP_HOST;
         return ST_STOP;
       }
-      if (ld_acquire_sys(&C->epoch) != sh.seen_epoch) return ST_REPLAN;
+      if (ld_acquire_gpu(&C->epoch) != sh.seen_epoch) return ST_REPLAN;
     }
   }
   return ST_OK;
@@ -593,7 +603,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
       return ST_STOP;
     }
   }
-  if (it.t > 0 && (int)(ld_acquire_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0) return ST_NOTREADY;
+  if (it.t > 0 && (int)(ld_relaxed_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0) return ST_NOTREADY;
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
@@ -679,7 +689,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
 // is acknowledged once no adopted chunk of the old plan is in flight.
 __device__ void apply_plan(const Cta& k, Shared& sh) {
   DevCtrl* C = k.me.dctrl;
-  const unsigned int e = ld_acquire_sys(&C->epoch);
+  const unsigned int e = ld_acquire_gpu(&C->epoch);
   sh.seen_epoch = e;
   sh.freeze = (int)ld_relaxed_sys(&C->freeze);
   sh.nent = (int)ld_relaxed_sys(&C->nentries);
@@ -890,7 +900,7 @@ __device__ void post_state(const Cta& k, const Shared& sh, unsigned int state, u
 __device__ void load_plan(Cta& k, Shared& sh) {
   if (k.tid == 0) {
     DevCtrl* C = k.me.dctrl;
-    unsigned int e = ld_acquire_sys(&C->epoch);
+    unsigned int e = ld_acquire_gpu(&C->epoch);
     sh.seen_epoch = e;
     sh.freeze = (int)ld_relaxed_sys(&C->freeze);
     sh.nent = (int)ld_relaxed_sys(&C->nentries);
@@ -956,7 +966,7 @@ __device__ int drain(Cta& k, Shared& sh) {
     const int nf = p.K * p.m;
     const unsigned int* fin = k.me.flags + fidx(p, p.fin_step, 0, 0);
     for (int i = k.tid; i < nf; i += k.nthr)
-      if ((int)(ld_acquire_sys(fin + i) - k.seq) < 0) ok = 0;
+      if ((int)(ld_relaxed_sys(fin + i) - k.seq) < 0) ok = 0;
     if (__syncthreads_and(ok)) {
       if (k.tid == 0) TRACE_MAX(k, 61);
       return ST_OK;
@@ -1162,7 +1172,6 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
       d[2] = p.recv_off[k.l];
       fence_sys();
       d[0] = k.seq;
-      fence_sys();
     }
   }
   __syncthreads();
