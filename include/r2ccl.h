@@ -107,6 +107,25 @@ typedef struct {
  *   channel_w         K integer weights (NULL = equal) for Balance
  *   sim_ranks         world == 1 only: k >= 1 simulated ranks on one GPU
  *                     (send/recv then hold k rank buffers back to back)
+ *   protocol          R2_PROTO_AUTO (default): per call, the alpha-beta model
+ *                     below picks SIMPLE or LL;
+ *                     R2_PROTO_SIMPLE / R2_PROTO_LL force one
+ *   ll_max_bytes      largest per-rank payload the LL protocol may carry
+ *                     (sizes its scratch: 4 x payload per rank; default 32 MiB,
+ *                     0 disables LL)
+ *   alpha_simple_ns, alpha_ll_ns, beta_mbps
+ *                     cost model: T = (#ring steps) * alpha + (wire bytes per
+ *                     rank) / beta, LL moving twice the bytes (defaults from
+ *                     profiles/r01_pingpong.log and r01_sizes_n4.jsonl)
+ *
+ * Protocols.  SIMPLE: 16-byte vectors straight into the peer's memory, one
+ * fence.acq_rel.sys per retired batch, then the completion word (P:33's
+ * work completion).  LL ("low latency", latency-bound sizes): every 16-byte
+ * vector travels as two 16-byte lines {w0, seq, w1, seq}, {w2, seq, w3, seq}
+ * into library scratch, self-validating at the receiver, so the completion
+ * word needs no fence; the receiver unpacks the last all-gather step locally
+ * (reading R-6).  Both keep the per-chunk completion words, rollback and
+ * re-placement unchanged.
  */
 typedef struct {
   int nchannels;
@@ -120,7 +139,13 @@ typedef struct {
   int channel_w[R2_MAX_CHANNELS];
   int use_channel_w;
   int sim_ranks;
+  int protocol;
+  size_t ll_max_bytes;
+  int alpha_simple_ns, alpha_ll_ns;
+  int beta_mbps;
 } r2_config_t;
+
+typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2 } r2_protocol_t;
 
 /*
  * An injected channel fault.  Fires in collective number
@@ -184,6 +209,7 @@ typedef struct {
   uint32_t dead_endpoints[R2_MAX_LOCAL * 4]; /* bit c of word r: endpoint (r,c) */
   uint32_t dead_links[R2_MAX_LOCAL * 4];     /* bit c of word r: link r->r+1    */
   uint64_t bytes[R2_MAX_LOCAL][R2_MAX_CHANNELS]; /* bytes pushed per local rank/channel */
+  int last_protocol;          /* r2_protocol_t the last enqueued collective used  */
 } r2_status_t;
 
 /* Fill *cfg with the defaults documented above. */

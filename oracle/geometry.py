@@ -27,6 +27,12 @@ to roundup(N, K*V) for the channel split (padding read as 0, never written).
     own memory -- reading R-5).
   * AllGather: steps t = 0..n-2 = the AllReduce's steps n-1..2n-3 (the owner
     sends its own shard at t = 0, then the ring forwards).
+
+LL protocol (ll=True, reading R-6): the all-gather data
+travels through library scratch as self-validating lines, so the receiver
+unpacks the last all-gather step itself: AllReduce and AllGather get one more
+step, a LOCAL item per (channel, chunk) whose input is the last step's
+completion word.  (The ReduceScatter already ends in a LOCAL final add.)
 """
 from __future__ import annotations
 
@@ -61,6 +67,7 @@ class Geometry:
     elem_bytes: int
     chunk_bytes: int          # the effective chunk (multiple of 16)
     op: str = ALLREDUCE       # N = per-shard count for REDUCE_SCATTER / ALL_GATHER
+    ll: bool = False          # LL protocol: + the LOCAL unpack step (AllReduce / AllGather)
 
     @property
     def V(self) -> int:
@@ -103,8 +110,11 @@ class Geometry:
         return self.n - 1 if self.op == ALL_GATHER else 0
 
     def local(self, t: int) -> bool:
-        """True for the ReduceScatter's final add (no connection used)."""
-        return self.op == REDUCE_SCATTER and t == self.n - 1
+        """True for a LOCAL item: the ReduceScatter's final add, or the LL
+        protocol's unpack of the last all-gather step (no connection used)."""
+        if self.op == REDUCE_SCATTER:
+            return t == self.n - 1
+        return self.ll and t == self.steps - 1
 
     @property
     def slice(self) -> int:
@@ -120,7 +130,8 @@ class Geometry:
 
     @property
     def steps(self) -> int:
-        return {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1}[self.op]
+        base = {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1}[self.op]
+        return base + (1 if self.ll and self.op != REDUCE_SCATTER else 0)
 
     def item_len(self, j: int) -> int:
         """Elements in chunk j of a channel slice."""

@@ -250,6 +250,8 @@ class Simulator:
         o0, o1 = e0 - s * g.stride, e1 - s * g.stride    # offsets inside the shard
         lim = g.shard_limit(s)
         r1 = (r + 1) % n
+        if g.local(t) and self.op != REDUCE_SCATTER:      # LL unpack: the data already landed here
+            return
         if ta <= n - 2:                                   # reduce-scatter hop
             val = self.xread(r, e0, e1, lim)
             if t > 0:

@@ -27,13 +27,15 @@ constexpr int kMaxInflight = 16;   // outstanding collectives per communicator
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
+ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, size_t ll_max_bytes) {
   ArenaLayout L{};
   const size_t q = (size_t)n * K * 16;
   L.slot_bytes = std::max<size_t>(align_up(std::max<size_t>(max_bytes, 16), q) / n, 16 * K);
   const size_t slice_cap = L.slot_bytes / K;
   L.m_cap = (int)std::max<size_t>((slice_cap + chunk - 1) / chunk, (size_t)W);
-  const int steps = n > 1 ? 2 * n - 2 : 1;
+  // LL: two 16-byte lines per 16-byte vector, one slot per ring step
+  L.ll_slot_bytes = ll_max_bytes ? 2 * std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K) : 0;
+  const int steps = n > 1 ? 2 * n - 1 : 1;     // + the LL unpack step
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -41,6 +43,7 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
     return o;
   };
   L.scratch = take((size_t)2 * std::max(n - 1, 1) * L.slot_bytes);
+  L.ll = take((size_t)2 * std::max(2 * n - 2, 1) * L.ll_slot_bytes);
   L.flags = take((size_t)steps * K * L.m_cap * 4);
   L.counters = take((size_t)steps * K * L.m_cap * 8);
   L.ep_dead = take((size_t)n * K * 4);
@@ -59,6 +62,7 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes) {
 RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
   RankPtrs p;
   p.scratch = base + L.scratch;
+  p.ll = base + L.ll;
   p.flags = (unsigned int*)(base + L.flags);
   p.counters = (unsigned long long*)(base + L.counters);
   p.ep_dead = (unsigned int*)(base + L.ep_dead);
@@ -184,6 +188,13 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->use_channel_w = 0;
   for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
   cfg->sim_ranks = 1;
+  cfg->protocol = R2_PROTO_AUTO;
+  cfg->ll_max_bytes = (size_t)32 << 20;   // covers the n = 8 crossover (~26 MB)
+  // fitted to the forced-protocol sweeps at n = 2 and 4 (profiles/r01_protocols_n{2,4}.jsonl):
+  // T(n=2) / T(n=4) = c + steps * alpha, crossovers 5 MB (n=2) and 12 MB (n=4)
+  cfg->alpha_simple_ns = 7150;     // per ring step, SIMPLE (fence + completion word + publish)
+  cfg->alpha_ll_ns = 2050;         // per ring step, LL (one line flight)
+  cfg->beta_mbps = 650000;         // per-GPU NVLink store rate at large sizes
 }
 
 extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,
@@ -223,13 +234,15 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     c->oob = *oob;
     c->has_oob = world > 1;
   }
-  c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes);
-  const int steps = c->n > 1 ? 2 * c->n - 2 : 1;
+  if (cfg.protocol < R2_PROTO_AUTO || cfg.protocol > R2_PROTO_LL) {
+    delete c;
+    return R2_ERR_INVALID_ARG;
+  }
+  c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes, cfg.ll_max_bytes);
   auto fail = [&](r2_result_t e) {
     delete c;
     return e;
   };
-  (void)steps;
   if (c->n > 1) {
     c->max_coop = r2_max_coop_ctas(c->threads);
     if (c->nlocal * c->K * c->W > c->max_coop) return fail(R2_ERR_INVALID_ARG);
@@ -320,7 +333,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     if (cudaHostAlloc(&h, c->health.size() * sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess)
       return fail(R2_ERR_CUDA);
     c->health_pinned = (uint32_t*)h;
-    const int steps_cap = c->n > 1 ? 2 * c->n - 2 : 1;
+    const int steps_cap = c->n > 1 ? 2 * c->n - 1 : 1;
     if (cudaHostAlloc(&h, (size_t)steps_cap * c->K * c->lay.m_cap * 4, cudaHostAllocDefault) != cudaSuccess)
       return fail(R2_ERR_CUDA);
     c->flags_pinned = (unsigned int*)h;
@@ -455,6 +468,22 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   if (e != R2_SUCCESS) return e;
   if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
   const uint32_t seq = (uint32_t)(c->seq + 1);
+  // protocol: alpha-beta model over the ring's steps; LL
+  // moves twice the bytes but pays no fence per step (r2ccl.h "Protocols")
+  bool ll = false;
+  const bool ll_fits = c->lay.ll_slot_bytes && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
+  if (c->cfg.protocol == R2_PROTO_LL) {
+    if (!ll_fits) return R2_ERR_INVALID_ARG;
+    ll = true;
+  } else if (c->cfg.protocol == R2_PROTO_AUTO && ll_fits) {
+    const double wire = (double)(op == R2_OP_ALLREDUCE ? 2 : 1) * (c->n - 1) * (double)g.shard * E;
+    const double bpns = std::max(c->cfg.beta_mbps, 1) / 1000.0;
+    const double t_simple = g.steps * (double)c->cfg.alpha_simple_ns + wire / bpns;
+    const double t_ll = (g.steps + (op != R2_OP_REDUCE_SCATTER)) * (double)c->cfg.alpha_ll_ns + 2 * wire / bpns;
+    ll = t_ll < t_simple;
+  }
+  const int steps = g.steps + (ll && op != R2_OP_REDUCE_SCATTER ? 1 : 0);   // + the LL unpack step
+  const int local_step = ll && op != R2_OP_REDUCE_SCATTER ? steps - 1 : g.local_step;
 
   LaunchParams p;
   memset(&p, 0, sizeof(p));
@@ -463,7 +492,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.K = c->K;
   p.W = c->W;
   p.m = g.m;
-  p.steps = g.steps;
+  p.steps = steps;
   p.nlocal = c->nlocal;
   p.first_rank = c->first_rank;
   p.dtype = dt == R2_INT32 ? R2D_INT32 : (dt == R2_FLOAT32 ? R2D_FLOAT32 : R2D_BF16);
@@ -471,9 +500,11 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.V = g.V;
   p.op = op;
   p.t0 = g.t0;
-  p.local_step = g.local_step;
-  p.fin_step = op == R2_OP_REDUCE_SCATTER ? c->n - 2 : g.steps - 1;
-  p.peer_recv = op != R2_OP_REDUCE_SCATTER;
+  p.local_step = local_step;
+  p.fin_step = local_step >= 0 ? local_step - 1 : steps - 1;   // last step with incoming words
+  p.peer_recv = !ll && op != R2_OP_REDUCE_SCATTER;
+  p.ll = ll;
+  p.ll_slot_bytes = c->lay.ll_slot_bytes;
   p.sstride = g.stride;
   p.slen = op == R2_OP_ALLREDUCE ? g.shard : count;
   // in-place (NCCL's convention for RS / AG: recv / send is the own shard)
@@ -528,7 +559,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
       repairs.push_back({f.src_rank, f.channel});
       continue;
     }
-    if (f.step >= g.steps || f.chunk >= g.m || f.step == g.local_step) continue;   // no such send: never fires
+    if (f.step >= steps || f.chunk >= g.m || f.step == local_step) continue;   // no such send: never fires
     if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
     FaultDev& d = p.faults[p.nfaults++];
     d.rank = f.src_rank;
@@ -560,9 +591,10 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
 
   LaunchInfo li{};
   li.seq = seq;
-  li.local_step = g.local_step;
+  li.local_step = local_step;
+  li.ll = ll;
   li.m = g.m;
-  li.steps = g.steps;
+  li.steps = steps;
   li.V = g.V;
   li.slice = g.slice;
   li.chunk = g.chunk;
@@ -587,6 +619,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     }
   }
   c->seq = seq;
+  c->last_protocol = ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
   int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W, c->threads, stream);
   c->last_stream = stream;
   if (rc != 0) return R2_ERR_CUDA;
@@ -748,6 +781,7 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->world = c->n;
     out->nlocal = c->nlocal;
     out->nchannels = c->K;
+    out->last_protocol = c->last_protocol;
     const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {

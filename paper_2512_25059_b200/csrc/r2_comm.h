@@ -49,7 +49,8 @@ struct Reg {
 
 struct LaunchInfo {                          // what the monitor needs about a seq
   uint32_t seq;
-  int local_step;                            // ReduceScatter's LOCAL step (own completion words) or -1
+  int local_step;                            // LOCAL step (own completion words) or -1
+  bool ll;                                   // LL protocol
   int m, steps, V;
   unsigned long long slice, chunk;
   int nfaults;
@@ -97,6 +98,7 @@ struct r2_comm {
   r2_config_t cfg{};
   int K = 8, W = 4, threads = 512;
   int trace = 0;                             // R2_TRACE=1: record the device timeline (r2_trace)
+  int last_protocol = 0;                     // r2_protocol_t of the last enqueued collective
   unsigned int weights[R2_MAXK]{};
   ArenaLayout lay{};
   r2_oob_t oob{};

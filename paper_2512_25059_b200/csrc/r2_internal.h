@@ -67,6 +67,7 @@ struct DevCtrl {
 
 struct RankPtrs {            // one rank's arena as seen from some process
   char* scratch;
+  char* ll;                  // LL line slots [2 parities][2n-2 steps][ll_slot_bytes]
   unsigned int* flags;
   unsigned long long* counters;
   unsigned int* ep_dead;
@@ -95,8 +96,9 @@ inline __host__ __device__ bool r2_dead_at(unsigned int dseq, unsigned int rseq,
 #endif
 
 struct ArenaLayout {
-  size_t scratch, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, dctrl, health, total;
+  size_t scratch, ll, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, dctrl, health, total;
   size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
+  size_t ll_slot_bytes;       // one LL slot (2 x the largest LL shard)
   int m_cap;
 };
 
@@ -147,6 +149,8 @@ struct LaunchParams {
   unsigned long long N, Np, shard, slice, chunk;   // elements (N: the whole user buffer)
   unsigned long long sstride, slen;      // shard stride in the user buffers / valid elements per shard
   size_t slot_bytes;
+  int ll;                                // LL protocol (r2ccl.h "Protocols")
+  size_t ll_slot_bytes;
   unsigned long long watchdog_ns;
   int trace;                             // record the r2_trace timeline
   int nfaults;

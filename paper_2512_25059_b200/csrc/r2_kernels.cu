@@ -69,11 +69,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// r2_trace timeline (LaunchParams.trace): slot layout in r2_internal.h
-#define TRACE_MIN(k, i) \
-  do { if ((k).p->trace) atomicMin(&(k).me.misc->trace[(i)], gtimer()); } while (0)
-#define TRACE_MAX(k, i) \
-  do { if ((k).p->trace) atomicMax(&(k).me.misc->trace[(i)], gtimer()); } while (0)
+// r2_trace timeline (LaunchParams.trace): slot layout in r2_internal.h.
+// trace = 1: min / max over all CTAs of the rank (contended atomics: they
+// stretch a latency-bound run by ~1-2 us per event); trace = 2: CTA 0 of the
+// rank only, plain stores (one lane's undisturbed timeline)
+#define TRACE_MIN(k, i)                                                                  \
+  do {                                                                                   \
+    if ((k).p->trace == 1) atomicMin(&(k).me.misc->trace[(i)], gtimer());                \
+    else if ((k).p->trace == 2 && (k).cta_in_rank == 0 && (k).me.misc->trace[(i)] == ~0ull) \
+      (k).me.misc->trace[(i)] = gtimer();                                                \
+  } while (0)
+#define TRACE_MAX(k, i)                                                                  \
+  do {                                                                                   \
+    if ((k).p->trace == 1) atomicMax(&(k).me.misc->trace[(i)], gtimer());                \
+    else if ((k).p->trace == 2 && (k).cta_in_rank == 0) (k).me.misc->trace[(i)] = gtimer(); \
+  } while (0)
 __device__ __forceinline__ uint4 ld_cg(const void* p) {
   uint4 v;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -185,6 +195,7 @@ struct Slot {                 // read by the data warps
   char* d_rem;
   char* d_loc;
   int rem_user, loc_user, rs;
+  int src_ll;                 // LL protocol: src is an LL slot (else user memory)
   int aligned;                // every user-buffer pointer 16-byte aligned (ReduceScatter /
                               // AllGather shards at a ragged stride may not be)
   unsigned long long e0;
@@ -215,6 +226,7 @@ struct Shared {
   unsigned long long first_adopt;
   unsigned long long wait_t0;
   unsigned long long t_poll, t_prev_poll;   // diagnostics
+  unsigned long long t_ctl;                 // last control / fabric check of try_publish
   unsigned int npoll;
   unsigned long long full[NSLOT];
   unsigned long long empty[NSLOT];
@@ -231,6 +243,7 @@ struct Cta {
   bool fault_channel;
   bool own_alive;
   unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
+  bool all_healthy;         // conn_mask covers every channel (LL speculation allowed)
   RankPtrs me, nx;
   Ctrl* ctrl;
   unsigned int total_items;
@@ -245,6 +258,43 @@ __device__ __forceinline__ size_t fidx(const LaunchParams& p, int t, int o, int 
 }
 __device__ __forceinline__ char* scratch_slot(const RankPtrs& rp, const LaunchParams& p, int par, int slot) {
   return rp.scratch + ((size_t)par * (p.n - 1) + slot) * p.slot_bytes;
+}
+
+// ------------------------------------------------------------ LL protocol
+// One 16-byte vector {w0, w1, w2, w3} travels as two 16-byte lines
+// {w0, seq, w1, seq}, {w2, seq, w3, seq} (r2ccl.h "Protocols"): a line is valid
+// when both its flags equal the collective's seq (stale lines of earlier
+// collectives carry older seqs), so the payload needs no fence.
+__device__ __forceinline__ char* ll_slot(const RankPtrs& rp, const LaunchParams& p, int par, int slot) {
+  return rp.ll + ((size_t)par * (2 * p.n - 2) + slot) * p.ll_slot_bytes;
+}
+__device__ __forceinline__ void ll_store(char* q, uint4 v, unsigned int seq) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(q), "r"(v.x), "r"(seq), "r"(v.y), "r"(seq)
+               : "memory");
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(q + 16), "r"(v.z), "r"(seq), "r"(v.w),
+               "r"(seq)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ll_line(const char* q) {
+  uint4 a;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w)
+               : "l"(q)
+               : "memory");
+  return a;
+}
+// The control lane publishes an LL item only after the sender's completion
+// word for its input (written after the sender issued every line), so the
+// lines are in flight and the spin is short; the abort word bounds it anyway.
+__device__ __forceinline__ uint4 ll_load(const char* q, unsigned int seq, const volatile unsigned int* abort_word) {
+  uint4 a = ll_line(q), b = ll_line(q + 16);
+  unsigned int spins = 0;
+  while (a.y != seq || a.w != seq || b.y != seq || b.w != seq) {
+    if ((++spins & 0x3FFu) == 0 && *abort_word == seq) break;
+    if (a.y != seq || a.w != seq) a = ll_line(q);
+    if (b.y != seq || b.w != seq) b = ll_line(q + 16);
+  }
+  return make_uint4(a.x, a.z, b.x, b.z);
 }
 
 // Balance part of channel c in an item of V vectors (reading C-15):
@@ -341,6 +391,29 @@ __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr,
       if (rem_user) st_user(d_rem + (size_t)v * 16, a, valid, E, aligned);
       else st_v4(d_rem + (size_t)v * 16, a);
     }
+    if (d_loc) {
+      if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E, aligned);
+      else st_v4(d_loc + (size_t)v * 16, a);
+    }
+  }
+}
+
+// LL item: src user memory (or an LL slot when src_ll), s_in an LL slot, d_rem
+// an LL slot at the peer, d_loc user memory / stage.  Padding vectors travel
+// as zeros so that the receiver can validate every line.
+template <int DT>
+__device__ void move_ll(const LaunchParams& p, unsigned int tid, unsigned int nthr, const char* src, bool src_ll,
+                        const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
+                        unsigned int nvec, unsigned long long lim, bool aligned, unsigned int seq,
+                        const volatile unsigned int* abort_word) {
+  const int E = p.elem_bytes, V = p.V;
+  for (unsigned int v = tid; v < nvec; v += nthr) {
+    const long long ev = (long long)(e0 + (unsigned long long)v * V);
+    const long long left = (long long)lim - ev;
+    const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+    uint4 a = src_ll ? ll_load(src + (size_t)v * 32, seq, abort_word) : ld_user(src + (size_t)v * 16, valid, E, aligned);
+    if (s_in) a = vadd<DT>(ll_load(s_in + (size_t)v * 32, seq, abort_word), a);
+    if (d_rem) ll_store(d_rem + (size_t)v * 32, a, seq);
     if (d_loc) {
       if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E, aligned);
       else st_v4(d_loc + (size_t)v * 16, a);
@@ -456,7 +529,7 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
       old = prev;
     }
     last = cnt == parts;
-    if (last) fence_sys();
+    if (last && !p.ll) fence_sys();
   }
   if (last) {
     // the completion word lives with its consumer: the receiver, or this rank
@@ -491,6 +564,36 @@ struct ItemRef {
 
 __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out) {
   const LaunchParams& p = *k.p;
+  if (k.all_healthy && !sh.dynamic && !sh.freeze) {
+    // healthy static plan: the lane's own chunks only, (t, c, j = w, w+W, ...)
+    // in order -- O(1) per item (the general walk below visits all K origins
+    // of every step, a few microseconds per item for one thread)
+    const int m = p.m, W = p.W;
+    while (it.t < p.steps) {
+      if (it.o < k.c) {
+        it.o = k.c;
+        it.j = k.w;
+      }
+      if (it.o == k.c && it.j < m) {
+        const int j = it.j;
+        it.j += W;
+        if (keyof(it.t, k.c, j) < k.own_next_key) continue;
+        out.t = it.t;
+        out.o = k.c;
+        out.j = j;
+        out.lo = 0;
+        out.hi = (unsigned int)((j == m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
+        out.parts = 1;
+        out.epoch = 0;
+        out.own = true;
+        return true;
+      }
+      it.o = 0;
+      it.j = k.w;
+      it.t++;
+    }
+    return false;
+  }
   while (it.t < p.steps) {
     const int t = it.t, o = it.o;
     const bool own = (o == k.c) && k.own_alive;
@@ -595,19 +698,39 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
       poison = f.poison;
     }
   }
+  // control words and the emulated fabric state: at most once per ~10 us
+  // (40k SM cycles; each check is a handful of global loads, ~2.5 us per
+  // publish when done every time -- it was the latency floor of small LL
+  // collectives).  Faults of this lane's own channel stop it
+  // deterministically (above); a death caused elsewhere, a stop or a new
+  // plan is noticed within the interval (failover takes ~300 us).
   if (first_try) {
-    const int st = poll_control(k, sh);
-    if (st != ST_OK) return st;
-    if (conn_phys_dead(k)) {
-      sh.cause = STOP_DEATH;
-      return ST_STOP;
+    const unsigned long long now = (unsigned long long)clock64();   // SM cycles: cheap to read
+    if (now - sh.t_ctl >= 40000ull || sh.t_ctl == 0) {
+      sh.t_ctl = now;
+      const int st = poll_control(k, sh);
+      if (st != ST_OK) return st;
+      if (conn_phys_dead(k)) {
+        sh.cause = STOP_DEATH;
+        return ST_STOP;
+      }
     }
   }
-  if (it.t > 0 && (int)(ld_relaxed_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0) return ST_NOTREADY;
+  // LL speculation: while this rank's plan is the healthy static one (no
+  // alert, no adoption), an LL item is published before its input's
+  // completion word -- the data warps wait on the self-validating lines
+  // themselves, so a ring step costs one line flight instead of line + word.
+  // Deadlock-free: every lane then holds only its own items, in key order,
+  // and an own item's inputs never depend on a later item of the same lane.
+  // Once alerted, items wait for the completion word again (an adopted
+  // residual must never queue behind a spinning item that needs it).
+  const bool spec = p.ll && k.all_healthy && !sh.alerted && !sh.dynamic;
+  if (it.t > 0 && !spec && (int)(ld_relaxed_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0)
+    return ST_NOTREADY;
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
-  if (ta >= n - 1 && !local && !try_recv_next(k, sh)) return ST_NOTREADY;
+  if (p.peer_recv && ta >= n - 1 && !local && !try_recv_next(k, sh)) return ST_NOTREADY;
 
   const int E = p.elem_bytes, V = p.V;
   const int s_ = (ta <= n - 2) ? ((k.r - 1 - ta) % n + n) % n : ((k.r - (ta - n + 1)) % n + n) % n;
@@ -625,7 +748,53 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   d.e0 = e0;
   d.lim = sbase + p.slen < p.N ? sbase + p.slen : p.N;
   d.rs = ta <= n - 2;
-  if (ta <= n - 2) {                                  // reduce-scatter hop
+  d.src_ll = 0;
+  if (p.ll) {
+    // LL: scratch traffic as lines; slot index = the AllReduce step that sends
+    // into it (RS hops 0..n-2, AG sends n-1..2n-3), offsets doubled
+    const unsigned long long lo = off * E * 2;
+    d.rs = 1;                                         // d_rem is library scratch
+    if (ta <= n - 2) {                                // reduce-scatter hop
+      d.src = p.send[k.l] + e0 * E;
+      d.s_in = t > 0 ? ll_slot(k.me, p, k.par, ta - 1) + lo : nullptr;
+      d.d_rem = ll_slot(k.nx, p, k.par, ta) + lo;
+      d.d_loc = nullptr;
+      d.loc_user = 0;
+    } else if (ta == n - 1 && p.op == R2_OP_ALLREDUCE) {   // final add + first all-gather send
+      d.src = p.send[k.l] + e0 * E;
+      d.s_in = ll_slot(k.me, p, k.par, n - 2) + lo;
+      d.d_rem = ll_slot(k.nx, p, k.par, n - 1) + lo;
+      d.d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
+      d.loc_user = !p.inplace;
+    } else if (ta == n - 1 && p.op == R2_OP_REDUCE_SCATTER) {   // final add into the own output
+      d.src = p.send[k.l] + e0 * E;
+      d.s_in = ll_slot(k.me, p, k.par, n - 2) + lo;
+      d.d_rem = nullptr;
+      d.d_loc = p.recv[k.l] + off * E;
+      d.loc_user = 1;
+    } else if (ta == n - 1) {                         // all-gather: the owner sends its own shard
+      d.src = p.send[k.l] + off * E;
+      d.s_in = nullptr;
+      d.d_rem = ll_slot(k.nx, p, k.par, n - 1) + lo;
+      d.d_loc = p.ag_inplace ? nullptr : (p.recv[k.l] + e0 * E);
+      d.loc_user = 1;
+    } else if (!local) {                              // all-gather forward: unpack + send on
+      d.src = ll_slot(k.me, p, k.par, ta - 1) + lo;
+      d.src_ll = 1;
+      d.s_in = nullptr;
+      d.d_rem = ll_slot(k.nx, p, k.par, ta) + lo;
+      d.d_loc = p.recv[k.l] + e0 * E;
+      d.loc_user = 1;
+    } else {                                          // the last all-gather step, unpacked locally
+      d.src = ll_slot(k.me, p, k.par, ta - 1) + lo;
+      d.src_ll = 1;
+      d.s_in = nullptr;
+      d.d_rem = nullptr;
+      d.d_loc = p.recv[k.l] + e0 * E;
+      d.loc_user = 1;
+    }
+    d.rem_user = 0;
+  } else if (ta <= n - 2) {                           // reduce-scatter hop
     d.src = p.send[k.l] + e0 * E;
     d.s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
     d.d_rem = scratch_slot(k.nx, p, k.par, t) + off * E;
@@ -661,7 +830,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     d.d_loc = nullptr;
     d.loc_user = 0;
   }
-  d.aligned = ((((unsigned long long)d.src) | (d.rem_user ? (unsigned long long)d.d_rem : 0ull) |
+  d.aligned = ((((d.src_ll ? 0ull : (unsigned long long)d.src)) | (d.rem_user ? (unsigned long long)d.d_rem : 0ull) |
                 (d.loc_user ? (unsigned long long)d.d_loc : 0ull)) & 15ull) == 0;
   m.kind = fire ? META_FIRE : META_ITEM;
   m.local = local;
@@ -734,7 +903,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
     if (nd) {
       bool any = false;
       for (unsigned int i = 0; i < nd; ++i) any |= sh.meta[(sh.fin + i) % NSLOT].kind != META_END;
-      if (any) fence_sys();
+      if (any && !p.ll) fence_sys();   // LL lines validate themselves: no fence
       for (unsigned int i = 0; i < nd; ++i) {
         const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
         if (m.kind == META_ITEM) {
@@ -787,6 +956,10 @@ __device__ int control_run(Cta& k, Shared& sh) {
         have = false;
       }
     }
+    // 2b. an abort / timeout also releases data warps spinning on LL lines
+    if ((pending == ST_ABORT || pending == ST_TIMEOUT) && sh.fin != sh.pub &&
+        ld_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq) != k.seq)
+      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
     // 3. done: everything published is retired -> END releases the data warps
     if ((!have || pending != ST_OK) && sh.fin == sh.pub && !ack_epoch) {
       const unsigned int u = sh.pub % NSLOT;
@@ -856,15 +1029,27 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     const unsigned int u = dcount % NSLOT, ph = (dcount / NSLOT) & 1u;
     mbar_wait(&sh.full[u], ph);
     ++dcount;
+    if (p.trace == 2 && k.cta_in_rank == 0 && k.tid == 32 && dcount <= 8)
+      k.me.misc->trace[40 + dcount - 1] = gtimer();   // data warps take item dcount-1
     const Slot d = sh.slot[u];
     if (d.status == SLOT_END) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.empty[u]);
       return;
     }
-    move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
-             d.aligned != 0);
-    if (d.poison && d.d_rem) {
+    if (p.ll)
+      move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
+                  d.lim, d.aligned != 0, k.seq, &k.me.misc->abort_seq);
+    else
+      move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
+               d.aligned != 0);
+    if (d.poison && d.d_rem && p.ll) {
+      // LL: the rest of the faulted part arrives as invalid lines (reading C-6)
+      for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {
+        st_v4(d.d_rem + (size_t)v * 32, make_uint4(~0u, ~0u, ~0u, ~0u));
+        st_v4(d.d_rem + (size_t)v * 32 + 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+      }
+    } else if (d.poison && d.d_rem) {
       // poison the rest of the faulted part at the peer (reading C-6)
       for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {
         const long long ev = (long long)(d.e0 + (unsigned long long)v * p.V);
@@ -875,6 +1060,8 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
       }
     }
     __syncwarp();
+    if (p.trace == 2 && k.cta_in_rank == 0 && k.tid == 32 && dcount <= 8)
+      k.me.misc->trace[48 + dcount - 1] = gtimer();   // warp 1 done with item dcount-1
     if (lane == 0) mbar_arrive(&sh.empty[u]);
   }
 }
@@ -1136,6 +1323,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     k.conn_mask = mask;
   }
   k.own_alive = (k.conn_mask >> k.c) & 1u;
+  k.all_healthy = k.conn_mask == (p.K >= 32 ? 0xFFFFFFFFu : ((1u << p.K) - 1u));
   k.own_next_key = 0;
   k.fault_channel = false;
   for (int i = 0; i < p.nfaults; ++i)
@@ -1161,6 +1349,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     sh.first_adopt = 0;
     sh.wait_t0 = 0;
     sh.t_poll = sh.t_prev_poll = 0;
+    sh.t_ctl = 0;
     sh.npoll = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;

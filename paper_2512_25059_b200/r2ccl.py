@@ -44,7 +44,12 @@ class Config(C.Structure):
     _fields_ = [("nchannels", C.c_int), ("ctas_per_channel", C.c_int), ("threads_per_cta", C.c_int),
                 ("chunk_bytes", C.c_size_t), ("max_bytes", C.c_size_t), ("strategy", C.c_int),
                 ("probe_timeout_us", C.c_int), ("watchdog_ms", C.c_int),
-                ("channel_w", C.c_int * MAX_CHANNELS), ("use_channel_w", C.c_int), ("sim_ranks", C.c_int)]
+                ("channel_w", C.c_int * MAX_CHANNELS), ("use_channel_w", C.c_int), ("sim_ranks", C.c_int),
+                ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
+                ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int)]
+
+
+PROTO_AUTO, PROTO_SIMPLE, PROTO_LL = 0, 1, 2
 
 
 class Fault(C.Structure):
@@ -92,7 +97,7 @@ class Status(C.Structure):
     _fields_ = [("seq", C.c_uint64), ("last_error", C.c_int), ("last_error_seq", C.c_uint64),
                 ("n_events", C.c_int), ("world", C.c_int), ("nlocal", C.c_int), ("nchannels", C.c_int),
                 ("dead_endpoints", C.c_uint32 * (MAX_LOCAL * 4)), ("dead_links", C.c_uint32 * (MAX_LOCAL * 4)),
-                ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL)]
+                ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int)]
 
 
 class Geometry(C.Structure):
@@ -176,6 +181,8 @@ def config_default(**kw) -> Config:
             cfg.use_channel_w = 1
         elif k == "strategy" and isinstance(v, str):
             cfg.strategy = {"HOT_REPAIR": HOT_REPAIR, "BALANCE": BALANCE}[v]
+        elif k == "protocol" and isinstance(v, str):
+            cfg.protocol = {"AUTO": PROTO_AUTO, "SIMPLE": PROTO_SIMPLE, "LL": PROTO_LL}[v]
         else:
             setattr(cfg, k, v)
     return cfg
@@ -328,7 +335,8 @@ class Comm:
                 "n_events": s.n_events,
                 "dead_endpoints": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_endpoints[r] >> c) & 1),
                 "dead_links": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_links[r] >> c) & 1),
-                "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)]}
+                "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)],
+                "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE")}
 
     def events(self) -> list:
         st = Status()

@@ -43,9 +43,12 @@ def poisoned(n: int, N: int, dtype: str) -> torch.Tensor:
     return t
 
 
-def sim_comm(n, K=4, W=2, chunk_bytes=64 * 1024, max_bytes=16 << 20, strategy="BALANCE", **kw) -> R.Comm:
+def sim_comm(n, K=4, W=2, chunk_bytes=64 * 1024, max_bytes=16 << 20, strategy="BALANCE", protocol="SIMPLE",
+             **kw) -> R.Comm:
+    """Simulated-rank communicator.  The protocol is pinned (SIMPLE unless a
+    test asks for LL / AUTO) so that the oracle's step list is known."""
     cfg = R.config_default(sim_ranks=n, nchannels=K, ctas_per_channel=W, chunk_bytes=chunk_bytes,
-                           max_bytes=max_bytes, strategy=strategy, **kw)
+                           max_bytes=max_bytes, strategy=strategy, protocol=protocol, **kw)
     return R.Comm(0, 1, torch.cuda.current_device(), None, cfg)
 
 

@@ -52,8 +52,9 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     rc = comm.sync()
     E = r2inputs.elem_bytes(dtype)
     cfg = comm.cfg
+    ll = comm.status()["last_protocol"] == "LL"      # the alpha-beta choice (f3) shapes the step list
     g = Geometry(world, cfg.nchannels, N, E,
-                 effective_chunk_bytes(N, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel))
+                 effective_chunk_bytes(N, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel), ll=ll)
     y = OS.allreduce(xs, g.shard, dtype)
     ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), y.view(np.uint8))
     evs = [norm_event(e) for e in comm.events()[ne:]]
@@ -61,7 +62,8 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     dist.all_gather_object(all_evs, evs)
     oks = [None] * world
     dist.all_gather_object(oks, bool(ok))
-    out = {"N": N, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc, "ok": all(oks)}
+    out = {"N": N, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc, "ok": all(oks),
+           "protocol": "LL" if ll else "SIMPLE"}
     if faults:
         got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
         res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, inplace=inplace,
@@ -107,6 +109,7 @@ def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", 
     else:
         T.all_gather(comm, send, recv, sendcount=count)
     rc = comm.sync()
+    ll = comm.status()["last_protocol"] == "LL"
     ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), np.asarray(want).view(np.uint8))
     evs = [norm_event(e) for e in comm.events()[ne:]]
     all_evs = [None] * world
@@ -114,11 +117,11 @@ def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", 
     oks = [None] * world
     dist.all_gather_object(oks, bool(ok))
     out = {"op": op, "N": count, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc,
-           "inplace": inplace, "ok": all(oks)}
+           "inplace": inplace, "ok": all(oks), "protocol": "LL" if ll else "SIMPLE"}
     if faults:
         cfg = comm.cfg
         g = Geometry(world, cfg.nchannels, count, E, effective_chunk_bytes(
-            count, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel, op), op)
+            count, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel, op), op, ll=ll)
         got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
         res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, health=health,
                           faults=[OP.Fault(f["kind"], f["src_rank"], f["channel"], f["step"], f["chunk"],
@@ -160,6 +163,18 @@ def main():
             # degraded steady state (channel 1 of rank world-1 now dead): static plan
             results.append(case(comm, rank, world, 1 << 20, "float32", seed=12))
             comm.finalize()
+        # the LL protocol (f3) forced, over the real NVLink path
+        cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=16 * 1024, max_bytes=16 << 20,
+                               protocol="LL")
+        comm = T.comm_from_env(cfg)
+        for dtype, N in (("bfloat16", 100_003), ("float32", 1 << 16), ("int32", 5)):
+            results.append(case(comm, rank, world, N, dtype, seed=N + 1))
+        results.append(case(comm, rank, world, 77_777, "bfloat16", inplace=True, seed=2))
+        for op in ("reduce_scatter", "all_gather"):
+            results.append(case_op(comm, rank, world, op, 33_333, "bfloat16", seed=4))
+        f = dict(kind="LINK", src_rank=world - 1, channel=1, step=1, chunk=1, byte_offset=4096, poison=1)
+        results.append(case(comm, rank, world, 1 << 19, "bfloat16", [f], "BALANCE", seed=19))
+        comm.finalize()
         if world >= 2:
             cfg = R.config_default(nchannels=3, ctas_per_channel=2, chunk_bytes=32 * 1024, max_bytes=64 << 20)
             comm = T.comm_from_env(cfg)

@@ -198,3 +198,37 @@ def test_static_degraded_plan(op, strategy):
     for r in range(n):
         assert same(res.y[r], want[r])
     assert res.bytes_sent[1, 2] == 0
+
+
+# ------------------------------------------------------------ LL protocol (f3)
+
+@pytest.mark.parametrize("op", ["allreduce", REDUCE_SCATTER, ALL_GATHER])
+def test_ll_geometry_adds_unpack_step(op):
+    """Reading R-6: LL adds one LOCAL unpack step to AllReduce / AllGather; the
+    ReduceScatter already ends in a LOCAL final add."""
+    n, K, count = 4, 2, 1000
+    g0 = Geometry(n, K, count, 4, 256, op)
+    g1 = Geometry(n, K, count, 4, 256, op, ll=True)
+    extra = 0 if op == REDUCE_SCATTER else 1
+    assert g1.steps == g0.steps + extra
+    assert [t for t in range(g1.steps) if g1.local(t)] == [g1.steps - 1]
+
+
+@pytest.mark.parametrize("op", ["allreduce", REDUCE_SCATTER, ALL_GATHER])
+@pytest.mark.parametrize("strategy", [BALANCE, HOT_REPAIR])
+def test_ll_brute_force_single_fault(op, strategy):
+    """The LL step list under every single fault point: buffers == Layer 1;
+    unpack items are never fault points and are re-placed with the residual."""
+    n, K, m, vpc = 3, 3, 2, 2
+    count = (n * K if op == "allreduce" else K) * m * vpc * 4
+    g = Geometry(n, K, count, 4, vpc * 16, op, ll=True)
+    assert g.m == m
+    xs = (r2inputs.inputs(n, count, "int32", seed=99) if op == "allreduce" else op_inputs(op, n, count, "int32", 99))
+    want = [S.allreduce(xs, g.shard, "int32")] * n if op == "allreduce" else expected(op, xs, g, "int32")
+    for i, (r, c, t, j) in enumerate(itertools.product(range(n), range(K), range(g.steps), range(m))):
+        f = Fault("LINK", r, c, t, j, 16)
+        res = run(op, xs, g, "int32", faults=[f], strategy=strategy, seed=i)
+        assert res.error is None, f
+        for rr in range(n):
+            assert same(res.y[rr], want[rr]), (f, rr)
+        assert (len(res.fired) == 0) == g.local(t), f

@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--dtypes", default="bf16,fp32")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--sim-ranks", type=int, default=8)
+    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
+    ap.add_argument("--no-nccl", action="store_true")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -45,13 +47,14 @@ def main():
     n = a.sim_ranks if sim else world
     W = a.ctas or (2 if sim else 16)
     if sim:
-        comm = R.Comm(0, 1, 0, None, R.config_default(sim_ranks=n, nchannels=8, ctas_per_channel=W,
+        comm = R.Comm(0, 1, 0, None, R.config_default(sim_ranks=n, nchannels=8, ctas_per_channel=W, protocol=a.protocol,
                                                       max_bytes=maxb))
         reduce_max = lambda x: x
         barrier = torch.cuda.synchronize
     else:
         dist.init_process_group("gloo")
-        comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=maxb))
+        comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=maxb, protocol=a.protocol,
+                                                ll_max_bytes=min(maxb, 32 << 20)))
         os.environ["NCCL_NVLS_ENABLE"] = "0"
         saved = os.dup(1)
         os.dup2(2, 1)
@@ -94,8 +97,8 @@ def main():
             ms = reduce_max(timed(fn, iters, stream))
             assert comm.sync() == R.SUCCESS
             out = {"dtype": dt, "bytes": S, "ranks": n, "mode": "sim" if sim else "gpus", "r2_ms": ms,
-                   "r2_busbw": 2 * (n - 1) / n * S / (ms * 1e-3) / 1e9}
-            if not sim:
+                   "r2_busbw": 2 * (n - 1) / n * S / (ms * 1e-3) / 1e9, "protocol": comm.status()["last_protocol"]}
+            if not sim and not a.no_nccl:
                 buf = send[0, :cnt] if send.dim() == 2 else send[:cnt]
                 f2 = lambda: dist.all_reduce(buf, group=pg)
                 for _ in range(3):

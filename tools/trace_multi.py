@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["R2_TRACE"] = "1"
+os.environ.setdefault("R2_TRACE", "1")
 from paper_2512_25059_b200 import r2ccl as R  # noqa: E402
 from paper_2512_25059_b200 import torch_api as T  # noqa: E402
 
@@ -27,8 +27,9 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     W = int(os.environ.get("W", 16))
     sizes = [int(s) for s in os.environ.get("SIZES", "65536,16777216,268435456").split(",")]
-    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=max(sizes)))
-    steps = 2 * world - 2
+    proto = os.environ.get("PROTO", "AUTO")
+    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=max(sizes), protocol=proto))
+    steps = 2 * world - 1
     for S in sizes:
         x = torch.randn(S // 2, device="cuda").to(torch.bfloat16)
         y = torch.empty_like(x)
@@ -49,9 +50,12 @@ def main():
         rel = lambda v: (v - b) / 1e3 if 0 < v < (1 << 63) and v >= b else float("nan")  # noqa: E731
         pub = " ".join(f"{rel(tr[32 + t]):.1f}" for t in range(steps))
         ret = " ".join(f"{rel(tr[4 + t]):.1f}" for t in range(steps))
-        line = (f"[rank {rank}] S={S >> 10}KiB event {e0.elapsed_time(e1) * 1e3:.1f}us | init {rel(tr[1]):.1f} "
+        line = (f"[rank {rank}] {comm.status()['last_protocol']} S={S >> 10}KiB event {e0.elapsed_time(e1) * 1e3:.1f}us | init {rel(tr[1]):.1f} "
                 f"first-pub {rel(tr[2]):.1f} | step first-publish: {pub} | step last-retire: {ret} | ctl-end "
                 f"{rel(tr[60]):.1f} drain {rel(tr[61]):.1f} exit {rel(tr[62]):.1f}")
+        if os.environ.get("R2_TRACE") == "2":
+            line += " | data take: " + " ".join(f"{rel(tr[40 + i]):.1f}" for i in range(steps))
+            line += " | data done: " + " ".join(f"{rel(tr[48 + i]):.1f}" for i in range(steps))
         for r in range(world):
             if r == rank:
                 print(line, file=sys.stderr, flush=True)
