@@ -60,8 +60,11 @@ typedef enum {
   R2_FAULT_LOCAL = 0,   /* sender endpoint (src_rank, channel) dies           */
   R2_FAULT_REMOTE = 1,  /* receiver endpoint (src_rank+1, channel) dies       */
   R2_FAULT_LINK = 2,    /* ring link src_rank -> src_rank+1 on channel dies   */
-  R2_FAULT_REPAIR = 3   /* re-admit (src_rank, channel): stand-in for the
+  R2_FAULT_REPAIR = 3,  /* re-admit (src_rank, channel): stand-in for the
                            periodic re-probe of P:19 / S:345                  */
+  R2_FAULT_HEAL = 4     /* the emulated endpoint (src_rank, channel) and link
+                           src_rank -> src_rank+1 recover before at_seq; the
+                           library learns it only by re-probing (f4)    */
 } r2_fault_kind_t;
 
 /* Probe outcomes and verdicts (reading C-10). */
@@ -113,6 +116,10 @@ typedef struct {
  *   ll_max_bytes      largest per-rank payload the LL protocol may carry
  *                     (sizes its scratch: 4 x payload per rank; default 32 MiB,
  *                     0 disables LL)
+ *   reprobe_us        first re-probe of a dead connection after this many
+ *                     microseconds, then exponential back-off ("adapting
+ *                     probe frequency"); default 2000, 0 disables re-probing
+ *   reprobe_max_us    back-off cap (default 200000)
  *   alpha_simple_ns, alpha_ll_ns, beta_mbps
  *                     cost model: T = (#ring steps) * alpha + (wire bytes per
  *                     rank) / beta, LL moving twice the bytes (defaults from
@@ -143,6 +150,7 @@ typedef struct {
   size_t ll_max_bytes;
   int alpha_simple_ns, alpha_ll_ns;
   int beta_mbps;
+  int reprobe_us, reprobe_max_us;
 } r2_config_t;
 
 typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2 } r2_protocol_t;
@@ -210,6 +218,8 @@ typedef struct {
   uint32_t dead_links[R2_MAX_LOCAL * 4];     /* bit c of word r: link r->r+1    */
   uint64_t bytes[R2_MAX_LOCAL][R2_MAX_CHANNELS]; /* bytes pushed per local rank/channel */
   int last_protocol;          /* r2_protocol_t the last enqueued collective used  */
+  int n_readmits;             /* connections re-admitted after a successful re-probe */
+  int n_reprobes;             /* re-probe rounds run                              */
 } r2_status_t;
 
 /* Fill *cfg with the defaults documented above. */

@@ -119,3 +119,13 @@ def dead_after_verdict(v: str, a: int, b: int) -> tuple[list[int], bool]:
     if v in (LINK, INCONCLUSIVE):
         return [], True
     return [], False
+
+
+def reprobe_readmits(a: int, b: int, c: int, n: int, ep_dead, link_dead) -> bool:
+    """"R²CCL also periodically reprobes to detect component recovery
+    (e.g., NIC resets, cable fixes)".  A re-probe of the dead connection
+    (A -> B, c) is an ordinary round (run_round); the connection is usable
+    again exactly when the round finds nothing wrong, i.e. the verdict is NONE
+    (A->B and B->A both succeed: both endpoints and the link between them are
+    alive, reading C-11)."""
+    return run_round(a, b, c, n, ep_dead, link_dead)["verdict"] == NONE

@@ -195,6 +195,8 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->alpha_simple_ns = 7150;     // per ring step, SIMPLE (fence + completion word + publish)
   cfg->alpha_ll_ns = 2050;         // per ring step, LL (one line flight)
   cfg->beta_mbps = 650000;         // per-GPU NVLink store rate at large sizes
+  cfg->reprobe_us = 2000;
+  cfg->reprobe_max_us = 200000;
 }
 
 extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,
@@ -443,10 +445,10 @@ extern "C" r2_result_t r2_deregister(r2_comm_t c, uint64_t reg) {
 
 extern "C" r2_result_t r2_inject_fault(r2_comm_t c, const r2_fault_t* f) {
   if (!c || !f) return R2_ERR_INVALID_ARG;
-  if (f->kind < R2_FAULT_LOCAL || f->kind > R2_FAULT_REPAIR) return R2_ERR_INVALID_ARG;
+  if (f->kind < R2_FAULT_LOCAL || f->kind > R2_FAULT_HEAL) return R2_ERR_INVALID_ARG;
   if (f->src_rank < 0 || f->src_rank >= c->n || f->channel < 0 || f->channel >= c->K) return R2_ERR_INVALID_ARG;
   if (f->origin_channel < -1 || f->origin_channel >= c->K) return R2_ERR_INVALID_ARG;
-  if (f->kind != R2_FAULT_REPAIR && (f->step < 0 || f->chunk < 0)) return R2_ERR_INVALID_ARG;
+  if (f->kind <= R2_FAULT_LINK && (f->step < 0 || f->chunk < 0)) return R2_ERR_INVALID_ARG;
   if (f->at_seq <= c->seq) return R2_ERR_INVALID_ARG;   // must precede the targeted collective
   c->faults.push_back(*f);
   return R2_SUCCESS;
@@ -551,12 +553,13 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     p.recv_off[0] = (unsigned long long)((char*)recv - c->regs[found].dptr);
   }
 
-  // faults armed for this seq; REPAIRs take effect before it (stand-in for re-probe)
-  std::vector<std::pair<int, int>> repairs;
+  // faults armed for this seq; REPAIRs take effect before it (stand-in for
+  // re-probe); HEALs only repair the emulated fabric (found by re-probing)
+  std::vector<std::pair<int, int>> repairs, heals;
   for (const r2_fault_t& f : c->faults) {
     if (f.at_seq != seq) continue;
-    if (f.kind == R2_FAULT_REPAIR) {
-      repairs.push_back({f.src_rank, f.channel});
+    if (f.kind == R2_FAULT_REPAIR || f.kind == R2_FAULT_HEAL) {
+      (f.kind == R2_FAULT_REPAIR ? repairs : heals).push_back({f.src_rank, f.channel});
       continue;
     }
     if (f.step >= steps || f.chunk >= g.m || f.step == local_step) continue;   // no such send: never fires
@@ -577,11 +580,16 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     // REPAIR re-admits (rank, channel) from this seq on (seq-indexed: no
     // ordering against collectives already in flight is needed)
     for (auto& rc : repairs) r2_declare_repaired(c, rc.first, rc.second, seq);
-    if (!repairs.empty() && r2_push_health(c) != 0) return R2_ERR_CUDA;
+    // connections the monitor's re-probes found healthy again (f4)
+    const bool readmit = !c->readmit_pending.empty();
+    for (auto& rc : c->readmit_pending) r2_declare_conn_repaired(c, rc.first, rc.second, seq);
+    c->readmit_pending.clear();
+    if ((!repairs.empty() || readmit) && r2_push_health(c) != 0) return R2_ERR_CUDA;
     for (int l = 0; l < c->nlocal; ++l)
       if (!r2_conn_mask_at(c, c->first_rank + l, seq)) return R2_ERR_NO_BACKUP;   // known exhausted
   }
   // the emulated fabric heals in stream order
+  for (auto& h : heals) repairs.push_back(h);
   for (auto& rc : repairs)
     for (int l = 0; l < c->nlocal; ++l) {
       const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
@@ -782,6 +790,8 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->nlocal = c->nlocal;
     out->nchannels = c->K;
     out->last_protocol = c->last_protocol;
+    out->n_readmits = c->n_readmits;
+    out->n_reprobes = c->n_reprobes;
     const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {

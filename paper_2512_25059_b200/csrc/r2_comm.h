@@ -60,6 +60,7 @@ struct LaunchInfo {                          // what the monitor needs about a s
 struct Round {                               // one triangulation round
   uint32_t id, seq;
   int a, b, aux, channel, local;             // local: index of A in this process
+  bool reprobe;                              // recovery check of a dead connection: local only
   int outcomes[4];
   int need;
   uint64_t t_start;
@@ -99,6 +100,14 @@ struct r2_comm {
   int K = 8, W = 4, threads = 512;
   int trace = 0;                             // R2_TRACE=1: record the device timeline (r2_trace)
   int last_protocol = 0;                     // r2_protocol_t of the last enqueued collective
+  // re-probing of dead connections ("periodically reprobes to detect
+  // component recovery ... adapting probe frequency")
+  struct Reprobe { int r, ch; uint64_t next_ns, interval_ns; uint32_t round_id; };
+  std::vector<Reprobe> reprobes;             // monitor only
+  std::vector<std::pair<int, int>> readmit_pending;   // (rank, channel) -> next enqueue (mu)
+  int n_readmits = 0, n_reprobes = 0;        // (mu)
+  uint64_t reprobe_scan_ns = 0;
+  uint32_t reprobe_counter = 0;
   unsigned int weights[R2_MAXK]{};
   ArenaLayout lay{};
   r2_oob_t oob{};
@@ -210,5 +219,6 @@ bool r2_ep_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
 bool r2_link_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
 void r2_declare_dead(r2_comm* comm, int kind, int r, int c, uint32_t from_seq);   // kind 0 ep, 1 link
 void r2_declare_repaired(r2_comm* comm, int r, int c, uint32_t at_seq);
+void r2_declare_conn_repaired(r2_comm* comm, int r, int c, uint32_t at_seq);   // ep r, ep r+1, link r
 int r2_push_health(r2_comm* comm);                                     // mirror to every local arena
 cudaError_t r2_spin_sync(cudaStream_t s);

@@ -175,6 +175,21 @@ void r2_declare_repaired(r2_comm* c, int r, int k, uint32_t at_seq) {
   }
 }
 
+// A successful re-probe of connection r -> r+1 on channel k proves both
+// endpoints and the link alive: close those three records (only open
+// intervals, as r2_declare_repaired).
+void r2_declare_conn_repaired(r2_comm* c, int r, int k, uint32_t at_seq) {
+  const size_t nk = (size_t)c->n * c->K;
+  const int r1 = (r + 1) % c->n;
+  const struct { int kind; int rank; } recs[3] = {{0, r}, {0, r1}, {1, r}};
+  for (const auto& x : recs) {
+    const int i = x.rank * c->K + k;
+    uint32_t& d = c->health[(x.kind ? R2_H_LINK_DEAD : R2_H_EP_DEAD) * nk + i];
+    uint32_t& rs = c->health[(x.kind ? R2_H_LINK_REP : R2_H_EP_REP) * nk + i];
+    if (d != 0 && rs < d && at_seq >= d) rs = at_seq;
+  }
+}
+
 int r2_push_health(r2_comm* c) {
   const size_t bytes = c->health.size() * sizeof(uint32_t);
   memcpy(c->health_pinned, c->health.data(), bytes);     // pinned: true async DMA, no staging

@@ -91,6 +91,8 @@ void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int 
   c->probes.push_back(pr);
 }
 
+void reprobe_done(r2_comm* c, const Round& rd, int verdict);
+
 void round_result(r2_comm* c, uint32_t id, int slot, int outcome) {
   for (size_t i = 0; i < c->rounds.size(); ++i) {
     Round& rd = c->rounds[i];
@@ -99,6 +101,12 @@ void round_result(r2_comm* c, uint32_t id, int slot, int outcome) {
     for (int s = 0; s < rd.need; ++s)
       if (rd.outcomes[s] < 0) return;
     const int v = r2_triangulate(rd.outcomes, rd.aux >= 0);
+    if (rd.reprobe) {                    // recovery check: decided locally, no verdict broadcast
+      Round done = rd;
+      c->rounds.erase(c->rounds.begin() + i);
+      reprobe_done(c, done, v);
+      return;
+    }
     R2LOG("verdict round %08x seq %u (%d->%d ch%d aux %d) outcomes %d%d%d%d -> %d", rd.id, rd.seq, rd.a, rd.b,
           rd.channel, rd.aux, rd.outcomes[0], rd.outcomes[1], rd.outcomes[2], rd.outcomes[3], v);
     Msg m{};
@@ -129,8 +137,9 @@ void round_result(r2_comm* c, uint32_t id, int slot, int outcome) {
   }
 }
 
-void start_round(r2_comm* c, uint32_t id, uint32_t seq, int a, int b, int channel) {
+void start_round(r2_comm* c, uint32_t id, uint32_t seq, int a, int b, int channel, bool reprobe = false) {
   Round rd{};
+  rd.reprobe = reprobe;
   rd.id = id;
   rd.seq = seq;
   rd.a = a;
@@ -764,6 +773,86 @@ bool progress_timings(r2_comm* c) {
   return busy;
 }
 
+// ------------------------------------------------------------------ re-probe
+// P:19 "R²CCL also periodically reprobes to detect component recovery (e.g.,
+// NIC resets, cable fixes), adapting probe frequency": every dead outgoing
+// connection of a local rank gets a triangulation round after reprobe_us,
+// then after exponentially growing intervals (capped at reprobe_max_us).  A
+// round whose A->B and B->A probes both succeed (verdict NONE) re-admits the
+// connection from the next collective this process enqueues (the health
+// records are seq-indexed, so kernels already in flight keep their plan).
+// Re-probes never overlap an active failover.
+void reprobe_done(r2_comm* c, const Round& rd, int verdict) {
+  for (size_t i = 0; i < c->reprobes.size(); ++i) {
+    r2_comm::Reprobe& e = c->reprobes[i];
+    if (e.round_id != rd.id) continue;
+    e.round_id = 0;
+    if (verdict == R2_V_NONE) {
+      std::lock_guard<std::mutex> g(c->mu);
+      c->readmit_pending.push_back({e.r, e.ch});
+      c->n_readmits++;
+      R2LOG("re-probe %d->%d ch%d: healthy again, re-admitted from the next collective", rd.a, rd.b, rd.channel);
+      c->reprobes.erase(c->reprobes.begin() + i);
+    } else {
+      const uint64_t cap = (uint64_t)std::max(c->cfg.reprobe_max_us, c->cfg.reprobe_us) * 1000ull;
+      e.interval_ns = std::min(e.interval_ns * 2, cap);
+      e.next_ns = r2_now_ns() + e.interval_ns;
+      R2LOG("re-probe %d->%d ch%d: still failed (verdict %d), next in %.1f ms", rd.a, rd.b, rd.channel, verdict,
+            e.interval_ns / 1e6);
+    }
+    return;
+  }
+}
+
+bool progress_reprobes(r2_comm* c) {
+  if (c->cfg.reprobe_us <= 0 || c->n < 2) return false;
+  const uint64_t now = r2_now_ns();
+  if (now - c->reprobe_scan_ns < 200000ull) return false;   // scan every 0.2 ms
+  c->reprobe_scan_ns = now;
+  // dead own outgoing connections in the view of the next collective
+  std::vector<std::pair<int, int>> dead;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    const uint32_t q = (uint32_t)c->seq + 1;
+    for (int l = 0; l < c->nlocal; ++l)
+      for (int k = 0; k < c->K; ++k)
+        if (!r2_conn_ok_at(c, c->first_rank + l, k, q)) dead.push_back({c->first_rank + l, k});
+    for (auto& rp : c->readmit_pending)           // already found healthy
+      dead.erase(std::remove(dead.begin(), dead.end(), rp), dead.end());
+  }
+  // track / forget
+  for (size_t i = 0; i < c->reprobes.size();) {
+    const auto key = std::make_pair(c->reprobes[i].r, c->reprobes[i].ch);
+    if (std::find(dead.begin(), dead.end(), key) == dead.end() && c->reprobes[i].round_id == 0)
+      c->reprobes.erase(c->reprobes.begin() + i);
+    else
+      ++i;
+  }
+  for (auto& d : dead) {
+    bool known = false;
+    for (auto& e : c->reprobes) known |= (e.r == d.first && e.ch == d.second);
+    if (!known) {
+      const uint64_t iv = (uint64_t)c->cfg.reprobe_us * 1000ull;
+      c->reprobes.push_back({d.first, d.second, now + iv, iv, 0u});
+    }
+  }
+  if (!c->rounds.empty() || !c->replans.empty()) return false;   // a failover is in progress
+  bool busy = false;
+  for (auto& e : c->reprobes) {
+    if (e.round_id || now < e.next_ns) continue;
+    e.round_id = 0xC0000000u | (++c->reprobe_counter & 0x3FFFFFFFu);
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      c->n_reprobes++;
+    }
+    R2LOG("re-probe round %08x: %d->%d ch%d", e.round_id, e.r, (e.r + 1) % c->n, e.ch);
+    start_round(c, e.round_id, 0, e.r, (e.r + 1) % c->n, e.ch, true);
+    busy = true;
+    break;                                   // one round at a time
+  }
+  return busy;
+}
+
 bool take_probe_requests(r2_comm* c) {
   std::pair<int, std::pair<int, int>> req;
   uint32_t id;
@@ -804,6 +893,7 @@ void r2_monitor_main(r2_comm* c) {
     busy |= progress_replans(c);
     busy |= progress_timings(c);
     busy |= take_probe_requests(c);
+    busy |= progress_reprobes(c);
     if (!busy) std::this_thread::sleep_for(std::chrono::microseconds(10));
   }
 }

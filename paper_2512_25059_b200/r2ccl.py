@@ -26,7 +26,7 @@ DTYPE_NAMES = {"int32": INT32, "float32": FLOAT32, "bfloat16": BFLOAT16}
 HOT_REPAIR, BALANCE = 0, 1
 # fault kinds
 FAULT_LOCAL, FAULT_REMOTE, FAULT_LINK, FAULT_REPAIR = 0, 1, 2, 3
-FAULT_KINDS = {"LOCAL": 0, "REMOTE": 1, "LINK": 2, "REPAIR": 3}
+FAULT_KINDS = {"LOCAL": 0, "REMOTE": 1, "LINK": 2, "REPAIR": 3, "HEAL": 4}
 # probe outcomes / verdicts
 PROBE_NAMES = {0: "S", 1: "L", 2: "T", 3: "-"}
 VERDICT_NAMES = ["NONE", "LOCAL_ENDPOINT", "REMOTE_ENDPOINT", "LINK", "ENDPOINT_UNREACHABLE_A",
@@ -46,7 +46,8 @@ class Config(C.Structure):
                 ("probe_timeout_us", C.c_int), ("watchdog_ms", C.c_int),
                 ("channel_w", C.c_int * MAX_CHANNELS), ("use_channel_w", C.c_int), ("sim_ranks", C.c_int),
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
-                ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int)]
+                ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
+                ("reprobe_max_us", C.c_int)]
 
 
 PROTO_AUTO, PROTO_SIMPLE, PROTO_LL = 0, 1, 2
@@ -97,7 +98,8 @@ class Status(C.Structure):
     _fields_ = [("seq", C.c_uint64), ("last_error", C.c_int), ("last_error_seq", C.c_uint64),
                 ("n_events", C.c_int), ("world", C.c_int), ("nlocal", C.c_int), ("nchannels", C.c_int),
                 ("dead_endpoints", C.c_uint32 * (MAX_LOCAL * 4)), ("dead_links", C.c_uint32 * (MAX_LOCAL * 4)),
-                ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int)]
+                ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int),
+                ("n_readmits", C.c_int), ("n_reprobes", C.c_int)]
 
 
 class Geometry(C.Structure):
@@ -336,7 +338,8 @@ class Comm:
                 "dead_endpoints": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_endpoints[r] >> c) & 1),
                 "dead_links": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_links[r] >> c) & 1),
                 "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)],
-                "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE")}
+                "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE"),
+                "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes}
 
     def events(self) -> list:
         st = Status()

@@ -175,6 +175,28 @@ def main():
         f = dict(kind="LINK", src_rank=world - 1, channel=1, step=1, chunk=1, byte_offset=4096, poison=1)
         results.append(case(comm, rank, world, 1 << 19, "bfloat16", [f], "BALANCE", seed=19))
         comm.finalize()
+        # re-probe (f4): LINK fault, HEAL (the library is not told), re-admission by re-probing
+        cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=32 * 1024, max_bytes=16 << 20,
+                               reprobe_us=300, reprobe_max_us=5000)
+        comm = T.comm_from_env(cfg)
+        f = dict(kind="LINK", src_rank=world - 1, channel=3, step=0, chunk=0, byte_offset=1024)
+        results.append(case(comm, rank, world, 200_003, "bfloat16", [f], "BALANCE", seed=41))
+        results.append(case(comm, rank, world, 200_003, "bfloat16", seed=42))        # degraded
+        seq = comm.status()["seq"] + 1
+        comm.inject_fault(at_seq=seq, kind="HEAL", src_rank=world - 1, channel=3)
+        results.append(case(comm, rank, world, 200_003, "bfloat16", seed=43))        # fabric healed
+        import time
+        deadline = time.time() + 3.0
+        while rank == world - 1 and comm.status()["n_readmits"] == 0 and time.time() < deadline:
+            time.sleep(0.005)
+        dist.barrier()
+        results.append(case(comm, rank, world, 200_003, "bfloat16", seed=44))        # re-admitted
+        st = comm.status()
+        ok = rank != world - 1 or ((world - 1, 3) not in st["dead_links"] and st["n_readmits"] >= 1)
+        oks = [None] * world
+        dist.all_gather_object(oks, bool(ok))
+        results.append({"op": "reprobe", "ok": all(oks), "status": {k: st[k] for k in ("n_reprobes", "n_readmits")}})
+        comm.finalize()
         if world >= 2:
             cfg = R.config_default(nchannels=3, ctas_per_channel=2, chunk_bytes=32 * 1024, max_bytes=64 << 20)
             comm = T.comm_from_env(cfg)

@@ -311,3 +311,56 @@ def test_brute_force_small(strategy):
                             comm.inject_fault(at_seq=seq + 1, kind="REPAIR", src_rank=rr, channel=cc)
                     rc, out = run(comm, xs, "int32")
                     assert rc == R.SUCCESS
+
+
+# ------------------------------------------------------------ re-probe (f4)
+
+def test_reprobe_readmits_after_heal():
+    """P:19 periodic re-probe: a LINK-dead connection is re-probed with
+    back-off; after the emulated fabric heals (HEAL, which the library is not
+    told about) a re-probe finds A->B and B->A healthy and the connection is
+    re-admitted from the next collective; results bit-exact throughout."""
+    import time
+    n, K, N = 4, 3, 60_000
+    comm = sim_comm(n, K, 2, 8192, reprobe_us=300, reprobe_max_us=5000)
+    xs = r2inputs.inputs(n, N, "int32", seed=31)
+    g = oracle_geom(comm, N, "int32")
+    comm.inject_fault(at_seq=1, kind="LINK", src_rank=1, channel=2, step=1, chunk=0, byte_offset=64)
+    for _ in range(2):                       # faulted, then degraded
+        rc, out = run(comm, xs, "int32")
+        assert rc == R.SUCCESS
+        check_result(out, xs, g, "int32")
+    assert (1, 2) in comm.status()["dead_links"]
+    time.sleep(0.03)                         # re-probes fail: still dead, backing off
+    st = comm.status()
+    assert st["n_reprobes"] >= 2 and st["n_readmits"] == 0 and (1, 2) in st["dead_links"]
+    seq = st["seq"] + 1
+    comm.inject_fault(at_seq=seq, kind="HEAL", src_rank=1, channel=2)
+    rc, out = run(comm, xs, "int32")         # the fabric heals in stream order before this call
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "int32")
+    deadline = time.time() + 2.0
+    while comm.status()["n_readmits"] == 0 and time.time() < deadline:
+        time.sleep(0.005)
+    assert comm.status()["n_readmits"] == 1
+    b0 = comm.status()["bytes"][1][2]
+    rc, out = run(comm, xs, "int32")         # re-admitted from this collective on
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "int32")
+    st = comm.status()
+    assert st["dead_links"] == [] and st["bytes"][1][2] > b0
+
+
+def test_reprobe_disabled_keeps_connection_dead():
+    import time
+    n, K, N = 3, 2, 30_000
+    comm = sim_comm(n, K, 1, 8192, reprobe_us=0)
+    xs = r2inputs.inputs(n, N, "int32", seed=32)
+    comm.inject_fault(at_seq=1, kind="LINK", src_rank=0, channel=1, step=0, chunk=0, byte_offset=0)
+    comm.inject_fault(at_seq=2, kind="HEAL", src_rank=0, channel=1)
+    for _ in range(3):
+        rc, out = run(comm, xs, "int32")
+        assert rc == R.SUCCESS
+    time.sleep(0.02)
+    st = comm.status()
+    assert st["n_reprobes"] == 0 and (0, 1) in st["dead_links"]

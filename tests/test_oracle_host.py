@@ -226,3 +226,25 @@ def test_hbm_bytes_formula_by_counting():
         writes = (n - 1) + 1 + (n - 1)              # scratch in, own recv, recv in
         assert C.hbm_bytes_per_gpu(n, n) == pytest.approx(reads + writes)
         assert C.nvlink_bytes_per_gpu(n, n) == 2 * (n - 1)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_reprobe_readmits_exactly_when_connection_healthy(n):
+    """f4 (P:19 re-probe): for every emulated fabric state of one channel
+    (each endpoint and each ring link alive or dead, brute force), the
+    re-probe of (A -> A+1) re-admits iff both endpoints and the link A -> A+1
+    are alive -- faults elsewhere (other ranks' endpoints, other links) never
+    block re-admission and never fake it."""
+    import itertools
+    from oracle import triangulation as OT2
+    K = 1
+    for bits in itertools.product((False, True), repeat=2 * n):
+        ep = [[bits[r]] for r in range(n)]
+        ln = [[bits[n + r]] for r in range(n)]
+        for a in range(n):
+            b = (a + 1) % n
+            want = not ep[a][0] and not ep[b][0] and not ln[a][0]
+            if n == 2:   # the two ring links of a 2-ring join the same pair in opposite directions
+                want = want and not ln[b][0]
+            assert OT2.reprobe_readmits(a, b, 0, n, ep, ln) == want, (bits, a)
+    assert K == 1
