@@ -295,6 +295,37 @@ def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, red
     return out
 
 
+def successive_scenario(make_comm, run_step, healthy_ms, n, K, geom_m, strategy, get_result, ref_result,
+                        fault_rank=3, fault_ch=5, t=3, j=4, b=256 * 1024, stream=None, barrier=lambda: None,
+                        reduce_max=lambda x: x, gather=lambda evs: evs):
+    """Config 4: the config-3 LINK fault, then a second LINK fault on the
+    adopting backup (chain[0] = ch+1) while it carries the residual (P:36
+    successive failover: roll back again, move to the next chain entry)."""
+    import torch
+    comm = make_comm(strategy)
+    steps = 2 * n - 2
+    t1, j1 = min(t, steps - 2), min(j, geom_m - 1)
+    t2 = t1 + 1
+    r, c1, c2 = fault_rank % n, fault_ch % K, (fault_ch + 1) % K
+    comm.inject_fault(at_seq=2, kind="LINK", src_rank=r, channel=c1, step=t1, chunk=j1, byte_offset=b, poison=1)
+    comm.inject_fault(at_seq=2, kind="LINK", src_rank=r, channel=c2, step=t2, chunk=j1, byte_offset=b // 2,
+                      origin_channel=c1, poison=1)
+    run_step(comm)
+    torch.cuda.synchronize()
+    barrier()
+    ms = reduce_max(timed(lambda: run_step(comm), 1, stream))
+    rc = comm.sync()
+    identical = bool(torch.equal(get_result(), ref_result)) if ref_result is not None else None
+    identical = bool(reduce_max(0.0 if identical else 1.0) == 0.0)
+    evs = gather(comm.events())
+    out = {"strategy": strategy, "rc": rc, "bit_identical_to_healthy": identical, "ms_faulted_call": ms,
+           "extra_ms": ms - healthy_ms,
+           "events": [{k2: e.get(k2) for k2 in ("rank", "origin", "stopped_channel", "verdict", "resume", "retransmit",
+                                            "assignee", "chain_pos", "failover_ms")} for e in evs]}
+    comm.finalize()
+    return out
+
+
 def run_sim(a):
     """N = 1: k simulated ranks on one B200."""
     import torch
@@ -344,6 +375,9 @@ def run_sim(a):
         for strat in ("BALANCE", "HOT_REPAIR"):
             res["fault"].append(fault_scenario(mk, lambda c: T.allreduce(c, send, recv), ms, S, k, K, g.m, strat,
                                                lambda: recv, ref, stream=stream))
+        res["successive"] = [successive_scenario(mk, lambda c: T.allreduce(c, send, recv), ms, k, K, g.m, strat,
+                                                 lambda: recv, ref, stream=stream)
+                             for strat in ("BALANCE", "HOT_REPAIR")]
     return res, None
 
 
@@ -483,6 +517,10 @@ def run_multi(a):
                 mk, lambda c: T.allreduce(c, send, recv), ms, S, world, K, g.m, strat, lambda: recv, ref,
                 fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0,
                 gather=gather))
+        res["successive"] = [successive_scenario(
+            mk, lambda c: T.allreduce(c, send, recv), ms, world, K, g.m, strat, lambda: recv, ref,
+            fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, gather=gather)
+            for strat in ("BALANCE", "HOT_REPAIR")]
     return res, rank
 
 
@@ -554,6 +592,8 @@ def report(a, res, n_gpus, n_ranks, mode):
         line["collectives"] = res["collectives"]
     if "fault" in res:
         line["fault"] = res["fault"]
+    if "successive" in res:
+        line["successive_failover"] = res["successive"]
     return line
 
 
