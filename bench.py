@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-coll", action="store_true", help="skip the standalone ReduceScatter / AllGather section")
+    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--per-step", action="store_true", help="debug: per-step CUDA-event times to stderr")
     ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling period (ms)")
@@ -339,7 +340,7 @@ def run_sim(a):
     count = S // 2
     mk = lambda strategy: R.Comm(0, 1, 0, None, R.config_default(
         sim_ranks=k, nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk,
-        max_bytes=S, strategy=strategy))
+        max_bytes=S, strategy=strategy, protocol=a.protocol))
     comm = mk("BALANCE")
     send = torch.empty((k, count), dtype=torch.bfloat16, device="cuda")
     recv = torch.empty_like(send)
@@ -407,7 +408,7 @@ def run_multi(a):
     def mk(strategy):
         c = T.comm_from_env(R.config_default(
             nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
-            strategy=strategy))
+            strategy=strategy, protocol=a.protocol))
         T.register(c, recv)     # collective: recv mapped into every peer
         return c
 

@@ -843,6 +843,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   m.own = it.own;
   m.fault = fire - 1;
   mbar_arrive(&sh.full[u]);
+  if (p.trace == 2 && k.cta_in_rank == 0 && sh.pub < 8) k.me.misc->trace[24 + sh.pub] = gtimer();  // publish i
   sh.pub++;
   if (it.own) {
     k.own_next_key = key + 1;
@@ -893,7 +894,49 @@ __device__ int control_run(Cta& k, Shared& sh) {
   unsigned int ack_epoch = 0;             // freeze epoch still to acknowledge
   for (;;) {
     bool progress = false;
-    // 1. retire finished chunks in order: ONE release fence for all of them
+    // 1. publish as many chunks as possible (slot free, input arrived) BEFORE
+    //    retiring: the retire's fence blocks this lane until the retired
+    //    chunks' stores have landed, and the data warps must not idle meanwhile
+    //    (publishing after the fence cost one chunk transfer per chunk)
+    bool replanned = false;
+    while (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
+      bool fired = false;
+      int st = try_publish(k, sh, cur, first_try, &fired);
+      first_try = false;
+      if (st == ST_REPLAN) {
+        apply_plan(k, sh);
+        if (sh.freeze) ack_epoch = sh.seen_epoch;
+        it = Iter{0, 0, k.w};             // rescan: own chunks skip by key, re-placed ones by flag
+        have = iter_next(k, sh, it, cur);
+        first_try = true;
+        replanned = true;
+        break;
+      }
+      if (st == ST_OK) {
+        progress = true;
+        first_try = true;
+        if (!cur.own) {
+          if (!last_adopt_pub) k.ctrl->cta[k.cta_in_rank].t_pub_adopt = gtimer();
+          last_adopt_pub = sh.pub;
+        }
+        if (fired) {
+          if (cur.own) fired_key = keyof(cur.t, cur.o, cur.j);
+          pending = ST_STOP;
+          sh.cause = STOP_FAULT_FIRED;
+          have = false;
+        } else {
+          have = iter_next(k, sh, it, cur);
+        }
+      } else {
+        if (st != ST_NOTREADY) {
+          pending = st;
+          have = false;
+        }
+        break;
+      }
+    }
+    if (replanned) continue;
+    // 2. retire finished chunks in order: ONE release fence for all of them
     unsigned int nd = 0;
     while (sh.fin + nd != sh.pub) {
       const unsigned int u = sh.fin + nd;
@@ -914,6 +957,9 @@ __device__ int control_run(Cta& k, Shared& sh) {
           fire_fault(k, p.faults[m.fault], m.t, m.o, m.j);
         }
       }
+      if (p.trace == 2 && k.cta_in_rank == 0)
+        for (unsigned int i = 0; i < nd; ++i)
+          if (sh.fin + i < 8) k.me.misc->trace[16 + sh.fin + i] = gtimer();   // retire i
       sh.fin += nd;
       progress = true;
     }
@@ -922,39 +968,6 @@ __device__ int control_run(Cta& k, Shared& sh) {
       __threadfence_system();            // completion words before the acknowledgement
       k.ctrl->cta[k.cta_in_rank].ack = R2_SS(k.seq, ack_epoch);
       ack_epoch = 0;
-    }
-    // 2. publish the next chunk when a slot is free and its input has arrived
-    if (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
-      bool fired = false;
-      int st = try_publish(k, sh, cur, first_try, &fired);
-      first_try = false;
-      if (st == ST_REPLAN) {
-        apply_plan(k, sh);
-        if (sh.freeze) ack_epoch = sh.seen_epoch;
-        it = Iter{0, 0, k.w};             // rescan: own chunks skip by key, re-placed ones by flag
-        have = iter_next(k, sh, it, cur);
-        first_try = true;
-        continue;
-      }
-      if (st == ST_OK) {
-        progress = true;
-        first_try = true;
-        if (!cur.own) {
-          if (!last_adopt_pub) k.ctrl->cta[k.cta_in_rank].t_pub_adopt = gtimer();
-          last_adopt_pub = sh.pub;
-        }
-        if (fired) {
-          if (cur.own) fired_key = keyof(cur.t, cur.o, cur.j);
-          pending = ST_STOP;
-          sh.cause = STOP_FAULT_FIRED;
-          have = false;
-        } else {
-          have = iter_next(k, sh, it, cur);
-        }
-      } else if (st != ST_NOTREADY) {
-        pending = st;
-        have = false;
-      }
     }
     // 2b. an abort / timeout also releases data warps spinning on LL lines
     if ((pending == ST_ABORT || pending == ST_TIMEOUT) && sh.fin != sh.pub &&

@@ -28,7 +28,8 @@ def main():
     W = int(os.environ.get("W", 16))
     sizes = [int(s) for s in os.environ.get("SIZES", "65536,16777216,268435456").split(",")]
     proto = os.environ.get("PROTO", "AUTO")
-    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=max(sizes), protocol=proto))
+    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=max(sizes), protocol=proto,
+                                            chunk_bytes=int(os.environ.get("CHUNK", 512 * 1024))))
     steps = 2 * world - 1
     for S in sizes:
         x = torch.randn(S // 2, device="cuda").to(torch.bfloat16)
@@ -54,8 +55,10 @@ def main():
                 f"first-pub {rel(tr[2]):.1f} | step first-publish: {pub} | step last-retire: {ret} | ctl-end "
                 f"{rel(tr[60]):.1f} drain {rel(tr[61]):.1f} exit {rel(tr[62]):.1f}")
         if os.environ.get("R2_TRACE") == "2":
-            line += " | data take: " + " ".join(f"{rel(tr[40 + i]):.1f}" for i in range(steps))
-            line += " | data done: " + " ".join(f"{rel(tr[48 + i]):.1f}" for i in range(steps))
+            line += " | data take: " + " ".join(f"{rel(tr[40 + i]):.1f}" for i in range(8))
+            line += " | data done: " + " ".join(f"{rel(tr[48 + i]):.1f}" for i in range(8))
+            line += " | ctl publish: " + " ".join(f"{rel(tr[24 + i]):.1f}" for i in range(8))
+            line += " | ctl retire: " + " ".join(f"{rel(tr[16 + i]):.1f}" for i in range(8))
         for r in range(world):
             if r == rank:
                 print(line, file=sys.stderr, flush=True)
