@@ -28,6 +28,13 @@ to roundup(N, K*V) for the channel split (padding read as 0, never written).
   * AllGather: steps t = 0..n-2 = the AllReduce's steps n-1..2n-3 (the owner
     sends its own shard at t = 0, then the ring forwards).
 
+Standalone Broadcast (root; "the root sends D_total while all others
+receive it"): a pipelined chain root -> root+1 -> ... -> root-1 over the same
+ring connections.  N is the element count; one shard (the whole padded
+buffer) split into K channel slices of m chunks; steps t = 0..n-2 where rank
+r is active only at its chain position t_r = (r - root) mod n (the last rank
+of the chain only receives).  Reading R-8.
+
 LL protocol (ll=True, reading R-6): the all-gather data
 travels through library scratch as self-validating lines, so the receiver
 unpacks the last all-gather step itself: AllReduce and AllGather get one more
@@ -43,7 +50,7 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-ALLREDUCE, REDUCE_SCATTER, ALL_GATHER = "allreduce", "reduce_scatter", "all_gather"
+ALLREDUCE, REDUCE_SCATTER, ALL_GATHER, BROADCAST = "allreduce", "reduce_scatter", "all_gather", "broadcast"
 
 
 def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1,
@@ -53,6 +60,8 @@ def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: 
     if op == ALLREDUCE:
         Np = ceil_div(max(N, 1), n * K * V) * n * K * V
         slice_bytes = Np // (n * K) * elem_bytes
+    elif op == BROADCAST:
+        slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
     else:
         slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
     per_worker = ceil_div(ceil_div(slice_bytes, W), 16) * 16
@@ -68,6 +77,7 @@ class Geometry:
     chunk_bytes: int          # the effective chunk (multiple of 16)
     op: str = ALLREDUCE       # N = per-shard count for REDUCE_SCATTER / ALL_GATHER
     ll: bool = False          # LL protocol: + the LOCAL unpack step (AllReduce / AllGather)
+    root: int = 0             # BROADCAST only
 
     @property
     def V(self) -> int:
@@ -75,6 +85,8 @@ class Geometry:
 
     @property
     def Np(self) -> int:
+        if self.op == BROADCAST:
+            return self.shard
         if self.op != ALLREDUCE:
             return self.n * self.shard
         q = self.n * self.K * self.V
@@ -91,18 +103,26 @@ class Geometry:
     @property
     def stride(self) -> int:
         """Distance between shards in the user buffers."""
-        return self.shard if self.op == ALLREDUCE else self.N
+        return self.shard if self.op in (ALLREDUCE, BROADCAST) else self.N
 
     @property
     def total(self) -> int:
-        """Elements of the n-shard user buffer (AllReduce: N)."""
-        return self.N if self.op == ALLREDUCE else self.n * self.N
+        """Elements of the n-shard user buffer (AllReduce / Broadcast: N)."""
+        return self.N if self.op in (ALLREDUCE, BROADCAST) else self.n * self.N
 
     def shard_limit(self, s: int) -> int:
         """One past the last valid global element of shard s."""
         if self.op == ALLREDUCE:
             return min(self.N, (s + 1) * self.shard)
+        if self.op == BROADCAST:
+            return self.N
         return s * self.N + self.N
+
+    def active(self, r: int, t: int) -> bool:
+        """Does rank r send at step t?  (Broadcast: only at its chain position.)"""
+        if self.op != BROADCAST:
+            return True
+        return t == (r - self.root) % self.n and t <= self.n - 2
 
     @property
     def t0(self) -> int:
@@ -114,6 +134,8 @@ class Geometry:
         protocol's unpack of the last all-gather step (no connection used)."""
         if self.op == REDUCE_SCATTER:
             return t == self.n - 1
+        if self.op == BROADCAST:
+            return False
         return self.ll and t == self.steps - 1
 
     @property
@@ -130,7 +152,8 @@ class Geometry:
 
     @property
     def steps(self) -> int:
-        base = {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1}[self.op]
+        base = {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1,
+                BROADCAST: self.n - 1}[self.op]
         return base + (1 if self.ll and self.op != REDUCE_SCATTER else 0)
 
     def item_len(self, j: int) -> int:
@@ -142,6 +165,8 @@ class Geometry:
 
     def shard_sent(self, r: int, t: int) -> int:
         """Shard that rank r sends at (op-)step t (§8 header)."""
+        if self.op == BROADCAST:
+            return 0
         n = self.n
         ta = t + self.t0
         if ta <= n - 2:

@@ -45,6 +45,11 @@ owner itself, and a stopped worker's unfinished local items are re-placed
 with the rest of its residual (reading R-5).  In-place ReduceScatter
 (recv = own shard of send) needs no staging: the final add is the only
 writer of the own shard and a local item is never torn by a fault.
+
+Broadcast (f1, reading R-8): a pipelined chain from the root along the ring;
+worker (r, c) holds only the items of r's chain position t_r, reads the
+root's input (t_r = 0) or its own received buffer, and writes the next rank's
+buffer.  Positions of other steps count as complete in r's ledger.
 """
 from __future__ import annotations
 
@@ -55,7 +60,7 @@ import numpy as np
 from . import balance as _bal
 from . import ledger as _led
 from . import triangulation as _tri
-from .geometry import ALL_GATHER, ALLREDUCE, REDUCE_SCATTER, Geometry
+from .geometry import ALL_GATHER, ALLREDUCE, BROADCAST, REDUCE_SCATTER, Geometry
 from .semantic import hop_add, np_dtype
 
 HOT_REPAIR = "HOT_REPAIR"
@@ -143,6 +148,11 @@ class Simulator:
                 self.recv = [self.x[r][r * self.N:(r + 1) * self.N] for r in range(n)]
             else:
                 self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
+        elif self.op == BROADCAST:
+            self.x = [np.asarray(x, dtype=dt) for x in xs]
+            self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
+            if inplace:
+                self.recv[geom.root] = np.array(xs[geom.root], dtype=dt, copy=True)
         elif self.op == ALL_GATHER:
             self.recv = [self._poisoned(n * self.N, poison) for _ in range(n)]
             if inplace:
@@ -185,13 +195,13 @@ class Simulator:
             for c in range(K):
                 if self.conn_ok(r, c):
                     self.queue[(r, c)] = [Task(t, c, j, 0, geom.item_vectors(j))
-                                          for t in range(geom.steps) for j in range(self.m)]
+                                          for t in range(geom.steps) for j in range(self.m) if geom.active(r, t)]
                     self.state[(r, c)] = "run"
         # static plan (plan-time Balance / HotRepair for already-dead connections)
         for r in range(n):
             for c in range(K):
                 if not self.conn_ok(r, c) and self.error is None:
-                    items = [(t, j) for t in range(geom.steps) for j in range(self.m)]
+                    items = [(t, j) for t in range(geom.steps) for j in range(self.m) if geom.active(r, t)]
                     self._assign(r, c, items, record=None)
 
     # ------------------------------------------------------------ helpers
@@ -251,6 +261,12 @@ class Simulator:
         lim = g.shard_limit(s)
         r1 = (r + 1) % n
         if g.local(t) and self.op != REDUCE_SCATTER:      # LL unpack: the data already landed here
+            return
+        if self.op == BROADCAST:                          # chain: root's input, else what arrived here
+            val = self.xread(r, e0, e1, lim) if t == 0 else self.rread(r, e0, e1, lim)
+            if t == 0 and not self.inplace:
+                self.rwrite(r, e0, val, lim)
+            self.rwrite(r1, e0, val, lim)
             return
         if ta <= n - 2:                                   # reduce-scatter hop
             val = self.xread(r, e0, e1, lim)
@@ -320,7 +336,9 @@ class Simulator:
 
     # ------------------------------------------------------------ host side
     def _completed(self, r, origin):
-        return [(self.holder(r, t), t, origin, j) in self.flags for t in range(self.g.steps) for j in range(self.m)]
+        g = self.g
+        return [(not g.active(r, t)) or (self.holder(r, t), t, origin, j) in self.flags
+                for t in range(g.steps) for j in range(self.m)]
 
     def _assign(self, r, origin, items, record):
         """Place residual items of (r -> r+1, origin) on healthy channels."""
@@ -425,7 +443,7 @@ class Simulator:
         if self.error is None:
             missing = [(r, t, c, j) for r in range(self.n) for t in range(self.g.steps)
                        for c in range(self.K) for j in range(self.m)
-                       if (self.holder(r, t), t, c, j) not in self.flags]
+                       if self.g.active(r, t) and (self.holder(r, t), t, c, j) not in self.flags]
             if missing:
                 raise RuntimeError(f"deadlock: {len(missing)} items undelivered, e.g. {missing[:4]}")
             if self.stage is not None:

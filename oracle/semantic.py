@@ -134,6 +134,13 @@ def all_gather(shards: list[np.ndarray]) -> np.ndarray:
     return np.concatenate([np.asarray(s) for s in shards]) if shards else np.empty(0)
 
 
+def broadcast(xs: list[np.ndarray], root: int) -> list[np.ndarray]:
+    """Standalone Broadcast ("in a Broadcast, the root sends D_total while
+    all others receive it"): every rank ends with
+    the root's buffer, bits preserved."""
+    return [np.array(xs[root], copy=True) for _ in xs]
+
+
 def exact_sum_f64(xs: list[np.ndarray], dtype: str) -> np.ndarray:
     """The float64 sum (the 'exact' reference of the normwise bound, §8(c))."""
     if dtype == "bfloat16":

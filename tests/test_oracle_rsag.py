@@ -129,7 +129,7 @@ def test_inplace_and_traffic(op, inplace):
 
 
 def brute(op, n, K, m, vpc, kinds=("LOCAL", "REMOTE", "LINK")):
-    steps = n if op == REDUCE_SCATTER else n - 1
+    steps = n if op == REDUCE_SCATTER else n - 1     # AllGather and Broadcast: n - 1
     bs = sorted({0, (vpc // 2) * 16, vpc * 16 - 16})
     for r, c, t, j, b, kind in itertools.product(range(n), range(K), range(steps), range(m), bs, kinds):
         yield Fault(kind, r, c, t, j, b)
@@ -232,3 +232,53 @@ def test_ll_brute_force_single_fault(op, strategy):
         for rr in range(n):
             assert same(res.y[rr], want[rr]), (f, rr)
         assert (len(res.fired) == 0) == g.local(t), f
+
+
+# ------------------------------------------------------------ Broadcast (f1)
+
+from oracle.geometry import BROADCAST  # noqa: E402
+
+
+def test_broadcast_layer1_rank_tagged():
+    """Every rank receives the root's buffer: rank-tagged inputs."""
+    xs = [np.arange(11, dtype=np.int32) + 100 * r for r in range(5)]
+    for root in range(5):
+        for r, y in enumerate(S.broadcast(xs, root)):
+            assert np.array_equal(y, np.arange(11, dtype=np.int32) + 100 * root)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+@pytest.mark.parametrize("n,K,count,root", [(2, 1, 100, 1), (3, 2, 1000, 0), (4, 3, 4097, 2), (8, 8, 5000, 5)])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_broadcast_fault_free(dtype, n, K, count, root, inplace):
+    E = r2inputs.elem_bytes(dtype)
+    g = Geometry(n, K, count, E, effective_chunk_bytes(count, n, K, E, 256, 2, BROADCAST), BROADCAST, root=root)
+    xs = r2inputs.inputs(n, count, dtype, seed=n + root)
+    res = simulate(xs, g, dtype, seed=3, inplace=inplace)
+    assert res.error is None
+    for r in range(n):
+        assert same(res.y[r], xs[root]), r
+    # P:78: every rank but the last of the chain sends the (padded) buffer once
+    sent = res.bytes_sent.sum(axis=1)
+    last = (root - 1) % n
+    for r in range(n):
+        assert sent[r] == (0 if r == last else g.shard * E), (r, sent)
+
+
+@pytest.mark.parametrize("n,K,m", [(3, 2, 2), (4, 3, 1), (4, 2, 2)])
+@pytest.mark.parametrize("strategy", [BALANCE, HOT_REPAIR])
+def test_broadcast_brute_force_single_fault(n, K, m, strategy):
+    """Every (rank, channel, step, chunk, kind) fault: buffers == root's; a
+    fault at a step where the rank does not send never fires."""
+    vpc = 2
+    count = K * m * vpc * 4
+    for root in (0, n - 1):
+        g = Geometry(n, K, count, 4, vpc * 16, BROADCAST, root=root)
+        assert g.m == m
+        xs = r2inputs.inputs(n, count, "int32", seed=root + 7)
+        for i, f in enumerate(brute(BROADCAST, n, K, m, vpc)):
+            res = run(BROADCAST, xs, g, "int32", faults=[f], strategy=strategy, seed=i)
+            assert res.error is None, f
+            for r in range(n):
+                assert same(res.y[r], xs[root]), (f, r)
+            assert (len(res.fired) == 1) == g.active(f.rank, f.t), f
