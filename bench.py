@@ -267,7 +267,8 @@ def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, red
                 c.inject_fault(at_seq=1, kind="LINK", src_rank=3 % n, channel=5 % K, step=0, chunk=0,
                                byte_offset=4096)
             ops = {"reduce_scatter": lambda: T.reduce_scatter(c, send, shard, recvcount=cnt),
-                   "all_gather": lambda: T.all_gather(c, send[:cnt], recv, sendcount=cnt)}
+                   "all_gather": lambda: T.all_gather(c, send[:cnt], recv, sendcount=cnt),
+                   "broadcast": lambda: T.broadcast(c, send if rank == 0 else None, recv, 0)}
             for name, fn in ops.items():
                 for _ in range(3):
                     fn()
@@ -278,21 +279,29 @@ def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, red
                 d["degraded_ms" if degraded else "ms"] = ms
             assert c.sync() == R.SUCCESS
             c.finalize()
+    # Broadcast: nccl-tests busbw = algbw = S / t (the whole buffer crosses every link of the chain)
+    if "broadcast" in out:
+        d = out["broadcast"]
+        d["busbw"] = S / (d["ms"] * 1e-3) / 1e9
+        d["degraded_busbw"] = S / (d["degraded_ms"] * 1e-3) / 1e9
     for name, d in out.items():
         d["degraded_over_healthy"] = d["degraded_busbw"] / d["busbw"]
         d["degraded_over_bound"] = d["degraded_busbw"] / (d["busbw"] * (K - 1) / K)
     if pg is not None:
         rs_out = torch.empty(cnt, dtype=send.dtype, device="cuda")
         ag_out = torch.empty(n * cnt, dtype=send.dtype, device="cuda")
+        bc = send.clone()
         nc = {"reduce_scatter": lambda: dist.reduce_scatter_tensor(rs_out, send[:n * cnt], group=pg),
-              "all_gather": lambda: dist.all_gather_into_tensor(ag_out, send[:cnt], group=pg)}
+              "all_gather": lambda: dist.all_gather_into_tensor(ag_out, send[:cnt], group=pg),
+              "broadcast": lambda: dist.broadcast(bc, 0, group=pg)}
         for name, fn in nc.items():
             for _ in range(3):
                 fn()
             barrier()
-            out[name]["nccl_busbw"] = busbw(reduce_max(timed(fn, steps, stream)))
-    out["note"] = ("S-byte n-shard buffer per rank (RS input / AG output), bf16; degraded = one LINK fault "
-                   "(rank 3 % n, ch 5), Balance; bound (K-1)/K of healthy")
+            ms_n = reduce_max(timed(fn, steps, stream))
+            out[name]["nccl_busbw"] = (S / (ms_n * 1e-3) / 1e9) if name == "broadcast" else busbw(ms_n)
+    out["note"] = ("S-byte n-shard buffer per rank (RS input / AG output; Broadcast buffer, root 0), bf16; "
+                   "degraded = one LINK fault (rank 3 % n, ch 5), Balance; bound (K-1)/K of healthy")
     return out
 
 

@@ -50,7 +50,7 @@ typedef enum {
 typedef enum { R2_INT32 = 0, R2_FLOAT32 = 1, R2_BFLOAT16 = 2 } r2_dtype_t;
 
 /* Collectives on the ring (SURVEY §8(f) f1 for the standalone halves). */
-typedef enum { R2_OP_ALLREDUCE = 0, R2_OP_REDUCE_SCATTER = 1, R2_OP_ALL_GATHER = 2 } r2_op_t;
+typedef enum { R2_OP_ALLREDUCE = 0, R2_OP_REDUCE_SCATTER = 1, R2_OP_ALL_GATHER = 2, R2_OP_BROADCAST = 3 } r2_op_t;
 
 /* Single-failure strategies (P:57 HotRepair; P:73 R²CCL-Balance). */
 typedef enum { R2_HOT_REPAIR = 0, R2_BALANCE = 1 } r2_strategy_t;
@@ -298,6 +298,19 @@ r2_result_t r2_all_gather(r2_comm_t comm, const void* send, void* recv, size_t s
                           r2_dtype_t dt, void* stream);
 
 /*
+ * r2_broadcast -- collective, asynchronous (f1; "in a Broadcast, the
+ * root sends D_total while all others receive it").  The root's send (count
+ * elements) arrives in every rank's recv, bits preserved, over a pipelined
+ * chain root -> root+1 -> ... along the ring (reading R-8); send is read on the
+ * root only (may be NULL elsewhere); in-place on the root: send == recv.  recv
+ * must lie in a registered range.  Same fault handling (rollback, failover
+ * chain / Balance).  Always the SIMPLE protocol.  Sim mode: send / recv rows of
+ * count elements, 16-byte aligned.  Errors: as r2_allreduce; root out of range.
+ */
+r2_result_t r2_broadcast(r2_comm_t comm, const void* send, void* recv, size_t count, r2_dtype_t dt, int root,
+                         void* stream);
+
+/*
  * r2_allreduce_host -- as r2_allreduce, but send/recv are HOST buffers (pinned
  * memory recommended).  Enqueues H2D copy into a library-owned registered
  * device buffer, the allreduce and the D2H copy on `stream`; the caller
@@ -372,6 +385,8 @@ void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
 
 /* Geometry of one collective (SURVEY §8 header, reading C-3).
  * AllReduce: N = count, shards of Np/n at stride shard.
+ * Broadcast (f1): N = count, one shard of roundup(count, K*V) = Np, steps
+ * n-1 (rank r sends only at its chain position (r - root) mod n).
  * ReduceScatter / AllGather (f1): N = n * count (the n-shard user buffer),
  * shard = roundup(count, K*V) (the channel split), stride = count (shard
  * distance in the user buffers); steps n (RS: t = n-1 is the owner's LOCAL

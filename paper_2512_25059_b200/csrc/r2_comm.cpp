@@ -458,7 +458,7 @@ extern "C" r2_result_t r2_inject_fault(r2_comm_t c, const r2_fault_t* f) {
 // halves of SURVEY §8(f) f1).  `count`: AllReduce elements; RS recvcount; AG
 // sendcount.
 static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* recv, size_t count, r2_dtype_t dt,
-                                void* stream) {
+                                void* stream, int root = 0) {
   const int E = elem_bytes(dt);
   if (c->n == 1) {
     if (send != recv) CK(cudaMemcpyAsync(recv, send, count * E, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -474,7 +474,9 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   // moves twice the bytes but pays no fence per step (r2ccl.h "Protocols")
   bool ll = false;
   const bool ll_fits = c->lay.ll_slot_bytes && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
-  if (c->cfg.protocol == R2_PROTO_LL) {
+  if (op == R2_OP_BROADCAST) {
+    ll = false;                                        // always SIMPLE (r2ccl.h)
+  } else if (c->cfg.protocol == R2_PROTO_LL) {
     if (!ll_fits) return R2_ERR_INVALID_ARG;
     ll = true;
   } else if (c->cfg.protocol == R2_PROTO_AUTO && ll_fits) {
@@ -514,7 +516,12 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.inplace = op == R2_OP_ALLREDUCE && send == recv;
   if (op == R2_OP_ALL_GATHER && !c->sim)
     p.ag_inplace = (const char*)send == (const char*)recv + (size_t)c->rank * shard_bytes;
-  if (c->sim && op != R2_OP_ALLREDUCE && (send == recv)) return R2_ERR_INVALID_ARG;   // sim: out-of-place only
+  if (c->sim && (op == R2_OP_REDUCE_SCATTER || op == R2_OP_ALL_GATHER) && (send == recv))
+    return R2_ERR_INVALID_ARG;   // sim: out-of-place only
+  if (op == R2_OP_BROADCAST) {
+    p.root = root;
+    p.ag_inplace = send == recv;                       // root: no local copy
+  }
   p.strategy = c->cfg.strategy;
   p.sim = c->sim;
   p.N = g.N;
@@ -563,6 +570,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
       continue;
     }
     if (f.step >= steps || f.chunk >= g.m || f.step == local_step) continue;   // no such send: never fires
+    if (op == R2_OP_BROADCAST && f.step != ((f.src_rank - root) % c->n + c->n) % c->n) continue;
     if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
     FaultDev& d = p.faults[p.nfaults++];
     d.rank = f.src_rank;
@@ -601,6 +609,8 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   li.seq = seq;
   li.local_step = local_step;
   li.ll = ll;
+  li.op = op;
+  li.root = root;
   li.m = g.m;
   li.steps = steps;
   li.V = g.V;
@@ -669,6 +679,21 @@ static r2_result_t rs_ag(r2_comm_t c, r2_op_t op, const void* send, void* recv, 
   if ((size_t)c->n * count * E > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
   return enqueue_coll(c, op, send, recv, count, dt, stream);
+}
+
+extern "C" r2_result_t r2_broadcast(r2_comm_t c, const void* send, void* recv, size_t count, r2_dtype_t dt, int root,
+                                    void* stream) {
+  if (!c) return R2_ERR_INVALID_ARG;
+  int ae = take_async_error(c);
+  if (ae != R2_SUCCESS) return (r2_result_t)ae;
+  if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
+  if (root < 0 || root >= c->n) return R2_ERR_INVALID_ARG;
+  if (count == 0) return R2_SUCCESS;
+  const bool reads_send = c->sim || c->rank == root;
+  if (!recv || ((uintptr_t)recv & 15) || (reads_send && (!send || ((uintptr_t)send & 15)))) return R2_ERR_INVALID_ARG;
+  if (count * (size_t)elem_bytes(dt) > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
+  if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  return enqueue_coll(c, R2_OP_BROADCAST, reads_send ? send : recv, recv, count, dt, stream, root);
 }
 
 extern "C" r2_result_t r2_reduce_scatter(r2_comm_t c, const void* send, void* recv, size_t recvcount, r2_dtype_t dt,

@@ -51,6 +51,7 @@ struct LaunchInfo {                          // what the monitor needs about a s
   uint32_t seq;
   int local_step;                            // LOCAL step (own completion words) or -1
   bool ll;                                   // LL protocol
+  int op, root;                              // r2_op_t; Broadcast root
   int m, steps, V;
   unsigned long long slice, chunk;
   int nfaults;

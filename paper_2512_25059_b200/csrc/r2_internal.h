@@ -145,7 +145,8 @@ struct LaunchParams {
   int local_step;                        // op-step of LOCAL items (ReduceScatter: n-1) or -1
   int fin_step;                          // last op-step with incoming completion words
   int peer_recv;                         // some step writes the downstream rank's recv
-  int ag_inplace;                        // AllGather with send == own shard of recv
+  int ag_inplace;                        // AllGather with send == own shard of recv; Broadcast root send == recv
+  int root;                              // Broadcast root
   unsigned long long N, Np, shard, slice, chunk;   // elements (N: the whole user buffer)
   unsigned long long sstride, slen;      // shard stride in the user buffers / valid elements per shard
   size_t slot_bytes;

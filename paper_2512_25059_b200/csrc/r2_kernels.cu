@@ -244,6 +244,7 @@ struct Cta {
   bool own_alive;
   unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
   bool all_healthy;         // conn_mask covers every channel (LL speculation allowed)
+  int t_act;                // Broadcast: this rank's chain position (sends only at that step); else -1
   RankPtrs me, nx;
   Ctrl* ctrl;
   unsigned int total_items;
@@ -570,6 +571,13 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
     // of every step, a few microseconds per item for one thread)
     const int m = p.m, W = p.W;
     while (it.t < p.steps) {
+      if (k.t_act >= 0 && it.t != k.t_act) {         // Broadcast: only this rank's chain step
+        if (it.t > k.t_act) return false;
+        it.t = k.t_act;                              // (the last rank of the chain: t_act = steps)
+        it.o = 0;
+        it.j = k.w;
+        continue;
+      }
       if (it.o < k.c) {
         it.o = k.c;
         it.j = k.w;
@@ -595,6 +603,13 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
     return false;
   }
   while (it.t < p.steps) {
+    if (k.t_act >= 0 && it.t != k.t_act) {           // Broadcast: only this rank's chain step
+      if (it.t > k.t_act) return false;
+      it.t = k.t_act;
+      it.o = 0;
+      it.j = k.w;
+      continue;
+    }
     const int t = it.t, o = it.o;
     const bool own = (o == k.c) && k.own_alive;
     unsigned int mode = PLAN_NONE, mask = 0, assignee = 0, epoch = 0;
@@ -730,10 +745,12 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
-  if (p.peer_recv && ta >= n - 1 && !local && !try_recv_next(k, sh)) return ST_NOTREADY;
+  if (p.peer_recv && (ta >= n - 1 || p.op == R2_OP_BROADCAST) && !local && !try_recv_next(k, sh))
+    return ST_NOTREADY;
 
   const int E = p.elem_bytes, V = p.V;
-  const int s_ = (ta <= n - 2) ? ((k.r - 1 - ta) % n + n) % n : ((k.r - (ta - n + 1)) % n + n) % n;
+  const int s_ = p.op == R2_OP_BROADCAST ? 0
+               : (ta <= n - 2) ? ((k.r - 1 - ta) % n + n) % n : ((k.r - (ta - n + 1)) % n + n) % n;
   const unsigned long long off =
       (unsigned long long)it.o * p.slice + (unsigned long long)it.j * p.chunk + (unsigned long long)it.lo * V;
   const unsigned long long sbase = (unsigned long long)s_ * p.sstride;
@@ -749,7 +766,16 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   d.lim = sbase + p.slen < p.N ? sbase + p.slen : p.N;
   d.rs = ta <= n - 2;
   d.src_ll = 0;
-  if (p.ll) {
+  if (p.op == R2_OP_BROADCAST) {
+    // chain: the root's input (t = 0), else what arrived here; into the next rank's recv
+    d.rs = 0;
+    d.src = (t == 0 ? p.send[k.l] : (const char*)p.recv[k.l]) + off * E;
+    d.s_in = nullptr;
+    d.d_rem = sh.recv_next + off * E;
+    d.rem_user = 1;
+    d.d_loc = (t == 0 && !p.ag_inplace) ? p.recv[k.l] + off * E : nullptr;
+    d.loc_user = 1;
+  } else if (p.ll) {
     // LL: scratch traffic as lines; slot index = the AllReduce step that sends
     // into it (RS hops 0..n-2, AG sends n-1..2n-3), offsets doubled
     const unsigned long long lo = off * E * 2;
@@ -1164,8 +1190,9 @@ __device__ int drain(Cta& k, Shared& sh) {
     // all final incoming completion words present?
     int ok = 1;
     const int nf = p.K * p.m;
-    const unsigned int* fin = k.me.flags + fidx(p, p.fin_step, 0, 0);
-    for (int i = k.tid; i < nf; i += k.nthr)
+    const int fs = p.op == R2_OP_BROADCAST ? k.t_act - 1 : p.fin_step;   // the root receives nothing
+    const unsigned int* fin = k.me.flags + fidx(p, fs < 0 ? 0 : fs, 0, 0);
+    for (int i = k.tid; fs >= 0 && i < nf; i += k.nthr)
       if ((int)(ld_relaxed_sys(fin + i) - k.seq) < 0) ok = 0;
     if (__syncthreads_and(ok)) {
       if (k.tid == 0) TRACE_MAX(k, 61);
@@ -1317,7 +1344,9 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   k.me = p.peers[k.l * p.n + k.r];
   k.nx = p.peers[k.l * p.n + k.r1];
   k.ctrl = p.ctrl[k.l];
-  k.total_items = (unsigned int)(p.steps * p.K * p.m);
+  k.t_act = p.op == R2_OP_BROADCAST ? ((k.r - p.root) % p.n + p.n) % p.n : -1;
+  k.total_items = p.op == R2_OP_BROADCAST ? (k.t_act <= p.n - 2 ? (unsigned int)(p.K * p.m) : 0u)
+                                          : (unsigned int)(p.steps * p.K * p.m);
   if (k.tid == 0) TRACE_MIN(k, 0);
   // plan-time placement: read the host's health records for this seq;
   // every CTA of the rank computes the same mask (records for this seq are

@@ -535,7 +535,9 @@ void publish_plan(r2_comm* c, Replan& rp) {
     r2_spin_sync(c->mon_stream);
     R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
   }
+  const int t_act = li.op == R2_OP_BROADCAST ? ((r - li.root) % c->n + c->n) % c->n : -1;
   auto done = [&](int t, int o, int j) {
+    if (t_act >= 0 && t != t_act) return true;         // Broadcast: this rank sends only at t_act
     if (from_keys) {
       const unsigned long long key = ((unsigned long long)t << 40) | ((unsigned long long)o << 32) | (unsigned)j;
       return key < lane_key[j % c->W];

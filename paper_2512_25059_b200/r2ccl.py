@@ -145,6 +145,7 @@ EXPORTS = {
                                  C.POINTER(Geometry)]),
     "r2_reduce_scatter": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "r2_all_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
+    "r2_broadcast": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p]),
     "r2_oob_shm_open": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(Oob)]),
     "r2_oob_shm_close": (C.c_int, [C.POINTER(Oob)]),
 }
@@ -223,8 +224,9 @@ def rollback(completed) -> tuple:
     return r.value, f.value
 
 
-OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER = 0, 1, 2
-OPS = {"allreduce": OP_ALLREDUCE, "reduce_scatter": OP_REDUCE_SCATTER, "all_gather": OP_ALL_GATHER}
+OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER, OP_BROADCAST = 0, 1, 2, 3
+OPS = {"allreduce": OP_ALLREDUCE, "reduce_scatter": OP_REDUCE_SCATTER, "all_gather": OP_ALL_GATHER,
+       "broadcast": OP_BROADCAST}
 
 
 def geometry(count: int, dtype: int, n: int, K: int, W: int, chunk_bytes: int, op: int = OP_ALLREDUCE) -> Geometry:
@@ -313,6 +315,10 @@ class Comm:
     def all_gather(self, send_ptr: int, recv_ptr: int, sendcount: int, dtype: int, stream: int = 0):
         _check(lib().r2_all_gather(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), sendcount, dtype,
                                    C.c_void_p(stream)), "r2_all_gather")
+
+    def broadcast(self, send_ptr: int, recv_ptr: int, count: int, dtype: int, root: int, stream: int = 0):
+        _check(lib().r2_broadcast(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), count, dtype, root,
+                                  C.c_void_p(stream)), "r2_broadcast")
 
     def allreduce_host(self, send_ptr: int, recv_ptr: int, count: int, dtype: int, stream: int = 0):
         _check(lib().r2_allreduce_host(self._h, C.c_void_p(send_ptr), C.c_void_p(recv_ptr), count, dtype,

@@ -140,6 +140,25 @@ def all_gather(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None
     return recv
 
 
+def broadcast(comm: R.Comm, send: torch.Tensor | None, recv: torch.Tensor, root: int, stream=None,
+              count: int | None = None) -> torch.Tensor:
+    """Broadcast (r2_broadcast): the root's send arrives in every rank's recv
+    (registered).  send is only read on the root (None elsewhere; None on the
+    root means in place: recv).  Sim mode: send / recv [k, row] tensors."""
+    if send is None:
+        send = recv
+    _check_pair(send, recv)
+    if comm.sim:
+        count = count if count is not None else recv.shape[1]
+        _rows_ok(comm, send, count)
+        _rows_ok(comm, recv, count)
+    else:
+        count = recv.numel() if count is None else count
+    s = stream if stream is not None else torch.cuda.current_stream()
+    comm.broadcast(send.data_ptr(), recv.data_ptr(), count, r2_dtype(recv), root, s.cuda_stream)
+    return recv
+
+
 def allreduce_host(comm: R.Comm, send: torch.Tensor, recv: torch.Tensor, stream=None,
                    count: int | None = None) -> torch.Tensor:
     """Host (ideally pinned) tensors: H2D, allreduce, D2H on `stream`."""

@@ -134,6 +134,45 @@ def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", 
     return out
 
 
+def case_bcast(comm, rank, world, count, dtype, root, faults=(), strategy="BALANCE", seed=0):
+    """Broadcast (f1) over the real NVLink chain."""
+    xs = r2inputs.inputs(world, count, dtype, seed=seed)
+    recv = torch.empty(count, dtype=TD[dtype], device="cuda")
+    recv.view(torch.uint8).fill_(0xFF)
+    send = dev_tensor(xs[rank], dtype) if rank == root else None
+    T.register(comm, recv)
+    st = comm.status()
+    health = {"dead_links": st["dead_links"], "dead_endpoints": st["dead_endpoints"]}
+    seq = st["seq"] + 1
+    for f in faults:
+        comm.inject_fault(at_seq=seq, **f)
+    ne = len(comm.events())
+    T.broadcast(comm, send, recv, root)
+    rc = comm.sync()
+    ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), np.asarray(xs[root]).view(np.uint8))
+    evs = [norm_event(e) for e in comm.events()[ne:]]
+    all_evs = [None] * world
+    dist.all_gather_object(all_evs, evs)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok))
+    out = {"op": "broadcast", "root": root, "N": count, "dtype": dtype, "faults": list(faults), "rc": rc,
+           "ok": all(oks)}
+    if faults:
+        from oracle.geometry import BROADCAST
+        cfg = comm.cfg
+        E = r2inputs.elem_bytes(dtype)
+        g = Geometry(world, cfg.nchannels, count, E, effective_chunk_bytes(
+            count, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel, BROADCAST), BROADCAST, root=root)
+        got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, health=health,
+                          faults=[OP.Fault(f["kind"], f["src_rank"], f["channel"], f["step"], f["chunk"],
+                                           f.get("byte_offset", 0)) for f in faults])
+        want = sorted((norm_event(e) for e in res.events), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
+        out["events_equal"] = got == want
+        out["events"], out["want"] = got, want
+    return out
+
+
 def main():
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
@@ -152,6 +191,13 @@ def main():
             f = dict(kind="LINK", src_rank=world - 1, channel=1, step=max(0, world - 2), chunk=1,
                      byte_offset=12345, poison=1)
             results.append(case(comm, rank, world, 1 << 20, "bfloat16", [f], strategy, seed=11))
+            # Broadcast (f1): every root, and one LINK fault on a sending rank
+            if strategy == "BALANCE":
+                for root in range(world):
+                    results.append(case_bcast(comm, rank, world, 100_003, "bfloat16", root, seed=root))
+            fb = dict(kind="LINK", src_rank=(1 % world), channel=1, step=(1 % world) if world > 1 else 0, chunk=0,
+                      byte_offset=2048, poison=1)
+            results.append(case_bcast(comm, rank, world, 1 << 18, "int32", 0, [fb], strategy, seed=23))
             # standalone ReduceScatter / AllGather: healthy (ragged, in-place) and one LINK fault
             for op in ("reduce_scatter", "all_gather"):
                 if strategy == "BALANCE":

@@ -158,3 +158,19 @@ def test_oob_shm_multiprocess_gloo(world):
         p.join(120)
         assert p.exitcode == 0
     assert list(out) == [1] * world
+
+
+def test_geometry_broadcast_matches_oracle():
+    """Broadcast geometry (f1): one shard = the whole padded buffer."""
+    from oracle.geometry import BROADCAST
+    rng = np.random.default_rng(9)
+    for _ in range(2000):
+        dt = ["int32", "float32", "bfloat16"][int(rng.integers(3))]
+        E = r2inputs.elem_bytes(dt)
+        n, K, W = int(rng.integers(2, 9)), int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        count = int(rng.integers(1, 1 << 20))
+        chunk = int(rng.integers(1, 1 << 16)) * 16
+        g = R.geometry(count, R.DTYPE_NAMES[dt], n, K, W, chunk, R.OP_BROADCAST)
+        og = Geometry(n, K, count, E, effective_chunk_bytes(count, n, K, E, chunk, W, BROADCAST), BROADCAST)
+        assert (g.N, g.Np, g.shard, g.slice, g.chunk, g.m, g.steps, g.stride) == \
+            (og.total, og.Np, og.shard, og.slice, og.chunk, og.m, og.steps, og.stride)

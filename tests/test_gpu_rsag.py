@@ -233,3 +233,65 @@ def test_brute_force_small(op, strategy):
                 comm.inject_fault(at_seq=seq + 1, kind="REPAIR", src_rank=r, channel=c)
                 rc, out = run_op(comm, op, xs, count, "int32")
                 assert rc == R.SUCCESS
+
+
+# ------------------------------------------------------------ Broadcast (f1)
+
+from oracle.geometry import BROADCAST  # noqa: E402
+
+
+def run_bcast(comm, xs, count, dtype, root, inplace=False):
+    n = comm.n
+    send = rows(xs, count, dtype)
+    recv = send if inplace else rows([None] * n, count, dtype, poison=True)
+    from paper_2512_25059_b200 import torch_api as T2
+    T2.broadcast(comm, send, recv, root, count=count)
+    rc = comm.sync()
+    out = to_np(recv, dtype)
+    return rc, out[:, :count]
+
+
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16", "float32"])
+@pytest.mark.parametrize("n,root", [(2, 1), (3, 0), (4, 2), (8, 5)])
+@pytest.mark.parametrize("count", [1, 999, 100_003])
+def test_broadcast_fault_free(dtype, n, root, count):
+    comm = comm_for(n)
+    xs = r2inputs.inputs(n, count, dtype, seed=n * 7 + root)
+    rc, out = run_bcast(comm, xs, count, dtype, root)
+    assert rc == R.SUCCESS
+    for r in range(n):
+        assert same_bits(out[r], xs[root]), r
+
+
+def test_broadcast_inplace_root():
+    comm = comm_for(4)
+    xs = r2inputs.inputs(4, 50_001, "bfloat16", seed=3)
+    rc, out = run_bcast(comm, xs, 50_001, "bfloat16", 1, inplace=True)
+    assert rc == R.SUCCESS
+    for r in range(4):
+        assert same_bits(out[r], xs[1])
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+@pytest.mark.parametrize("root", [0, 2])
+def test_broadcast_link_fault_events_exact(strategy, root):
+    n, K, W, count = 4, 4, 2, 100_003
+    comm = sim_comm(n, K, W, 16384, strategy=strategy)
+    t = (1 - root) % n                       # rank 1's chain position: it sends there
+    f = dict(kind="LINK", src_rank=1, channel=2, step=t, chunk=1, byte_offset=4000, poison=1)
+    comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(n, count, "int32", seed=11)
+    rc, out = run_bcast(comm, xs, count, "int32", root)
+    assert rc == R.SUCCESS
+    for r in range(n):
+        assert same_bits(out[r], xs[root])
+    E = 4
+    g = Geometry(n, K, count, E, effective_chunk_bytes(count, n, K, E, 16384, W, BROADCAST), BROADCAST, root=root)
+    res = OP.simulate(xs, g, "int32", faults=oracle_faults([f]), strategy=strategy, seed=1)
+    if t <= n - 2:
+        assert [norm_event(e) for e in comm.events()] == [norm_event(e) for e in res.events]
+        assert comm.events() and comm.events()[0]["resume"] == t * g.m + 1
+    else:
+        assert comm.events() == [] and res.events == []
+    st = comm.status()
+    assert np.array_equal(np.array(st["bytes"])[:, :K], res.bytes_sent)
