@@ -1352,14 +1352,18 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   // every CTA of the rank computes the same mask (records for this seq are
   // never rewritten while it runs, see r2_internal.h)
   {
+    // all records loaded up front (independent loads in flight together; the
+    // short-circuit form issued them one dependent round trip at a time)
     const unsigned int nk = (unsigned int)(p.n * p.K);
     const unsigned int* h = k.me.health;
     unsigned int mask = 0;
+#pragma unroll 4
     for (int c = 0; c < p.K; ++c) {
       const unsigned int a = k.r * p.K + c, b = k.r1 * p.K + c;
-      bool dead = r2_dead_at(h[R2_H_EP_DEAD * nk + a], h[R2_H_EP_REP * nk + a], k.seq) ||
-                  r2_dead_at(h[R2_H_EP_DEAD * nk + b], h[R2_H_EP_REP * nk + b], k.seq) ||
-                  r2_dead_at(h[R2_H_LINK_DEAD * nk + a], h[R2_H_LINK_REP * nk + a], k.seq);
+      const unsigned int ead = h[R2_H_EP_DEAD * nk + a], ear = h[R2_H_EP_REP * nk + a];
+      const unsigned int ebd = h[R2_H_EP_DEAD * nk + b], ebr = h[R2_H_EP_REP * nk + b];
+      const unsigned int lad = h[R2_H_LINK_DEAD * nk + a], lar = h[R2_H_LINK_REP * nk + a];
+      const bool dead = r2_dead_at(ead, ear, k.seq) | r2_dead_at(ebd, ebr, k.seq) | r2_dead_at(lad, lar, k.seq);
       if (!dead) mask |= 1u << c;
     }
     k.conn_mask = mask;
