@@ -465,6 +465,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     c->last_stream = stream;
     return R2_SUCCESS;
   }
+  const uint64_t t_in = r2_debug >= 2 ? r2_now_ns() : 0;
   r2_geometry_t g;
   r2_result_t e = r2_geometry_op(op, count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
   if (e != R2_SUCCESS) return e;
@@ -626,6 +627,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   // bounded run-ahead: a full device launch queue would block the monitor's
   // probe-kernel launches behind a spinning collective (deadlock until the
   // watchdog), so at most kMaxInflight collectives are outstanding
+  const uint64_t t_win0 = r2_debug >= 2 ? r2_now_ns() : 0;
   {
     const uint64_t t0 = r2_now_ns();
     for (;;) {
@@ -638,7 +640,20 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   }
   c->seq = seq;
   c->last_protocol = ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
+  const uint64_t t_pre = r2_debug >= 2 ? r2_now_ns() : 0;
+  static uint64_t sum_win = 0;
+  if (r2_debug >= 2) sum_win += t_pre - t_win0;
   int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W, c->threads, stream);
+  if (r2_debug >= 2) {                       // host enqueue cost breakdown (diagnostics)
+    static uint64_t n_calls = 0, sum_pre = 0, sum_launch = 0;
+    const uint64_t t_post = r2_now_ns();
+    sum_pre += t_pre - t_in;
+    sum_launch += t_post - t_pre;
+    if (++n_calls % 500 == 0)
+      fprintf(stderr, "[r2 enqueue] rank %d: host prep %.2f us (of which in-flight window wait %.2f), "
+              "cooperative launch %.2f us per call\n", c->rank, sum_pre / 1e3 / 500, sum_win / 1e3 / 500,
+              sum_launch / 1e3 / 500), sum_pre = sum_launch = sum_win = 0;
+  }
   c->last_stream = stream;
   if (rc != 0) return R2_ERR_CUDA;
   return R2_SUCCESS;

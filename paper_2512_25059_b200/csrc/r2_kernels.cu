@@ -721,7 +721,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   // plan is noticed within the interval (failover takes ~300 us).
   if (first_try) {
     const unsigned long long now = (unsigned long long)clock64();   // SM cycles: cheap to read
-    if (now - sh.t_ctl >= 40000ull || sh.t_ctl == 0) {
+    if (now - sh.t_ctl >= 40000ull) {
       sh.t_ctl = now;
       const int st = poll_control(k, sh);
       if (st != ST_OK) return st;
@@ -1190,7 +1190,9 @@ __device__ int drain(Cta& k, Shared& sh) {
     // all final incoming completion words present?
     int ok = 1;
     const int nf = p.K * p.m;
-    const int fs = p.op == R2_OP_BROADCAST ? k.t_act - 1 : p.fin_step;   // the root receives nothing
+    // the root of a Broadcast receives nothing; under LL the last incoming step
+    // is consumed by this rank's own unpack items (already delivered)
+    const int fs = p.op == R2_OP_BROADCAST ? k.t_act - 1 : (p.ll && p.local_step >= 0 ? -1 : p.fin_step);
     const unsigned int* fin = k.me.flags + fidx(p, fs < 0 ? 0 : fs, 0, 0);
     for (int i = k.tid; fs >= 0 && i < nf; i += k.nthr)
       if ((int)(ld_relaxed_sys(fin + i) - k.seq) < 0) ok = 0;
@@ -1395,7 +1397,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     sh.first_adopt = 0;
     sh.wait_t0 = 0;
     sh.t_poll = sh.t_prev_poll = 0;
-    sh.t_ctl = 0;
+    sh.t_ctl = (unsigned long long)clock64();   // the plan was read just now: first check after the interval
     sh.npoll = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;
