@@ -31,7 +31,9 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, siz
   ArenaLayout L{};
   const size_t q = (size_t)n * K * 16;
   L.slot_bytes = std::max<size_t>(align_up(std::max<size_t>(max_bytes, 16), q) / n, 16 * K);
-  const size_t slice_cap = L.slot_bytes / K;
+  // chunks per channel slice: a Broadcast's slice is the whole buffer / K (n times an
+  // AllReduce slice)
+  const size_t slice_cap = align_up(std::max<size_t>(max_bytes, 16), (size_t)K * 16) / K;
   L.m_cap = (int)std::max<size_t>((slice_cap + chunk - 1) / chunk, (size_t)W);
   // LL: two 16-byte lines per 16-byte vector, one slot per ring step
   L.ll_slot_bytes = ll_max_bytes ? 2 * std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K) : 0;
@@ -469,7 +471,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   r2_geometry_t g;
   r2_result_t e = r2_geometry_op(op, count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
   if (e != R2_SUCCESS) return e;
-  if (g.shard * E > c->lay.slot_bytes || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
+  if ((op != R2_OP_BROADCAST && g.shard * E > c->lay.slot_bytes) || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
   const uint32_t seq = (uint32_t)(c->seq + 1);
   // protocol: alpha-beta model over the ring's steps; LL
   // moves twice the bytes but pays no fence per step (r2ccl.h "Protocols")

@@ -295,3 +295,16 @@ def test_broadcast_link_fault_events_exact(strategy, root):
         assert comm.events() == [] and res.events == []
     st = comm.status()
     assert np.array_equal(np.array(st["bytes"])[:, :K], res.bytes_sent)
+
+
+def test_broadcast_at_max_bytes():
+    """A Broadcast of exactly max_bytes (its one shard is n times an AllReduce
+    shard; the chunk table must hold it)."""
+    n = 4
+    comm = sim_comm(n, 4, 2, 16384, max_bytes=1 << 20)
+    count = (1 << 20) // 4
+    xs = r2inputs.inputs(n, count, "float32", seed=4)
+    rc, out = run_bcast(comm, xs, count, "float32", 2)
+    assert rc == R.SUCCESS
+    for r in range(n):
+        assert same_bits(out[r], xs[2])
