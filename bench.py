@@ -305,6 +305,16 @@ def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, red
     return out
 
 
+def guarded(fn):
+    """Run an auxiliary bench section; on an exception record it (the
+    headline measurement is printed regardless)."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        print(f"bench: auxiliary section failed: {e!r}", file=sys.stderr, flush=True)
+        return {"error": repr(e)}
+
+
 def successive_scenario(make_comm, run_step, healthy_ms, n, K, geom_m, strategy, get_result, ref_result,
                         fault_rank=3, fault_ch=5, t=3, j=4, b=256 * 1024, stream=None, barrier=lambda: None,
                         reduce_max=lambda x: x, gather=lambda evs: evs):
@@ -381,13 +391,12 @@ def run_sim(a):
         del hs, hr
     comm.finalize()
     if not a.no_fault:
-        res["fault"] = []
-        for strat in ("BALANCE", "HOT_REPAIR"):
-            res["fault"].append(fault_scenario(mk, lambda c: T.allreduce(c, send, recv), ms, S, k, K, g.m, strat,
-                                               lambda: recv, ref, stream=stream))
-        res["successive"] = [successive_scenario(mk, lambda c: T.allreduce(c, send, recv), ms, k, K, g.m, strat,
-                                                 lambda: recv, ref, stream=stream)
-                             for strat in ("BALANCE", "HOT_REPAIR")]
+        res["fault"] = [guarded(lambda strat=strat: fault_scenario(
+            mk, lambda c: T.allreduce(c, send, recv), ms, S, k, K, g.m, strat, lambda: recv, ref, stream=stream))
+            for strat in ("BALANCE", "HOT_REPAIR")]
+        res["successive"] = [guarded(lambda strat=strat: successive_scenario(
+            mk, lambda c: T.allreduce(c, send, recv), ms, k, K, g.m, strat, lambda: recv, ref, stream=stream))
+            for strat in ("BALANCE", "HOT_REPAIR")]
     return res, None
 
 
@@ -517,19 +526,18 @@ def run_multi(a):
                        "nvls": "disabled (NCCL_NVLS_ENABLE=0; the paper disabled SHARP)",
                        "version": ".".join(map(str, torch.cuda.nccl.version()))}
     comm.finalize()
+    # auxiliary sections: an error there is recorded, never loses the headline line
     if not a.no_coll and world >= 2:
-        res["collectives"] = coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, reduce_max,
-                                          pg if not a.no_nccl else None)
+        res["collectives"] = guarded(lambda: coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier,
+                                                          reduce_max, pg if not a.no_nccl else None))
     if not a.no_fault and world >= 2:
-        res["fault"] = []
-        for strat in ("BALANCE", "HOT_REPAIR"):
-            res["fault"].append(fault_scenario(
-                mk, lambda c: T.allreduce(c, send, recv), ms, S, world, K, g.m, strat, lambda: recv, ref,
-                fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0,
-                gather=gather))
-        res["successive"] = [successive_scenario(
+        res["fault"] = [guarded(lambda strat=strat: fault_scenario(
+            mk, lambda c: T.allreduce(c, send, recv), ms, S, world, K, g.m, strat, lambda: recv, ref,
+            fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, is_root=rank == 0,
+            gather=gather)) for strat in ("BALANCE", "HOT_REPAIR")]
+        res["successive"] = [guarded(lambda strat=strat: successive_scenario(
             mk, lambda c: T.allreduce(c, send, recv), ms, world, K, g.m, strat, lambda: recv, ref,
-            fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, gather=gather)
+            fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, gather=gather))
             for strat in ("BALANCE", "HOT_REPAIR")]
     return res, rank
 
