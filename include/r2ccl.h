@@ -386,7 +386,8 @@ void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
 /* Geometry of one collective (SURVEY §8 header, reading C-3).
  * AllReduce: N = count, shards of Np/n at stride shard.
  * Broadcast (f1): N = count, one shard of roundup(count, K*V) = Np, steps
- * n-1 (rank r sends only at its chain position (r - root) mod n).
+ * n-1 (rank r sends only at its chain position (r - root) mod n), chunks
+ * capped at 128 KiB.
  * ReduceScatter / AllGather (f1): N = n * count (the n-shard user buffer),
  * shard = roundup(count, K*V) (the channel split), stride = count (shard
  * distance in the user buffers); steps n (RS: t = n-1 is the owner's LOCAL

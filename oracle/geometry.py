@@ -51,6 +51,7 @@ def ceil_div(a: int, b: int) -> int:
 
 
 ALLREDUCE, REDUCE_SCATTER, ALL_GATHER, BROADCAST = "allreduce", "reduce_scatter", "all_gather", "broadcast"
+BCAST_CHUNK_CAP = 128 * 1024
 
 
 def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1,
@@ -65,6 +66,8 @@ def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: 
     else:
         slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
     per_worker = ceil_div(ceil_div(slice_bytes, W), 16) * 16
+    if op == BROADCAST:   # a chain pipelines per chunk: fill = (n-2) chunk hops (reading R-8)
+        chunk_bytes = min(chunk_bytes, BCAST_CHUNK_CAP)
     return max(16, min(chunk_bytes, per_worker))
 
 

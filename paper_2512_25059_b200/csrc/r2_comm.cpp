@@ -34,7 +34,8 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, siz
   // chunks per channel slice: a Broadcast's slice is the whole buffer / K (n times an
   // AllReduce slice)
   const size_t slice_cap = align_up(std::max<size_t>(max_bytes, 16), (size_t)K * 16) / K;
-  L.m_cap = (int)std::max<size_t>((slice_cap + chunk - 1) / chunk, (size_t)W);
+  const size_t bchunk = std::min<size_t>(chunk, (size_t)128 << 10);   // Broadcast chunk cap (r2_geometry_op)
+  L.m_cap = (int)std::max<size_t>((slice_cap + bchunk - 1) / bchunk, (size_t)W);
   // LL: two 16-byte lines per 16-byte vector, one slot per ring step
   L.ll_slot_bytes = ll_max_bytes ? 2 * std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K) : 0;
   const int steps = n > 1 ? 2 * n - 1 : 1;     // + the LL unpack step

@@ -92,7 +92,9 @@ extern "C" r2_result_t r2_geometry_op(r2_op_t op, uint64_t count, r2_dtype_t dt,
   const uint64_t slice = Np_cap / ((uint64_t)(op == R2_OP_BROADCAST ? 1 : n) * K);
   const uint64_t slice_bytes = slice * E;
   uint64_t per_worker = ((slice_bytes + W - 1) / W + 15) / 16 * 16;
-  uint64_t chunkb = chunk_bytes < per_worker ? chunk_bytes : per_worker;
+  // a Broadcast chain pipelines per chunk (fill = (n-2) chunk hops): 128 KiB cap (reading R-8)
+  const uint64_t cap = op == R2_OP_BROADCAST && chunk_bytes > (128u << 10) ? (128u << 10) : chunk_bytes;
+  uint64_t chunkb = cap < per_worker ? cap : per_worker;
   if (chunkb < 16) chunkb = 16;
   memset(g, 0, sizeof(*g));
   g->N = (op == R2_OP_ALLREDUCE || op == R2_OP_BROADCAST) ? count : (uint64_t)n * count;

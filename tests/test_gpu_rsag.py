@@ -297,12 +297,14 @@ def test_broadcast_link_fault_events_exact(strategy, root):
     assert np.array_equal(np.array(st["bytes"])[:, :K], res.bytes_sent)
 
 
-def test_broadcast_at_max_bytes():
+@pytest.mark.parametrize("chunk", [16384, 512 * 1024])
+def test_broadcast_at_max_bytes(chunk):
     """A Broadcast of exactly max_bytes (its one shard is n times an AllReduce
-    shard; the chunk table must hold it)."""
+    shard, its chunks are capped at 128 KiB: the chunk table must hold it) --
+    the bench's configuration."""
     n = 4
-    comm = sim_comm(n, 4, 2, 16384, max_bytes=1 << 20)
-    count = (1 << 20) // 4
+    comm = sim_comm(n, 8, 16, chunk, max_bytes=4 << 20)
+    count = (4 << 20) // 4
     xs = r2inputs.inputs(n, count, "float32", seed=4)
     rc, out = run_bcast(comm, xs, count, "float32", 2)
     assert rc == R.SUCCESS
