@@ -303,7 +303,7 @@ def test_broadcast_at_max_bytes(chunk):
     shard, its chunks are capped at 128 KiB: the chunk table must hold it) --
     the bench's configuration."""
     n = 4
-    comm = sim_comm(n, 8, 16, chunk, max_bytes=4 << 20)
+    comm = sim_comm(n, 8, 4, chunk, max_bytes=4 << 20)
     count = (4 << 20) // 4
     xs = r2inputs.inputs(n, count, "float32", seed=4)
     rc, out = run_bcast(comm, xs, count, "float32", 2)
