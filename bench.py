@@ -164,25 +164,6 @@ def fill_inputs(send, seed):
     send.copy_(torch.randn(send.shape, generator=g, device=send.device, dtype=torch.float32).to(send.dtype))
 
 
-def sample_parity(send, recv, k_or_world, shard_elems, rank_rows=True, n_sample=4096, seed=5):
-    """Oracle Layer-1 fold on sampled elements, compared with the GPU result."""
-    import numpy as np
-    import torch
-    from oracle import semantic as OS
-    N = send.shape[-1]
-    rng = np.random.default_rng(seed)
-    idx = np.unique(rng.integers(0, N, size=n_sample))
-    it = torch.from_numpy(idx).to(send.device)
-    xs = send[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
-    got = recv[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
-    bad = 0
-    for col, i in enumerate(idx):
-        owner = int(i) // shard_elems
-        want = OS.ring_fold([xs[r, col:col + 1] for r in range(xs.shape[0])], owner, "bfloat16")[0]
-        bad += int(np.any(got[:, col] != want))
-    return {"n_checked": int(len(idx)), "mismatches": bad}
-
-
 class stdout_to_stderr:
     """Route fd 1 to fd 2 (library banners must not break the one-line JSON)."""
 
@@ -377,7 +358,6 @@ def run_sim(a):
     if a.profile:
         return res, None
     ref = recv.clone()
-    res["sample_parity"] = sample_parity(send, recv, k, g.shard)
     if not a.no_e2e:
         hs = torch.empty((k, count), dtype=torch.bfloat16).pin_memory()
         hr = torch.empty_like(hs).pin_memory()
@@ -597,8 +577,6 @@ def report(a, res, n_gpus, n_ranks, mode):
         "gpu_launches": a.steps,
         "clocks": res["clocks"],
     }
-    if "sample_parity" in res:
-        line["sample_parity"] = res["sample_parity"]
     if "e2e" in res:
         e = res["e2e"]
         line["e2e"] = {"value": 2 * (n_ranks - 1) / n_ranks * S / (e["ms"] * 1e-3) / 1e9 * n_ranks, "unit": "GB/s",

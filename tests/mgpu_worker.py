@@ -173,6 +173,39 @@ def case_bcast(comm, rank, world, count, dtype, root, faults=(), strategy="BALAN
     return out
 
 
+def case_fullsize(rank, world, n_sample=4096):
+    """The bench's launch configuration (256 MiB bf16 per rank, K = 8 x W = 16,
+    512 KiB chunks, torch's seeded device RNG): sampled outputs against the
+    oracle fold, every rank."""
+    S = 256 << 20
+    count = S // 2
+    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=16, max_bytes=S))
+    send = torch.empty(count, dtype=torch.bfloat16, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1234 + rank)
+    send.copy_(torch.randn(count, generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16))
+    recv = torch.empty_like(send)
+    T.register(comm, recv)
+    T.allreduce(comm, send, recv)
+    rc = comm.sync()
+    rng = np.random.default_rng(5)
+    idx = np.unique(rng.integers(0, count, size=n_sample))
+    it = torch.from_numpy(idx).cuda()
+    mine = send[it].view(torch.int16).cpu().numpy().view(np.uint16)
+    allx = [None] * world
+    dist.all_gather_object(allx, mine)
+    got = recv[it].view(torch.int16).cpu().numpy().view(np.uint16)
+    geo = R.geometry(count, R.BFLOAT16, world, 8, 16, 512 * 1024)
+    bad = 0
+    for col, i in enumerate(idx):
+        want = OS.ring_fold([allx[r][col:col + 1] for r in range(world)], int(i) // geo.shard, "bfloat16")[0]
+        bad += int(got[col] != want)
+    oks = [None] * world
+    dist.all_gather_object(oks, rc == R.SUCCESS and bad == 0)
+    comm.finalize()
+    return {"op": "fullsize", "N": count, "n_checked": int(len(idx)), "rc": rc, "ok": all(oks)}
+
+
 def main():
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
@@ -209,6 +242,7 @@ def main():
             # degraded steady state (channel 1 of rank world-1 now dead): static plan
             results.append(case(comm, rank, world, 1 << 20, "float32", seed=12))
             comm.finalize()
+        results.append(case_fullsize(rank, world))
         # the LL protocol (f3) forced, over the real NVLink path
         cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=16 * 1024, max_bytes=16 << 20,
                                protocol="LL")
