@@ -310,3 +310,17 @@ def test_broadcast_at_max_bytes(chunk):
     assert rc == R.SUCCESS
     for r in range(n):
         assert same_bits(out[r], xs[2])
+
+
+def test_single_rank_degenerate_copies():
+    """n = 1 (the degenerate case): every collective is a copy of the input."""
+    comm = sim_comm(1, 2, 1, 4096)
+    x = rows(r2inputs.inputs(1, 1001, "float32", seed=1), 1001, "float32")
+    for fn in (lambda y: T.allreduce(comm, x, y, count=1001),
+               lambda y: T.reduce_scatter(comm, x, y, recvcount=1001),
+               lambda y: T.all_gather(comm, x, y, sendcount=1001),
+               lambda y: T.broadcast(comm, x, y, 0, count=1001)):
+        y = rows([None], 1001, "float32", poison=True)
+        fn(y)
+        assert comm.sync() == R.SUCCESS
+        assert torch.equal(y[:, :1001], x[:, :1001])
