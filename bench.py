@@ -41,7 +41,9 @@ def parse():
     ap.add_argument("--sim-ranks", type=int, default=8)
     ap.add_argument("--channels", type=int, default=8)
     ap.add_argument("--ctas", type=int, default=0, help="CTAs per channel (0 = auto)")
-    ap.add_argument("--threads", type=int, default=512)
+    ap.add_argument("--threads", type=int, default=0,
+                    help="threads per CTA (0 = auto: 512 for the HBM-bound simulated ranks, 256 on GPUs -- "
+                         "profiles/r01_sweep_threads_n4.log)")
     ap.add_argument("--chunk", type=int, default=512 * 1024)
     ap.add_argument("--no-fault", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -241,7 +243,8 @@ def coll_section(a, T, R, world, rank, K, W, S, send, recv, stream, barrier, red
     busbw = lambda ms: (n - 1) / n * S / (ms * 1e-3) / 1e9  # noqa: E731
     for strategy in ("BALANCE",):
         for degraded in (False, True):
-            c = T.comm_from_env(R.config_default(nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads,
+            # 512 threads: the ReduceScatter's local final add is HBM-bound (256 halves it)
+            c = T.comm_from_env(R.config_default(nchannels=K, ctas_per_channel=W, threads_per_cta=512,
                                                  chunk_bytes=a.chunk, max_bytes=S, strategy=strategy))
             T.register(c, recv)
             if degraded:   # the config-3 LINK fault, then the steady state with the channel dead
@@ -570,6 +573,7 @@ def report(a, res, n_gpus, n_ranks, mode):
                                 % (S // MIB, n_ranks, "simulated (1 GPU)" if mode == "sim" else "GPU", K, res["W"],
                                    a.chunk // 1024)),
                    "bytes_per_rank": S, "ranks": n_ranks, "mode": mode, "channels": K, "ctas_per_channel": res["W"],
+                   "threads_per_cta": a.threads,
                    "chunks_per_slice": res["m"], "l2": "inputs larger than L2 (no flush)",
                    "parallelism": f"ring allreduce over {n_ranks} ranks"},
         "busbw_per_rank": busbw_rank,
@@ -598,6 +602,8 @@ def main():
     if a.impl == "reference":
         return reference_arm(a)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if not a.threads:
+        a.threads = 256 if world > 1 else 512
     if world > 1:
         res, rank = run_multi(a)
         if rank == 0:
