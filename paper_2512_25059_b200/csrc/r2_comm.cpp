@@ -743,6 +743,46 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
     if (e != R2_SUCCESS) return e;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  if (c->nlocal == 1 && bytes >= ((size_t)8 << 20)) {
+    // Pipelined: segment i's H2D (copy stream), allreduce (caller's stream) and
+    // D2H (second copy stream) overlap with the neighbouring segments'; PCIe
+    // is full duplex, so the call costs about one direction's transfer.  Every
+    // rank derives the same segmentation from count (each segment is one
+    // collective).
+    const size_t V = 16 / (size_t)elem_bytes(dt);
+    const int nseg = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / ((size_t)4 << 20)));
+    const size_t seg = (count + nseg - 1) / nseg / V * V + V;      // elements, 16-byte multiple
+    if (!c->h2d_stream) {
+      CK(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+      c->host_ev.resize(3 * 8 + 1);
+      for (auto& ev : c->host_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    cudaEvent_t ev_begin = c->host_ev[3 * 8];
+    CK(cudaEventRecord(ev_begin, s));                             // after the caller's earlier work
+    CK(cudaStreamWaitEvent(c->h2d_stream, ev_begin, 0));          // (the previous call's D2H included)
+    const char* hs = (const char*)send;
+    char* hr = (char*)recv;
+    int last = -1;
+    for (int i = 0; i < nseg; ++i) {
+      const size_t lo = (size_t)i * seg;
+      if (lo >= count) break;
+      const size_t n_i = std::min(seg, count - lo), off = lo * (size_t)elem_bytes(dt), b_i = n_i * elem_bytes(dt);
+      cudaEvent_t e_in = c->host_ev[3 * i], e_ar = c->host_ev[3 * i + 1], e_out = c->host_ev[3 * i + 2];
+      CK(cudaMemcpyAsync(c->host_stage + off, hs + off, b_i, cudaMemcpyHostToDevice, c->h2d_stream));
+      CK(cudaEventRecord(e_in, c->h2d_stream));
+      CK(cudaStreamWaitEvent(s, e_in, 0));
+      r2_result_t e = enqueue_coll(c, R2_OP_ALLREDUCE, c->host_stage + off, c->host_stage + off, n_i, dt, stream);
+      if (e != R2_SUCCESS) return e;
+      CK(cudaEventRecord(e_ar, s));
+      CK(cudaStreamWaitEvent(c->d2h_stream, e_ar, 0));
+      CK(cudaMemcpyAsync(hr + off, c->host_stage + off, b_i, cudaMemcpyDeviceToHost, c->d2h_stream));
+      CK(cudaEventRecord(e_out, c->d2h_stream));
+      last = i;
+    }
+    if (last >= 0) CK(cudaStreamWaitEvent(s, c->host_ev[3 * last + 2], 0));   // the caller's stream sees it all
+    return R2_SUCCESS;
+  }
   // one contiguous copy each way when the host rows are packed like the stage
   if (stride == bytes || c->nlocal == 1) {
     CK(cudaMemcpyAsync(c->host_stage, send, bytes * c->nlocal, cudaMemcpyHostToDevice, s));
@@ -887,6 +927,9 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   if (c->peers_dev) cudaFree(c->peers_dev);
   if (c->regtab_dev) cudaFree(c->regtab_dev);
   if (c->host_stage) cudaFree(c->host_stage);
+  for (auto& ev : c->host_ev) cudaEventDestroy(ev);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   if (c->mon_stream) cudaStreamDestroy(c->mon_stream);
   if (c->health_stream) cudaStreamDestroy(c->health_stream);
   for (int i = 0; i < r2_comm::kProbeStreams; ++i)

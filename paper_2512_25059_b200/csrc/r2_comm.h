@@ -144,6 +144,8 @@ struct r2_comm {
   char* host_stage = nullptr;
   uint64_t host_stage_reg = 0;
   size_t host_stage_bytes = 0;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;   // pipelined host path
+  std::vector<cudaEvent_t> host_ev;
 
   // shared with the monitor (mu)
   std::mutex mu;

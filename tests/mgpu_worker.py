@@ -206,6 +206,37 @@ def case_fullsize(rank, world, n_sample=4096):
     return {"op": "fullsize", "N": count, "n_checked": int(len(idx)), "rc": rc, "ok": all(oks)}
 
 
+def case_host(rank, world):
+    """r2_allreduce_host on pinned buffers large enough for the pipelined
+    (segmented) path, twice back to back: bit-identical to the oracle fold."""
+    count = (24 << 20) // 2 + 13              # 24 MiB bf16, ragged
+    comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=16, max_bytes=32 << 20))
+    xs = r2inputs.inputs(world, count, "bfloat16", seed=99)
+    hs = torch.from_numpy(xs[rank].view(np.int16).copy()).view(torch.bfloat16).pin_memory()
+    hr = torch.empty_like(hs).pin_memory()
+    ok = True
+    for _ in range(2):
+        hr.view(torch.int16).fill_(-1)
+        T.allreduce_host(comm, hs, hr)
+        rc = comm.sync()
+        torch.cuda.synchronize()
+        E = 2
+        cfg = comm.cfg
+        nseg = min(8, max(1, count * E // (4 << 20)))
+        seg = (count + nseg - 1) // nseg // 8 * 8 + 8
+        got = hr.view(torch.int16).numpy().view(np.uint16)
+        for lo in range(0, count, seg):       # every segment is one collective
+            hi = min(count, lo + seg)
+            g = Geometry(world, cfg.nchannels, hi - lo, E,
+                         effective_chunk_bytes(hi - lo, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel))
+            y = OS.allreduce([x[lo:hi] for x in xs], g.shard, "bfloat16")
+            ok &= rc == R.SUCCESS and np.array_equal(got[lo:hi], y)
+    oks = [None] * world
+    dist.all_gather_object(oks, bool(ok))
+    comm.finalize()
+    return {"op": "allreduce_host", "N": count, "ok": all(oks)}
+
+
 def main():
     out_path = sys.argv[1]
     dist.init_process_group("gloo")
@@ -243,6 +274,7 @@ def main():
             results.append(case(comm, rank, world, 1 << 20, "float32", seed=12))
             comm.finalize()
         results.append(case_fullsize(rank, world))
+        results.append(case_host(rank, world))
         # the LL protocol (f3) forced, over the real NVLink path
         cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=16 * 1024, max_bytes=16 << 20,
                                protocol="LL")
