@@ -314,7 +314,7 @@ r2_result_t r2_broadcast(r2_comm_t comm, const void* send, void* recv, size_t co
  * r2_allreduce_host -- as r2_allreduce, but send/recv are HOST buffers (pinned
  * memory recommended).  Copies into a library-owned registered device buffer,
  * allreduces, copies back; the caller synchronizes `stream` before reading
- * recv.  From 8 MiB on (one rank per process) the payload is cut into up to 8
+ * recv.  From 8 MiB on the payload is cut into up to 8
  * segments, each its own collective, whose H2D copy, allreduce and D2H copy
  * overlap the neighbouring segments' (two library copy streams, ordered with
  * `stream` by events).  The result is that of r2_allreduce applied to each

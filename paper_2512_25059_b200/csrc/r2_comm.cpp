@@ -735,7 +735,7 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
   if (bytes > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
   const size_t stride = align_up(bytes, 16);
-  const size_t need = align_up(c->cfg.max_bytes, 16) * c->nlocal;
+  const size_t need = (align_up(c->cfg.max_bytes, 16) + 4096) * c->nlocal;   // + per-segment row padding
   if (!c->host_stage) {
     CK(cudaMalloc(&c->host_stage, need));
     c->host_stage_bytes = need;
@@ -743,13 +743,16 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
     if (e != R2_SUCCESS) return e;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (c->nlocal == 1 && bytes >= ((size_t)8 << 20)) {
+  if (bytes >= ((size_t)8 << 20)) {
     // Pipelined: segment i's H2D (copy stream), allreduce (caller's stream) and
     // D2H (second copy stream) overlap with the neighbouring segments'; PCIe
     // is full duplex, so the call costs about one direction's transfer.  Every
     // rank derives the same segmentation from count (each segment is one
-    // collective).
+    // collective).  Simulated ranks: segment i of every rank row is packed into
+    // its own stage region [nlocal][roundup(seg_i, 16 B)] (2-D copies), the row
+    // layout a sim-mode collective of seg_i elements expects.
     const size_t V = 16 / (size_t)elem_bytes(dt);
+    const size_t E = (size_t)elem_bytes(dt);
     const int nseg = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / ((size_t)4 << 20)));
     const size_t seg = (count + nseg - 1) / nseg / V * V + V;      // elements, 16-byte multiple
     if (!c->h2d_stream) {
@@ -764,20 +767,24 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
     const char* hs = (const char*)send;
     char* hr = (char*)recv;
     int last = -1;
+    size_t region = 0;                                             // stage offset of segment i's rows
     for (int i = 0; i < nseg; ++i) {
       const size_t lo = (size_t)i * seg;
       if (lo >= count) break;
-      const size_t n_i = std::min(seg, count - lo), off = lo * (size_t)elem_bytes(dt), b_i = n_i * elem_bytes(dt);
+      const size_t n_i = std::min(seg, count - lo), off = lo * E, b_i = n_i * E;
+      const size_t pitch = align_up(b_i, 16);                      // sim rows of this segment
+      char* st = c->host_stage + region;
       cudaEvent_t e_in = c->host_ev[3 * i], e_ar = c->host_ev[3 * i + 1], e_out = c->host_ev[3 * i + 2];
-      CK(cudaMemcpyAsync(c->host_stage + off, hs + off, b_i, cudaMemcpyHostToDevice, c->h2d_stream));
+      CK(cudaMemcpy2DAsync(st, pitch, hs + off, stride, b_i, c->nlocal, cudaMemcpyHostToDevice, c->h2d_stream));
       CK(cudaEventRecord(e_in, c->h2d_stream));
       CK(cudaStreamWaitEvent(s, e_in, 0));
-      r2_result_t e = enqueue_coll(c, R2_OP_ALLREDUCE, c->host_stage + off, c->host_stage + off, n_i, dt, stream);
+      r2_result_t e = enqueue_coll(c, R2_OP_ALLREDUCE, st, st, n_i, dt, stream);
       if (e != R2_SUCCESS) return e;
       CK(cudaEventRecord(e_ar, s));
       CK(cudaStreamWaitEvent(c->d2h_stream, e_ar, 0));
-      CK(cudaMemcpyAsync(hr + off, c->host_stage + off, b_i, cudaMemcpyDeviceToHost, c->d2h_stream));
+      CK(cudaMemcpy2DAsync(hr + off, stride, st, pitch, b_i, c->nlocal, cudaMemcpyDeviceToHost, c->d2h_stream));
       CK(cudaEventRecord(e_out, c->d2h_stream));
+      region += pitch * c->nlocal;
       last = i;
     }
     if (last >= 0) CK(cudaStreamWaitEvent(s, c->host_ev[3 * last + 2], 0));   // the caller's stream sees it all

@@ -9,6 +9,7 @@ import torch
 
 import r2inputs
 from oracle import protocol as OP
+from oracle import semantic as OS
 from tests.gpu_util import (check_result, norm_event, oracle_faults, oracle_geom, poisoned, run, same_bits,
                             sim_comm, to_dev, to_np)
 from paper_2512_25059_b200 import build as B
@@ -99,6 +100,43 @@ def test_host_buffers():
     T.allreduce_host(comm, send, recv)
     assert comm.sync() == R.SUCCESS
     check_result(recv.numpy(), xs, oracle_geom(comm, N, "float32"), "float32")
+
+
+def host_segments(count, E):
+    """The pipelined host path's segmentation (r2ccl.h r2_allreduce_host)."""
+    if count * E < (8 << 20):
+        return [(0, count)]
+    V = 16 // E
+    nseg = min(8, max(1, count * E // (4 << 20)))
+    seg = (count + nseg - 1) // nseg // V * V + V
+    return [(lo, min(count, lo + seg)) for lo in range(0, count, seg)][:nseg]
+
+
+@pytest.mark.parametrize("N", [(12 << 20) // 2 + 5, (9 << 20) // 2])
+def test_host_buffers_segmented(N):
+    """From 8 MiB on the host path is segmented and pipelined; every segment
+    is its own collective: bit-exact against the oracle fold per segment
+    (ragged rows: 2-D copies into packed per-segment stage rows)."""
+    n, dt = 4, "bfloat16"
+    comm = sim_comm(n, 4, 2, 64 * 1024, max_bytes=16 << 20)
+    xs = r2inputs.inputs(n, N, dt, seed=17)
+    row = -(-N // 8) * 8
+    a = np.zeros((n, row), dtype=np.uint16)
+    a[:, :N] = np.stack(xs)
+    send = torch.from_numpy(a.view(np.int16)).pin_memory()
+    recv = torch.empty_like(send).pin_memory()
+    for _ in range(2):
+        recv.fill_(-1)
+        comm.allreduce_host(send.data_ptr(), recv.data_ptr(), N, R.BFLOAT16, torch.cuda.current_stream().cuda_stream)
+        assert comm.sync() == R.SUCCESS
+        torch.cuda.synchronize()
+        out = recv.numpy().view(np.uint16)
+        for lo, hi in host_segments(N, 2):
+            g = oracle_geom(comm, hi - lo, dt)
+            y = OS.allreduce([x[lo:hi] for x in xs], g.shard, dt)
+            for r in range(n):
+                assert same_bits(out[r, lo:hi], y), (lo, r)
+        assert np.all(out[:, N:] == 0xFFFF)      # row padding untouched
 
 
 # ------------------------------------------------------------ faults
