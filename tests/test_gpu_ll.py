@@ -193,3 +193,20 @@ def test_ll_speculation_with_midcall_fault_many_points():
         comm.inject_fault(at_seq=seq + 1, kind="REPAIR", src_rank=t % n, channel=t % K)
         rc, out = run(comm, xs, "bfloat16")
         assert rc == R.SUCCESS
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_ll_inplace_with_fault(strategy):
+    """In-place AllReduce under LL with a mid-collective LINK fault in the fused
+    final-add step (the staged own shard protects the overwritten input)."""
+    n, K, W, N = 4, 3, 2, 40_003
+    comm = sim_comm(n, K, W, 4096, strategy=strategy, protocol="LL")
+    f = dict(kind="LINK", src_rank=1, channel=2, step=n - 1, chunk=1, byte_offset=512, poison=1)
+    comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(n, N, "bfloat16", seed=44)
+    rc, out = run(comm, xs, "bfloat16", inplace=True)
+    assert rc == R.SUCCESS
+    g = geom(comm, AR, N, "bfloat16")
+    check_result(out, xs, g, "bfloat16")
+    res = OP.simulate(xs, g, "bfloat16", faults=oracle_faults([f]), strategy=strategy, seed=1, inplace=True)
+    assert [norm_event(e) for e in comm.events()] == [norm_event(e) for e in res.events]

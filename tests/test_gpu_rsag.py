@@ -324,3 +324,20 @@ def test_single_rank_degenerate_copies():
         fn(y)
         assert comm.sync() == R.SUCCESS
         assert torch.equal(y[:, :1001], x[:, :1001])
+
+
+@pytest.mark.parametrize("kind", ["LOCAL", "REMOTE"])
+def test_broadcast_endpoint_faults(kind):
+    """Endpoint faults on a Broadcast chain: the root's buffer still arrives
+    everywhere bit for bit."""
+    n, K, W, count, root = 4, 3, 2, 80_001, 1
+    comm = sim_comm(n, K, W, 8192)
+    src = 2                                   # chain position 1 for root 1
+    f = dict(kind=kind, src_rank=src, channel=0, step=(src - root) % n, chunk=0, byte_offset=256, poison=1)
+    comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(n, count, "int32", seed=5)
+    rc, out = run_bcast(comm, xs, count, "int32", root)
+    assert rc == R.SUCCESS
+    for r in range(n):
+        assert same_bits(out[r], xs[root]), r
+    assert any(e["rank"] == src for e in comm.events())
