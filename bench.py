@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-coll", action="store_true", help="skip the standalone ReduceScatter / AllGather section")
     ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
+    ap.add_argument("--bw-model-gbps", type=int, default=80,
+                    help="per-channel bandwidth of the channel-as-NIC fault section (0 = skip; r2ccl.h channel_gbps)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
     ap.add_argument("--per-step", action="store_true", help="debug: per-step CUDA-event times to stderr")
     ap.add_argument("--clock-ms", type=int, default=20, help="nvidia-smi sampling period (ms)")
@@ -551,7 +553,38 @@ def run_multi(a):
             mk, lambda c: T.allreduce(c, send, recv), ms, world, K, g.m, strat, lambda: recv, ref,
             fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, gather=gather))
             for strat in ("BALANCE", "HOT_REPAIR")]
+    if not a.no_fault and world >= 2 and a.bw_model_gbps > 0:
+        res["fault_bw_model"] = guarded(lambda: bw_model_section(
+            a, T, R, mk, send, recv, ref, S, world, K, W, g.m, stream, barrier, reduce_max, gather))
     return res, rank
+
+
+def bw_model_section(a, T, R, mk_default, send, recv, ref, S, world, K, W, m, stream, barrier, reduce_max, gather):
+    """Config 3 with channels as bandwidth units (r2ccl.h channel_gbps): every
+    lane paces its sends to channel_gbps / W, as a NIC would, so one dead
+    channel of K costs bandwidth -- the setting of the paper's surviving-
+    bandwidth bound (Balance (K-1)/K, HotRepair 1/2)."""
+    def mk(strategy):
+        c = T.comm_from_env(R.config_default(
+            nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+            strategy=strategy, protocol=a.protocol, channel_gbps=a.bw_model_gbps))
+        T.register(c, recv)
+        return c
+    c = mk("BALANCE")
+    step = lambda: T.allreduce(c, send, recv)  # noqa: E731
+    for _ in range(3):
+        step()
+    barrier()
+    ms_h = reduce_max(timed(step, 20, stream))
+    assert c.sync() == R.SUCCESS
+    c.finalize()
+    out = {"channel_gbps": a.bw_model_gbps, "ms_healthy": ms_h,
+           "busbw_per_rank_healthy": 2 * (world - 1) / world * S / (ms_h * 1e-3) / 1e9, "fault": []}
+    for strat in ("BALANCE", "HOT_REPAIR"):
+        out["fault"].append(fault_scenario(mk, lambda cc: T.allreduce(cc, send, recv), ms_h, S, world, K, m, strat,
+                                           lambda: recv, ref, fault_rank=3 % world, stream=stream, barrier=barrier,
+                                           reduce_max=reduce_max, gather=gather))
+    return out
 
 
 def ncu_traffic(a, n_ranks, W):
@@ -627,6 +660,8 @@ def report(a, res, n_gpus, n_ranks, mode):
         line["fault"] = res["fault"]
     if "successive" in res:
         line["successive_failover"] = res["successive"]
+    if "fault_bw_model" in res:
+        line["fault_bandwidth_model"] = res["fault_bw_model"]
     return line
 
 

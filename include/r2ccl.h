@@ -120,6 +120,11 @@ typedef struct {
  *                     microseconds, then exponential back-off ("adapting
  *                     probe frequency"); default 2000, 0 disables re-probing
  *   reprobe_max_us    back-off cap (default 200000)
+ *   channel_gbps      bandwidth model of a channel (0 = off, the default): every
+ *                     lane paces its sends to channel_gbps / W, so a channel is
+ *                     a bandwidth unit like the paper's NIC (reading C-1: without
+ *                     it channels share the GPU's NVLink ports and a dead channel
+ *                     only removes CTAs)
  *   alpha_simple_ns, alpha_ll_ns, beta_mbps
  *                     cost model: T = (#ring steps) * alpha + (wire bytes per
  *                     rank) / beta, LL moving twice the bytes (defaults from
@@ -151,6 +156,7 @@ typedef struct {
   int alpha_simple_ns, alpha_ll_ns;
   int beta_mbps;
   int reprobe_us, reprobe_max_us;
+  int channel_gbps;
 } r2_config_t;
 
 typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2 } r2_protocol_t;

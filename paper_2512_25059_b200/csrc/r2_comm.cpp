@@ -513,6 +513,8 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.peer_recv = !ll && op != R2_OP_REDUCE_SCATTER;
   p.ll = ll;
   p.ll_slot_bytes = c->lay.ll_slot_bytes;
+  if (c->cfg.channel_gbps > 0)          // lane rate = channel rate / W
+    p.lane_ps_per_byte = (unsigned int)((1000ull * c->W + c->cfg.channel_gbps / 2) / c->cfg.channel_gbps);
   p.sstride = g.stride;
   p.slen = op == R2_OP_ALLREDUCE ? g.shard : count;
   // in-place (NCCL's convention for RS / AG: recv / send is the own shard)

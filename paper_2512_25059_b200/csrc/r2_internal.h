@@ -151,6 +151,7 @@ struct LaunchParams {
   unsigned long long sstride, slen;      // shard stride in the user buffers / valid elements per shard
   size_t slot_bytes;
   int ll;                                // LL protocol (r2ccl.h "Protocols")
+  unsigned int lane_ps_per_byte;         // channel bandwidth model: pacing per lane (0 = off)
   size_t ll_slot_bytes;
   unsigned long long watchdog_ns;
   int trace;                             // record the r2_trace timeline

@@ -227,6 +227,7 @@ struct Shared {
   unsigned long long wait_t0;
   unsigned long long t_poll, t_prev_poll;   // diagnostics
   unsigned long long t_ctl;                 // last control / fabric check of try_publish
+  unsigned long long pace_next;             // channel bandwidth model: earliest next send
   unsigned int npoll;
   unsigned long long full[NSLOT];
   unsigned long long empty[NSLOT];
@@ -747,6 +748,13 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   const bool local = t == p.local_step;
   if (p.peer_recv && (ta >= n - 1 || p.op == R2_OP_BROADCAST) && !local && !try_recv_next(k, sh))
     return ST_NOTREADY;
+  if (p.lane_ps_per_byte && !local) {
+    // channel bandwidth model (r2ccl.h channel_gbps): a token bucket per lane
+    const unsigned long long now = gtimer();
+    if (now < sh.pace_next) return ST_NOTREADY;
+    const unsigned long long wire = (unsigned long long)(it.hi - it.lo) * 16ull * (p.ll ? 2ull : 1ull);
+    sh.pace_next = (now > sh.pace_next ? now : sh.pace_next) + wire * p.lane_ps_per_byte / 1000ull;
+  }
 
   const int E = p.elem_bytes, V = p.V;
   const int s_ = p.op == R2_OP_BROADCAST ? 0
@@ -1398,6 +1406,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     sh.wait_t0 = 0;
     sh.t_poll = sh.t_prev_poll = 0;
     sh.t_ctl = (unsigned long long)clock64();   // the plan was read just now: first check after the interval
+    sh.pace_next = 0;
     sh.npoll = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;

@@ -47,7 +47,7 @@ class Config(C.Structure):
                 ("channel_w", C.c_int * MAX_CHANNELS), ("use_channel_w", C.c_int), ("sim_ranks", C.c_int),
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
                 ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
-                ("reprobe_max_us", C.c_int)]
+                ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int)]
 
 
 PROTO_AUTO, PROTO_SIMPLE, PROTO_LL = 0, 1, 2

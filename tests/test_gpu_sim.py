@@ -402,3 +402,23 @@ def test_reprobe_disabled_keeps_connection_dead():
     time.sleep(0.02)
     st = comm.status()
     assert st["n_reprobes"] == 0 and (0, 1) in st["dead_links"]
+
+
+@pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
+def test_channel_bandwidth_model(strategy):
+    """channel_gbps (channels as bandwidth units, r2ccl.h): paced lanes give the
+    same bits and the same failover records as the unpaced path."""
+    n, K, W, N = 4, 3, 2, 200_003
+    comm = sim_comm(n, K, W, 16384, strategy=strategy, channel_gbps=20)
+    f = dict(kind="LINK", src_rank=2, channel=1, step=2, chunk=1, byte_offset=5000, poison=1)
+    comm.inject_fault(at_seq=1, **f)
+    xs = r2inputs.inputs(n, N, "int32", seed=51)
+    rc, out = run(comm, xs, "int32")
+    assert rc == R.SUCCESS
+    g = oracle_geom(comm, N, "int32")
+    check_result(out, xs, g, "int32")
+    res = OP.simulate(xs, g, "int32", faults=oracle_faults([f]), strategy=strategy, seed=1)
+    assert [norm_event(e) for e in comm.events()] == [norm_event(e) for e in res.events]
+    rc, out = run(comm, xs, "int32")          # degraded steady state, paced
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, "int32")
