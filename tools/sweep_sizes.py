@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--sim-ranks", type=int, default=8)
     ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = 512 sim / 256 GPUs, as bench.py)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -54,7 +55,7 @@ def main():
     else:
         dist.init_process_group("gloo")
         comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=maxb, protocol=a.protocol,
-                                                ll_max_bytes=min(maxb, 32 << 20)))
+                                                ll_max_bytes=min(maxb, 32 << 20), threads_per_cta=a.threads or 256))
         os.environ["NCCL_NVLS_ENABLE"] = "0"
         saved = os.dup(1)
         os.dup2(2, 1)
