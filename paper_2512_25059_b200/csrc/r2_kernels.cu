@@ -554,7 +554,8 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
 // The merged work list of one CTA in (step, origin, chunk) order: its own
 // chunks (j = w, w+W, ...) and the chunks it adopts for dead origins (static
 // plan: plan-time placement from the health records; dynamic plan: the
-// monitor's residual bitmaps).  Resumable iterator of the control lane.
+// monitor's plan entries; a re-placed chunk is skipped once its completion
+// word is set).  Resumable iterator of the control lane.
 struct Iter {
   int t, o, j;
 };
