@@ -138,7 +138,8 @@ def oracle_rate(k: int, sample_bytes: int, reps: int = 1) -> dict:
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     import r2inputs
     from oracle import protocol as OP
-    from oracle.geometry import Geometry, effective_chunk_bytes
+    from oracle.geometry import Geometry
+    from tests.scenario import effective_chunk_bytes
     N = sample_bytes // 2
     xs = r2inputs.inputs(k, N, "bfloat16", seed=1)
     g = Geometry(k, 8, N, 2, effective_chunk_bytes(N, k, 8, 2, 512 * 1024, 1))

@@ -212,6 +212,13 @@ typedef struct {
   uint64_t t_fire_dev_ns, t_first_retx_dev_ns;
   uint64_t t_detect_host_ns, t_verdict_host_ns, t_plan_host_ns;
   double failover_ms;     /* t_first_retx_dev - t_fire_dev (-1 if unknown)     */
+  /* bilateral notification ("notifies both sides to avoid
+     half-open states"): the detector's NOTIFY and the acknowledgements of
+     every rank (the other endpoint included); filled in on the detecting
+     rank's record once the acknowledgements arrive                          */
+  int notify_acks;        /* acknowledgements received (expected: world)      */
+  int notify_peer_acked;  /* the connection's other endpoint acknowledged     */
+  double notify_ack_ms;   /* NOTIFY sent -> last acknowledgement (-1 pending) */
 } r2_event_t;
 
 typedef struct {
@@ -226,6 +233,8 @@ typedef struct {
   int last_protocol;          /* r2_protocol_t the last enqueued collective used  */
   int n_readmits;             /* connections re-admitted after a successful re-probe */
   int n_reprobes;             /* re-probe rounds run                              */
+  int n_service_kernels;      /* standalone service-kernel launches (monitor work
+                                 with no collective resident to serve it)         */
 } r2_status_t;
 
 /* Fill *cfg with the defaults documented above. */

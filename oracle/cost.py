@@ -6,8 +6,12 @@ P:78 (§5.1 Overhead Analysis): "a ReduceScatter retains only a 1/n shard and
 must send (n-1)/n D_total; an AllGather must receive the same amount ... The
 NCCL's ring algorithm realizes these lower bounds."  P:121: "The time for a
 ring AllReduce is given by 2(ng-1)/(ng) x D/B."  P:122-136 and App. A
-(P:358-447): T1, T2, T3, T(Y), Y*, threshold.  nccl-tests bus bandwidth
-(the paper's tool): busbw = algbw * 2(n-1)/n.
+(P:358-447): T1, T2, T3, T(Y), Y*, threshold.
+
+Pins (tests/test_oracle_host.py): nvlink_bytes_per_gpu and hbm_bytes_per_gpu
+against the bytes the Layer-2 simulator actually moves (oracle/protocol.py
+SimResult.bytes_sent / hbm_bytes) and SURVEY §8(d)'s printed table; App. A
+against SPEC's printed values, T1(Y*) = T2(Y*) and a grid argmin.
 """
 from __future__ import annotations
 
@@ -16,11 +20,6 @@ def ring_allreduce_time(n: int, g: int, D: float, B: float) -> float:
     """P:121: 2(ng-1)/(ng) * D/B."""
     ng = n * g
     return 2 * (ng - 1) / ng * D / B
-
-
-def busbw(S_bytes: float, seconds: float, n: int) -> float:
-    """nccl-tests bus bandwidth (bytes/s)."""
-    return S_bytes / seconds * 2 * (n - 1) / n if n > 1 else 0.0
 
 
 def nvlink_bytes_per_gpu(S: float, n: int) -> float:
@@ -41,20 +40,6 @@ def hbm_bytes_per_gpu(S: float, n: int) -> float:
     writes (n-1)+1+(n-1) = 2n-1.
     """
     return (5 * n - 4) / n * S
-
-
-def hbm_bytes_sim(S: float, k: int) -> float:
-    """1-GPU simulated-rank mode with k ranks: all ranks' traffic is local:
-    (5k-4)/k S per rank x k ranks."""
-    return (5 * k - 4) * S
-
-
-def degraded_bound(healthy_busbw: float, K: int, dead: int = 1, strategy: str = "BALANCE") -> float:
-    """Surviving-bandwidth bound (SURVEY §8(d)): Balance (K-dead)/K of healthy;
-    HotRepair model: the backup carries 2x -> 1/2."""
-    if strategy == "HOT_REPAIR":
-        return healthy_busbw * 0.5
-    return healthy_busbw * (K - dead) / K
 
 
 # ------------------------------------------------------------- App. A (NEXT)

@@ -10,12 +10,13 @@ P:94 ring AllReduce = ReduceScatter then AllGather; reading C-3 (chunking).
 * N' = roundup(N, n*K*V) (logical padding, read as 0, never written).
 * shard s = [s*N'/n, (s+1)*N'/n); channel slice c of each shard has
   N'/(n*K) elements; chunks j = 0..m-1 of <= chunk elements (last may be short).
+  The chunk size is an INPUT of the scenario (chunk_bytes), like n and K: the
+  oracle does not derive the library's chunking policy (readings C-3 / R-8;
+  tests/scenario.py states the policy a configured communicator uses).
 * connection (r -> r+1, channel c) carries stream positions q = t*m + j,
   t = 0..2n-3: steps 0..n-2 are reduce-scatter, n-1..2n-3 all-gather.
 * at step t rank r sends shard (r-1-t) mod n during RS and
   (r-(t-n+1)) mod n during AG.
-* effective chunk: min(configured chunk, ceil(slice / W) rounded up to a
-  vector) so that W workers per channel all get chunks (reading C-3).
 
 Standalone ReduceScatter / AllGather: the two
 halves of the same ring.  N is then the per-rank shard count (recvcount /
@@ -51,33 +52,13 @@ def ceil_div(a: int, b: int) -> int:
 
 
 ALLREDUCE, REDUCE_SCATTER, ALL_GATHER, BROADCAST = "allreduce", "reduce_scatter", "all_gather", "broadcast"
-BCAST_CHUNK_CAP = 128 * 1024
-
-
-def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1,
-                          op: str = ALLREDUCE) -> int:
-    """Chunk size actually used (reading C-3); multiple of 16 bytes."""
-    V = 16 // elem_bytes
-    if op == ALLREDUCE:
-        Np = ceil_div(max(N, 1), n * K * V) * n * K * V
-        slice_bytes = Np // (n * K) * elem_bytes
-    elif op == BROADCAST:
-        slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
-    else:
-        slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
-    per_worker = ceil_div(ceil_div(slice_bytes, W), 16) * 16
-    if op == BROADCAST:   # a chain pipelines per chunk: fill = (n-2) chunk hops (reading R-8)
-        chunk_bytes = min(chunk_bytes, BCAST_CHUNK_CAP)
-    return max(16, min(chunk_bytes, per_worker))
-
-
 @dataclass(frozen=True)
 class Geometry:
     n: int
     K: int
     N: int
     elem_bytes: int
-    chunk_bytes: int          # the effective chunk (multiple of 16)
+    chunk_bytes: int          # the scenario's chunk (multiple of 16)
     op: str = ALLREDUCE       # N = per-shard count for REDUCE_SCATTER / ALL_GATHER
     ll: bool = False          # LL protocol: + the LOCAL unpack step (AllReduce / AllGather)
     root: int = 0             # BROADCAST only

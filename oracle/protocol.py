@@ -114,6 +114,7 @@ class SimResult:
     retransmitted_items: int
     retransmitted_bytes: int
     fired: list
+    hbm_bytes: np.ndarray | None = None   # [rank] bytes read from / written into rank's own memory
 
 
 class Simulator:
@@ -180,6 +181,9 @@ class Simulator:
         self.faults = [f for f in faults]
         self.fired: list = []
         self.bytes_sent = np.zeros((n, K), dtype=np.int64)
+        # bytes each rank's memory serves (reads) or absorbs (writes, local or
+        # arriving from the upstream peer): the executed schedule's HBM traffic
+        self.hbm = np.zeros(n, dtype=np.int64)
         self.events: list = []
         self.detections: list = []
         self.pending: list = []            # host notifications (rank, channel)
@@ -260,6 +264,7 @@ class Simulator:
         o0, o1 = e0 - s * g.stride, e1 - s * g.stride    # offsets inside the shard
         lim = g.shard_limit(s)
         r1 = (r + 1) % n
+        nb = (e1 - e0) * g.elem_bytes                     # bytes of one operand of this part
         if g.local(t) and self.op != REDUCE_SCATTER:      # LL unpack: the data already landed here
             return
         if self.op == BROADCAST:                          # chain: root's input, else what arrived here
@@ -270,16 +275,21 @@ class Simulator:
             return
         if ta <= n - 2:                                   # reduce-scatter hop
             val = self.xread(r, e0, e1, lim)
+            self.hbm[r] += nb
             if t > 0:
                 val = hop_add(self.scratch[r][t - 1][o0:o1], val, self.dtype)
+                self.hbm[r] += nb
             self.scratch[r1][t][o0:o1] = val
+            self.hbm[r1] += nb
         elif ta == n - 1 and self.op == ALLREDUCE:        # final add + first all-gather send
             val = hop_add(self.scratch[r][n - 2][o0:o1], self.xread(r, e0, e1, lim), self.dtype)
+            self.hbm[r] += 3 * nb                         # scratch + x read, own result written
             if self.inplace:
                 self.stage[r][o0:o1] = val
             else:
                 self.rwrite(r, e0, val, lim)
             self.rwrite(r1, e0, val, lim)
+            self.hbm[r1] += nb
         elif ta == n - 1 and self.op == REDUCE_SCATTER:   # final add into the own output (LOCAL)
             val = hop_add(self.scratch[r][n - 2][o0:o1], self.xread(r, e0, e1, lim), self.dtype)
             self.rwrite(r, e0, val, lim, base=s * g.stride)
@@ -290,6 +300,8 @@ class Simulator:
             self.rwrite(r1, e0, val, lim)
         else:                                             # all-gather forward
             self.rwrite(r1, e0, self.rread(r, e0, e1, lim), lim)
+            self.hbm[r] += nb
+            self.hbm[r1] += nb
 
     def _run_task(self, w, task: Task):
         r, c = w
@@ -454,7 +466,7 @@ class Simulator:
         health = {"dead_endpoints": sorted((r, c) for r in range(self.n) for c in range(self.K) if self.known_ep_dead[r][c]),
                   "dead_links": sorted((r, c) for r in range(self.n) for c in range(self.K) if self.known_link_dead[r][c])}
         return SimResult(self.recv, self.events, self.detections, self.bytes_sent, self.error, health,
-                         self.retx_items, self.retx_bytes, list(self.fired))
+                         self.retx_items, self.retx_bytes, list(self.fired), self.hbm)
 
 
 def simulate(xs, geom: Geometry, dtype: str, **kw) -> SimResult:

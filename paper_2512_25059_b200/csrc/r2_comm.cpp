@@ -160,6 +160,52 @@ void track_live(r2_comm* c, bool add) {
   }
 }
 
+// Every resource r2_init may have acquired (null / empty members are
+// skipped): the error path of r2_init and r2_finalize share it.
+void release_resources(r2_comm* c) {
+  for (auto& rg : c->regs)
+    for (void* p : rg.opened) close_peer(c, p);
+  c->regs.clear();
+  for (void* p : c->peer_arena_opened)
+    if (p) cudaIpcCloseMemHandle(p);
+  c->peer_arena_opened.clear();
+  for (char* a : c->arena)
+    if (a) cudaFree(a);
+  c->arena.clear();
+  for (Ctrl* h : c->ctrl_host)
+    if (h) cudaFreeHost(h);
+  c->ctrl_host.clear();
+  if (c->probe_res_host) cudaFreeHost((void*)c->probe_res_host);
+  if (c->probe_t0_host) cudaFreeHost((void*)c->probe_t0_host);
+  if (c->svc_host) cudaFreeHost(c->svc_host);
+  if (c->flags_map_host) cudaFreeHost(c->flags_map_host);
+  if (c->health_map_host) cudaFreeHost(c->health_map_host);
+  if (c->health_pinned) cudaFreeHost(c->health_pinned);
+  if (c->peers_dev) cudaFree(c->peers_dev);
+  if (c->regtab_dev) cudaFree(c->regtab_dev);
+  if (c->host_stage) cudaFree(c->host_stage);
+  for (auto& ev : c->host_ev) cudaEventDestroy(ev);
+  if (c->svc_ev) cudaEventDestroy(c->svc_ev);
+  cudaStream_t streams[] = {c->h2d_stream, c->d2h_stream, c->mon_stream, c->health_stream, c->svc_stream};
+  for (cudaStream_t s : streams)
+    if (s) cudaStreamDestroy(s);
+  for (int i = 0; i < r2_comm::kProbeStreams; ++i)
+    if (c->probe_stream[i]) cudaStreamDestroy(c->probe_stream[i]);
+}
+
+// host-mapped pinned block: host pointer + device alias
+template <class T>
+bool alloc_mapped(size_t bytes, T** host, T** dev) {
+  void* h = nullptr;
+  if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped) != cudaSuccess) return false;
+  memset(h, 0, bytes);
+  *host = (T*)h;
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return false;
+  *dev = (T*)d;
+  return true;
+}
+
 int take_async_error(r2_comm* c) {
   std::lock_guard<std::mutex> g(c->mu);
   int e = c->unreported_error;
@@ -245,6 +291,8 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   }
   c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes, cfg.ll_max_bytes);
   auto fail = [&](r2_result_t e) {
+    cudaDeviceSynchronize();
+    release_resources(c);
     delete c;
     return e;
   };
@@ -254,9 +302,9 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   }
 
   // ---- arenas (scratch, flags, counters, fabric state, mailboxes)
-  c->arena.resize(c->nlocal);
-  c->ctrl_host.resize(c->nlocal);
-  c->ctrl_dev.resize(c->nlocal);
+  c->arena.assign(c->nlocal, nullptr);
+  c->ctrl_host.assign(c->nlocal, nullptr);
+  c->ctrl_dev.assign(c->nlocal, nullptr);
   for (int l = 0; l < c->nlocal; ++l) {
     if (cudaMalloc(&c->arena[l], c->lay.total) != cudaSuccess) return fail(R2_ERR_CUDA);
     if (cudaMemset(c->arena[l], 0, c->lay.total) != cudaSuccess) return fail(R2_ERR_CUDA);
@@ -283,6 +331,12 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     memset(h, 0, sizeof(unsigned long long) * r2_comm::kProbeSlots);
     if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) return fail(R2_ERR_CUDA);
     c->probe_t0_dev = (unsigned long long*)d;
+    if (!alloc_mapped(sizeof(SvcBlock), &c->svc_host, &c->svc_dev)) return fail(R2_ERR_CUDA);
+    const size_t flag_words = (size_t)(c->n > 1 ? 2 * c->n - 1 : 1) * c->K * c->lay.m_cap;
+    if (!alloc_mapped(flag_words * 4, &c->flags_map_host, &c->flags_map_dev)) return fail(R2_ERR_CUDA);
+    if (!alloc_mapped((size_t)4 * c->n * c->K * 4, &c->health_map_host, &c->health_map_dev)) return fail(R2_ERR_CUDA);
+    if (cudaStreamCreateWithFlags(&c->svc_stream, cudaStreamNonBlocking) != cudaSuccess) return fail(R2_ERR_CUDA);
+    if (cudaEventCreateWithFlags(&c->svc_ev, cudaEventDisableTiming) != cudaSuccess) return fail(R2_ERR_CUDA);
   }
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(R2_ERR_CUDA);
 
@@ -338,10 +392,6 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     if (cudaHostAlloc(&h, c->health.size() * sizeof(uint32_t), cudaHostAllocDefault) != cudaSuccess)
       return fail(R2_ERR_CUDA);
     c->health_pinned = (uint32_t*)h;
-    const int steps_cap = c->n > 1 ? 2 * c->n - 1 : 1;
-    if (cudaHostAlloc(&h, (size_t)steps_cap * c->K * c->lay.m_cap * 4, cudaHostAllocDefault) != cudaSuccess)
-      return fail(R2_ERR_CUDA);
-    c->flags_pinned = (unsigned int*)h;
   }
   if (c->n > 1) {
     // pre-load the kernels (see r2_warmup): a healthy self-probe
@@ -551,6 +601,7 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     p.recv[l] = (char*)recv + (size_t)l * rstride;
     p.ctrl[l] = c->ctrl_dev[l];
   }
+  p.svc = c->svc_dev;
   if (!c->sim && p.peer_recv) {
     const size_t rbytes = (size_t)g.N * E;
     int found = -1;
@@ -639,8 +690,12 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
       uint32_t done = 0xFFFFFFFFu;
       for (int l = 0; l < c->nlocal; ++l) done = std::min(done, (uint32_t)c->ctrl_host[l]->done_seq);
       if ((int32_t)(seq - done) <= kMaxInflight) break;
-      if (r2_now_ns() - t0 > (uint64_t)c->cfg.watchdog_ms * 3000000ull) return R2_ERR_TIMEOUT;
-      std::this_thread::yield();
+      // every kernel ends within its watchdog (the service lane publishes
+      // done_seq on any exit): twice that is a broken device
+      const uint64_t waited = r2_now_ns() - t0;
+      if (waited > (uint64_t)c->cfg.watchdog_ms * 2000000ull) return R2_ERR_TIMEOUT;
+      if (waited > 1000000ull) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      else std::this_thread::yield();
     }
   }
   c->seq = seq;
@@ -648,7 +703,8 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   const uint64_t t_pre = r2_debug >= 2 ? r2_now_ns() : 0;
   static uint64_t sum_win = 0;
   if (r2_debug >= 2) sum_win += t_pre - t_win0;
-  int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W, c->threads, stream);
+  // worker CTAs + the service CTA (r2_kernels.cu service_main)
+  int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W + 1, c->threads, stream);
   if (r2_debug >= 2) {                       // host enqueue cost breakdown (diagnostics)
     static uint64_t n_calls = 0, sum_pre = 0, sum_launch = 0;
     const uint64_t t_post = r2_now_ns();
@@ -810,21 +866,30 @@ extern "C" r2_result_t r2_allreduce_host(r2_comm_t c, const void* send, void* re
   return R2_SUCCESS;
 }
 
+// Deterministic: once the stream is synchronised every kernel up to c->seq
+// has exited, and a rank whose kernel left without a complete result (watchdog,
+// abort, exhausted chain) wrote Ctrl.fail_seq / fail_code before exiting.  A
+// kernel that exits normally has every incoming completion word, so its
+// result is complete: SUCCESS is never returned for a wrong buffer.
 extern "C" r2_result_t r2_sync(r2_comm_t c) {
   if (!c) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
   if (cudaStreamSynchronize((cudaStream_t)c->last_stream) != cudaSuccess) return R2_ERR_CUDA;
-  // give the monitor a moment to record a NO_BACKUP / TIMEOUT for the last seq
-  for (int i = 0; i < 50; ++i) {
-    {
-      std::lock_guard<std::mutex> g(c->mu);
-      if (c->unreported_error != R2_SUCCESS) break;
-      bool busy = !c->replans.empty();
-      if (!busy) break;
+  int err = R2_SUCCESS;
+  if (c->n > 1)
+    for (int l = 0; l < c->nlocal; ++l) {
+      const uint32_t fs = c->ctrl_host[l]->fail_seq;
+      if (fs && fs > c->reported_seq && fs <= c->seq) err = (int)c->ctrl_host[l]->fail_code;
     }
-    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  std::lock_guard<std::mutex> g(c->mu);
+  if (err == R2_SUCCESS) err = c->unreported_error;
+  c->unreported_error = R2_SUCCESS;
+  c->reported_seq = c->seq;
+  if (err != R2_SUCCESS && c->last_error == R2_SUCCESS) {
+    c->last_error = err;
+    c->last_error_seq = c->seq;
   }
-  return (r2_result_t)take_async_error(c);
+  return (r2_result_t)err;
 }
 
 extern "C" r2_result_t r2_trace(r2_comm_t c, int rank_local, uint64_t out[64]) {
@@ -884,6 +949,7 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->last_protocol = c->last_protocol;
     out->n_readmits = c->n_readmits;
     out->n_reprobes = c->n_reprobes;
+    out->n_service_kernels = c->n_svc_kicks;
     const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {
@@ -924,27 +990,15 @@ extern "C" r2_result_t r2_finalize(r2_comm_t c) {
   track_live(c, false);
   c->stop.store(true);
   if (c->mon.joinable()) c->mon.join();
+  cudaDeviceSynchronize();                  // a standalone service kernel, if any
   for (auto& rg : c->regs)
     for (void* p : rg.opened) close_peer(c, p);
+  c->regs.clear();
   for (void* p : c->peer_arena_opened)
     if (p) cudaIpcCloseMemHandle(p);
+  c->peer_arena_opened.clear();
   if (c->has_oob) c->oob.barrier(c->oob.ctx);
-  for (char* a : c->arena) cudaFree(a);
-  for (Ctrl* h : c->ctrl_host) cudaFreeHost(h);
-  if (c->probe_res_host) cudaFreeHost((void*)c->probe_res_host);
-  if (c->probe_t0_host) cudaFreeHost((void*)c->probe_t0_host);
-  if (c->peers_dev) cudaFree(c->peers_dev);
-  if (c->regtab_dev) cudaFree(c->regtab_dev);
-  if (c->host_stage) cudaFree(c->host_stage);
-  for (auto& ev : c->host_ev) cudaEventDestroy(ev);
-  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
-  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
-  if (c->mon_stream) cudaStreamDestroy(c->mon_stream);
-  if (c->health_stream) cudaStreamDestroy(c->health_stream);
-  for (int i = 0; i < r2_comm::kProbeStreams; ++i)
-    if (c->probe_stream[i]) cudaStreamDestroy(c->probe_stream[i]);
-  if (c->health_pinned) cudaFreeHost(c->health_pinned);
-  if (c->flags_pinned) cudaFreeHost(c->flags_pinned);
+  release_resources(c);
   delete c;
   return R2_SUCCESS;
 }

@@ -20,6 +20,7 @@ enum MsgType : uint32_t {
   MSG_PROBE_RES = 3,     // prober -> round owner: outcome
   MSG_VERDICT = 4,       // round owner -> all: triangulated verdict
   MSG_ABORT = 5,         // any -> all: collective seq is unrecoverable
+  MSG_NOTIFY_ACK = 6,    // every rank -> detector: NOTIFY received ("notifies both sides")
 };
 
 struct Msg {
@@ -84,6 +85,17 @@ struct PendingProbe {
   uint32_t round_id, seq;
   volatile int* res_host;
   int res_index;
+};
+
+struct NotifyState {                         // one NOTIFY broadcast by this process
+  uint32_t seq;
+  int a, channel;                            // detecting sender, its channel
+  int expected, acks, resends;
+  uint64_t acked_by;                         // bit per acknowledging rank (duplicates after a resend)
+  uint64_t t_sent, t_last_send, t_acked;     // host CLOCK_MONOTONIC
+  bool peer_acked;                           // the other endpoint (a+1) confirmed: no half-open side
+  bool dirty;                                // event records to update
+  Msg msg;
 };
 
 struct EventTiming {                         // finalize failover_ms later
@@ -157,6 +169,7 @@ struct r2_comm {
   int last_error = R2_SUCCESS;
   uint64_t last_error_seq = 0;
   int unreported_error = R2_SUCCESS;
+  uint64_t reported_seq = 0;                 // errors of collectives <= this were returned by r2_sync
   std::map<uint32_t, LaunchInfo> launches;
 
   // monitor
@@ -167,7 +180,19 @@ struct r2_comm {
   cudaStream_t probe_stream[kProbeStreams] = {};
   int probe_stream_next = 0;
   uint32_t* health_pinned = nullptr;         // pinned staging of the health records
-  unsigned int* flags_pinned = nullptr;      // rollback: receiver's completion words
+  // service ring (r2_internal.h SvcBlock): posted by the monitor thread only
+  SvcBlock* svc_host = nullptr;
+  SvcBlock* svc_dev = nullptr;
+  uint32_t svc_posted = 0;                   // requests posted (= last tag)
+  uint64_t svc_tpost[R2_SVC_RING] = {};      // host time each slot's request was posted
+  cudaStream_t svc_stream = nullptr;         // standalone service kernel
+  cudaEvent_t svc_ev = nullptr;
+  bool svc_launched = false;
+  int n_svc_kicks = 0;
+  unsigned int* flags_map_host = nullptr;    // rollback: receiver's completion words (host-mapped)
+  unsigned int* flags_map_dev = nullptr;
+  uint32_t* health_map_host = nullptr;       // health records staged for a service COPY
+  uint32_t* health_map_dev = nullptr;
   std::mutex qmu;                            // local message queue (sim + self)
   std::deque<Msg> localq;
   std::vector<uint32_t> handled_err;         // [nlocal*K] last handled err seq
@@ -176,6 +201,7 @@ struct r2_comm {
   std::vector<Replan> replans;
   std::vector<PendingProbe> probes;
   std::vector<EventTiming> timings;
+  std::vector<NotifyState> notifies;         // outstanding / recent NOTIFYs (monitor)
   std::map<std::pair<uint32_t, int>, int> planned;  // (seq, l*K+c) already re-placed
   std::vector<uint32_t> epoch;               // [nlocal] last epoch written
   std::vector<uint32_t> plan_seq;            // [nlocal] seq the ctrl block serves
@@ -211,6 +237,14 @@ inline void rec_ss(const CtaRec& r, uint32_t* seq, uint32_t* state) {
 
 // r2_monitor.cpp
 void r2_monitor_main(r2_comm* comm);
+// service ring (monitor thread): post a request (tag returned), ask whether it
+// is done, launch the standalone service kernel when no resident service lane
+// will take it, wait for a request (kicking as needed; false on timeout)
+uint32_t r2_svc_post(r2_comm* comm, SvcReq& r);
+bool r2_svc_done(const r2_comm* comm, uint32_t tag);
+void r2_svc_kick(r2_comm* comm);
+bool r2_svc_wait(r2_comm* comm, uint32_t tag, uint64_t timeout_ns);
+int r2_push_health_svc(r2_comm* comm);                                 // monitor: via the service ring
 void r2_send_msg(r2_comm* comm, int dst, Msg m);
 uint64_t r2_now_ns();
 

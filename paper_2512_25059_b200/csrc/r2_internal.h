@@ -48,6 +48,10 @@ struct MiscDev {
   unsigned long long bytes[R2_MAXK];  // cumulative bytes pushed per carrier channel
   unsigned long long first_retx_ns;   // min over adopters (debug)
   unsigned long long trace[R2_TRACE_SLOTS];  // %globaltimer timeline when LaunchParams.trace (r2_trace)
+  // service lane (local rank 0's arena only): request claim state shared by the
+  // resident service CTA and the standalone service kernel, and the count of
+  // local ranks whose worker CTAs have all left the kernel
+  unsigned int svc_lock, svc_tail, grid_exited, pad_svc;
 };
 
 struct PlanEntry {           // dynamic re-placement of one origin channel
@@ -124,9 +128,44 @@ struct ErrRec {              // one per channel: the stop that needs handling
 struct Ctrl {                // host-mapped, one per local rank
   volatile unsigned int plan_seq, epoch, freeze, abort;
   volatile unsigned int stop_mask, nentries, done_seq, pad1;   // done_seq: last collective finished
+  // last collective this rank's kernel left WITHOUT a complete result (watchdog,
+  // abort, exhausted chain) and its r2_result_t: written by the exiting CTAs
+  // before the kernel ends, so r2_sync reads it deterministically after the
+  // stream synchronisation (never SUCCESS for an aborted collective)
+  volatile unsigned int fail_code, fail_seq;
   PlanEntry entries[R2_MAXK];
   ErrRec err[R2_MAXK];
   CtaRec cta[R2_MAX_CTAS_PER_RANK];
+};
+
+// ------------------------------------------------------------------ service
+// The monitor's device-side work (probe-flag stores and read-backs, installs of
+// the plan mirror DevCtrl, copies of health records / completion words) is a
+// ring of requests in host-mapped memory.  It is served by the SERVICE CTA of
+// the resident collective kernel (one extra CTA in the cooperative grid; its
+// warp 0 polls the ring), so failover needs no second kernel to run next to
+// the persistent one (profilers and sanitizers serialise kernels; other work
+// may hold the spare SMs).  With no collective resident, the monitor launches
+// the standalone service kernel, which serves the same ring.  Requests are
+// claimed under a device-memory lock (svc_lock/svc_tail in MiscDev), in order.
+enum { SVC_PROBE = 1, SVC_MIRROR = 2, SVC_COPY = 3, SVC_STORE = 4 };   // STORE: u32 nwords -> *dst
+#define R2_SVC_RING 64
+#define R2_SVC_MAXPROBES 8
+struct SvcReq {
+  unsigned int kind, mode, tag, nwords;   // MIRROR mode: 0 new collective (plan_seq last), 1 update (epoch last);
+                                          // STORE: nwords is the value
+  unsigned long long src, dst;            // COPY: nwords u32 src -> dst; MIRROR: dst = DevCtrl
+  unsigned long long mailbox, ep_dead, link_dead, result, t_start;   // PROBE (device addresses)
+  int prober, target, channel, n, K;
+  unsigned int token;
+  unsigned long long timeout_ns;
+  DevCtrl v;                              // MIRROR: the snapshot to install
+};
+struct SvcBlock {                         // host-mapped, one per process
+  volatile unsigned int head, pad;        // requests posted (host)
+  volatile unsigned long long alive;      // seq << 32 | 1 while a resident service lane polls, | 0 after
+  volatile unsigned int ack[R2_SVC_RING]; // = tag once request tag is done
+  SvcReq req[R2_SVC_RING];
 };
 
 // ------------------------------------------------------------------ launch
@@ -165,6 +204,7 @@ struct LaunchParams {
   const RankPtrs* peers;                 // [nlocal][n] device array
   const unsigned long long* regtab;      // [R2_MAX_REGS][n] peer registered bases
   Ctrl* ctrl[R2_MAXL];                   // device aliases of host-mapped blocks
+  SvcBlock* svc;                         // device alias of the host-mapped service ring
 };
 
 struct ProbeParams {
@@ -187,9 +227,8 @@ int r2_launch_probe(const ProbeParams& p, void* stream);
 int r2_kernel_smem_bytes();
 int r2_max_coop_ctas(int threads);
 int r2_warmup(const ProbeParams& p, void* stream);
-// mode 0: a new collective takes over the block (body, fence, plan_seq);
-// mode 1: update within the collective (body, fence, epoch)
-int r2_launch_ctrl_push(DevCtrl* dst, const DevCtrl& v, int mode, void* stream);
+// standalone service kernel: serves the ring until it is empty
+int r2_launch_service(SvcBlock* svc, MiscDev* misc0, void* stream);
 #ifdef __cplusplus
 }
 #endif

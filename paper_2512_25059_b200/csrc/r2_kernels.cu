@@ -212,6 +212,7 @@ struct Meta {                 // read by the control warp at retirement
 struct Shared {
   int decision;
   int cause;
+  unsigned int abort_code;    // r2_result_t of a monitor abort (DevCtrl.abort)
   int pipe_status;
   unsigned int seen_epoch;
   int dynamic;
@@ -438,8 +439,10 @@ __device__ int poll_control(const Cta& k, Shared& sh) {
   if (sh.alerted) {
     DevCtrl* C = k.me.dctrl;
     if (ld_relaxed_sys(&C->plan_seq) == k.seq) {
-      if (ld_relaxed_sys(&C->abort)) {
+      const unsigned int ab = ld_relaxed_sys(&C->abort);
+      if (ab) {
         sh.cause = STOP_ABORT;
+        sh.abort_code = ab;
         return ST_ABORT;
       }
       if (ld_relaxed_sys(&C->stop_mask) >> k.c & 1u) {
@@ -1253,8 +1256,9 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
 }
 
 // thread 0, once per CTA on the way out.  The last CTA of the rank resets
-// the per-collective counters (nobody reads them any more in this launch)
-// and publishes done_seq for the host's in-flight window.
+// the per-collective counters (nobody reads them any more in this launch) and
+// tells the service lane (which publishes done_seq once every local rank is
+// out, see service_main).
 __device__ void last_out(const Cta& k) {
   const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
   TRACE_MAX(k, 62);
@@ -1263,8 +1267,18 @@ __device__ void last_out(const Cta& k) {
     k.me.misc->copy_next = 0;
     __threadfence();
     atomicExch(&k.me.misc->exited, 0u);
-    k.ctrl->done_seq = k.seq;
+    __threadfence();
+    atomicAdd(&k.p->peers[k.p->first_rank].misc->grid_exited, 1u);   // local rank 0's arena
   }
+}
+
+// thread 0: this rank's kernel leaves without a complete result (watchdog,
+// abort, exhausted chain): record it for r2_sync before the kernel ends
+__device__ void post_failure(const Cta& k, unsigned int code) {
+  k.ctrl->fail_code = code;
+  __threadfence_system();
+  k.ctrl->fail_seq = k.seq;
+  __threadfence_system();
 }
 
 template <int DT>
@@ -1277,7 +1291,7 @@ __device__ void cta_main(Cta& k, Shared& sh) {
     if (k.tid == 0) {
       st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
       k.ctrl->cta[k.cta_in_rank].cause = STOP_NOBACKUP;
-      __threadfence_system();
+      post_failure(k, R2_ERR_NO_BACKUP);
       k.ctrl->cta[k.cta_in_rank].ss = R2_SS(k.seq, CTA_EXITED);
       last_out(k);
     }
@@ -1315,6 +1329,8 @@ __device__ void cta_main(Cta& k, Shared& sh) {
       // local abort: the rest of this rank stops waiting too
       st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
     }
+    if (st == ST_TIMEOUT || st == ST_ABORT)
+      post_failure(k, st == ST_ABORT && sh.abort_code ? sh.abort_code : (unsigned int)R2_ERR_TIMEOUT);
     if (st == ST_STOP && sh.cause == STOP_DEATH) {
       // bilateral awareness starts at the detecting sender; the
       // surviving CTAs of every rank must start reading the control block
@@ -1337,11 +1353,237 @@ __device__ void cta_main(Cta& k, Shared& sh) {
   }
 }
 
+// ------------------------------------------------------------ service lane
+// Warp 0 of the service CTA (the last CTA of the cooperative grid) or of the
+// standalone service kernel serves the monitor's request ring (r2_internal.h
+// SvcBlock): probe-flag stores + read-backs (reading C-11), installs of
+// the plan mirror (DevCtrl) and word copies (health records, completion words
+// for rollback).  Requests are claimed in order under svc_lock; probes run
+// concurrently (up to R2_SVC_MAXPROBES, lanes 0..7 watch one each).
+struct SvcProbe {
+  int active, dropped;
+  unsigned int tag, token, slot;
+  unsigned long long t0, timeout_ns, mailbox, result;
+};
+struct SvcShared {
+  SvcReq rq;
+  SvcProbe pr[R2_SVC_MAXPROBES];
+  int go, nactive;
+};
+
+__device__ __forceinline__ void svc_ack(SvcBlock* S, unsigned int slot, unsigned int tag) {
+  __threadfence_system();
+  S->ack[slot] = tag;
+}
+
+// lane 0: start one probe (completion is watched by svc_probes)
+__device__ void svc_probe_start(SvcBlock* S, SvcShared& ss, unsigned int slot) {
+  const SvcReq& r = ss.rq;
+  const unsigned int* ep = (const unsigned int*)r.ep_dead;
+  const unsigned int* lk = (const unsigned int*)r.link_dead;
+  const int K = r.K, c = r.channel;
+  if (r.t_start) *(volatile unsigned long long*)r.t_start = gtimer();
+  if (ld_relaxed_sys(ep + r.prober * K + c)) {         // the prober's own endpoint: immediate local error
+    *(volatile int*)r.result = R2_PROBE_LOCAL_ERROR;
+    svc_ack(S, slot, r.tag);
+    return;
+  }
+  const bool link = ((r.target == (r.prober + 1) % r.n) && ld_relaxed_sys(lk + r.prober * K + c)) ||
+                    ((r.prober == (r.target + 1) % r.n) && ld_relaxed_sys(lk + r.target * K + c));
+  const bool dropped = link || ld_relaxed_sys(ep + r.target * K + c);
+  if (!dropped) {
+    st_relaxed_sys((volatile unsigned int*)r.mailbox, r.token);
+    fence_sys();
+  }
+  for (int i = 0; i < R2_SVC_MAXPROBES; ++i)
+    if (!ss.pr[i].active) {
+      SvcProbe& q = ss.pr[i];
+      q.dropped = dropped;
+      q.tag = r.tag;
+      q.token = r.token;
+      q.slot = slot;
+      q.t0 = gtimer();
+      q.timeout_ns = r.timeout_ns;
+      q.mailbox = r.mailbox;
+      q.result = r.result;
+      q.active = 1;
+      ss.nactive++;
+      return;
+    }
+}
+
+// lanes 0..7: finish probes whose read-back arrived or whose timeout expired
+__device__ void svc_probes(SvcBlock* S, SvcShared& ss, unsigned int lane) {
+  if (lane < R2_SVC_MAXPROBES && ss.pr[lane].active) {
+    SvcProbe& q = ss.pr[lane];
+    int res = -1;
+    if (!q.dropped && ld_acquire_sys((const volatile unsigned int*)q.mailbox) == q.token) res = R2_PROBE_SUCCESS;
+    else if (gtimer() - q.t0 >= q.timeout_ns) res = R2_PROBE_TIMEOUT;
+    if (res >= 0) {
+      *(volatile int*)q.result = res;
+      svc_ack(S, q.slot, q.tag);
+      q.active = 0;
+      atomicSub(&ss.nactive, 1);
+    }
+  }
+  __syncwarp();
+}
+
+// whole warp: claim and execute the posted requests (returns with the lock
+// released).  A probe request waits for a free probe slot.
+__device__ void svc_take(SvcBlock* S, MiscDev* m0, SvcShared& ss, unsigned int lane) {
+  if (lane == 0) ss.go = atomicCAS(&m0->svc_lock, 0u, 1u) == 0u;
+  __syncwarp();
+  if (!ss.go) return;
+  for (;;) {
+    if (lane == 0) {
+      __threadfence();
+      const unsigned int tail = *(volatile unsigned int*)&m0->svc_tail;
+      const unsigned int head = S->head;
+      ss.go = (tail != head) && ss.nactive < R2_SVC_MAXPROBES;
+    }
+    __syncwarp();
+    if (!ss.go) break;
+    const unsigned int tail = *(volatile unsigned int*)&m0->svc_tail;
+    const unsigned int slot = tail % R2_SVC_RING;
+    // the request (host-mapped): every lane loads 8-byte words, one PCIe round trip
+    {
+      const volatile unsigned long long* src = (const volatile unsigned long long*)&S->req[slot];
+      unsigned long long* dst = (unsigned long long*)&ss.rq;
+      for (unsigned int i = lane; i < sizeof(SvcReq) / 8; i += 32) dst[i] = src[i];
+    }
+    __syncwarp();
+    const SvcReq& r = ss.rq;
+    if (r.kind == SVC_MIRROR) {
+      // body, fence, then the word that publishes it (plan_seq for a new
+      // collective, epoch for an update): same order as the CTAs read it
+      volatile unsigned int* d = (volatile unsigned int*)r.dst;
+      const unsigned int* v = (const unsigned int*)&r.v;
+      for (unsigned int i = 2 + lane; i < sizeof(DevCtrl) / 4; i += 32) d[i] = v[i];
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        d[1] = r.v.epoch;
+        if (r.mode == 0) {
+          __threadfence();
+          d[0] = r.v.plan_seq;
+        }
+        __threadfence();
+        svc_ack(S, slot, r.tag);
+      }
+    } else if (r.kind == SVC_COPY) {
+      const volatile unsigned int* a = (const volatile unsigned int*)r.src;
+      volatile unsigned int* b = (volatile unsigned int*)r.dst;
+      for (unsigned int i = lane; i < r.nwords; i += 32) b[i] = ld_relaxed_sys(a + i);
+      __threadfence_system();
+      __syncwarp();
+      if (lane == 0) svc_ack(S, slot, r.tag);
+    } else if (r.kind == SVC_STORE) {
+      if (lane == 0) {
+        st_relaxed_sys((volatile unsigned int*)r.dst, r.nwords);
+        svc_ack(S, slot, r.tag);
+      }
+    } else if (r.kind == SVC_PROBE) {
+      if (lane == 0) svc_probe_start(S, ss, slot);
+    } else if (lane == 0) {
+      svc_ack(S, slot, r.tag);                        // unknown kind: consumed
+    }
+    __syncwarp();
+    if (lane == 0) {
+      *(volatile unsigned int*)&m0->svc_tail = tail + 1;
+      __threadfence();
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(&m0->svc_lock, 0u);
+  }
+  __syncwarp();
+}
+
+// Resident flavour (the service CTA of a collective): serve until every local
+// rank's worker CTAs have left, then publish done_seq for all of them.
+__device__ void service_main(const LaunchParams& p) {
+  __shared__ SvcShared ss;
+  const unsigned int lane = threadIdx.x & 31u;
+  SvcBlock* S = p.svc;
+  MiscDev* m0 = p.peers[p.first_rank].misc;
+  if (lane == 0) {
+    ss.nactive = 0;
+    for (int i = 0; i < R2_SVC_MAXPROBES; ++i) ss.pr[i].active = 0;
+    S->alive = R2_SS(p.seq, 1);
+  }
+  __syncwarp();
+  unsigned long long t_head = 0;
+  unsigned int head_seen = 0, tail_seen = 0;
+  for (;;) {
+    // the host's head word costs a PCIe round trip: read it every ~2 us
+    int take = 0;
+    if (lane == 0) {
+      const unsigned long long now = gtimer();
+      if (now - t_head >= 2000ull) {
+        t_head = now;
+        head_seen = S->head;
+        tail_seen = *(volatile unsigned int*)&m0->svc_tail;
+      }
+      take = head_seen != tail_seen;
+    }
+    take = __shfl_sync(0xFFFFFFFFu, take, 0);
+    if (take) {
+      svc_take(S, m0, ss, lane);
+      if (lane == 0) t_head = 0;                      // look again right away
+    }
+    if (ss.nactive) svc_probes(S, ss, lane);
+    int out = 0;
+    if (lane == 0)
+      out = ss.nactive == 0 && ld_relaxed_sys((const volatile unsigned int*)&m0->grid_exited) == (unsigned)p.nlocal;
+    out = __shfl_sync(0xFFFFFFFFu, out, 0);
+    if (out) break;
+    __nanosleep(100);
+  }
+  if (lane == 0) {
+    m0->grid_exited = 0;                              // nobody else touches it in this launch
+    __threadfence();
+    S->alive = R2_SS(p.seq, 0);
+    for (int l = 0; l < p.nlocal; ++l) p.ctrl[l]->done_seq = p.seq;
+    __threadfence_system();
+  }
+}
+
+// Standalone flavour: no collective resident; serve until the ring is empty
+// and no probe is outstanding.
+__global__ void r2_service_kernel(SvcBlock* S, MiscDev* m0) {
+  __shared__ SvcShared ss;
+  const unsigned int lane = threadIdx.x & 31u;
+  if (threadIdx.x >= 32) return;
+  if (lane == 0) {
+    ss.nactive = 0;
+    for (int i = 0; i < R2_SVC_MAXPROBES; ++i) ss.pr[i].active = 0;
+  }
+  __syncwarp();
+  for (;;) {
+    svc_take(S, m0, ss, lane);
+    if (ss.nactive) svc_probes(S, ss, lane);
+    int out = 0;
+    if (lane == 0) {
+      __threadfence();
+      out = ss.nactive == 0 && S->head == *(volatile unsigned int*)&m0->svc_tail;
+    }
+    out = __shfl_sync(0xFFFFFFFFu, out, 0);
+    if (out) break;
+  }
+}
+
 __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_constant__ LaunchParams p) {
+  const int per_rank = p.K * p.W;
+  if (blockIdx.x == (unsigned)(p.nlocal * per_rank)) {   // the service CTA (last in the grid)
+    if (threadIdx.x < 32) service_main(p);
+    return;
+  }
   __shared__ Shared sh;
   Cta k;
   k.p = &p;
-  const int per_rank = p.K * p.W;
   k.l = blockIdx.x / per_rank;
   k.cta_in_rank = blockIdx.x % per_rank;
   k.c = k.cta_in_rank / p.W;
@@ -1390,6 +1632,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   if (k.tid == 0) {
     sh.decision = 0;
     sh.cause = 0;
+    sh.abort_code = 0;
     sh.pipe_status = 0;
     sh.pub = 0;
     sh.fin = 0;
@@ -1483,25 +1726,8 @@ int r2_kernel_smem_bytes() { return (int)sizeof(Shared); }
 // allreduce kernel -- which itself waits for the probe verdict (deadlock
 // until the watchdog).  A warm-up launch of the probe kernel (self-probe of a
 // healthy mailbox) and an attribute query of the allreduce kernel load them.
-// one thread: install a plan/stop/abort update into the device mirror
-__global__ void r2_ctrl_push_kernel(DevCtrl* dst, const __grid_constant__ DevCtrl v, int mode) {
-  volatile unsigned int* d = (volatile unsigned int*)dst;
-  const unsigned int* s = (const unsigned int*)&v;
-  const int words = (int)(sizeof(DevCtrl) / 4);
-  for (int i = 2; i < words; ++i) d[i] = s[i];          // body: freeze .. entries
-  __threadfence();
-  if (mode == 0) {
-    d[1] = v.epoch;
-    __threadfence();
-    d[0] = v.plan_seq;
-  } else {
-    d[1] = v.epoch;
-  }
-  __threadfence();
-}
-
-int r2_launch_ctrl_push(DevCtrl* dst, const DevCtrl& v, int mode, void* stream) {
-  r2_ctrl_push_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dst, v, mode);
+int r2_launch_service(SvcBlock* svc, MiscDev* misc0, void* stream) {
+  r2_service_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(svc, misc0);
   return (int)cudaGetLastError();
 }
 
@@ -1511,7 +1737,7 @@ int r2_warmup(const ProbeParams& p, void* stream) {
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncGetAttributes(&a, r2_probe_kernel);
   if (e != cudaSuccess) return (int)e;
-  e = cudaFuncGetAttributes(&a, r2_ctrl_push_kernel);
+  e = cudaFuncGetAttributes(&a, r2_service_kernel);
   if (e != cudaSuccess) return (int)e;
   r2_probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   e = cudaGetLastError();
@@ -1519,8 +1745,9 @@ int r2_warmup(const ProbeParams& p, void* stream) {
   return (int)cudaStreamSynchronize((cudaStream_t)stream);
 }
 
-// The cooperative grid leaves two SMs free: the probe-flag kernels and the
-// control-block pushes of the monitor must run while a collective is stuck.
+// Worker CTAs available to one cooperative launch: the service CTA takes one
+// more SM; one stays free for the standalone service kernel (no failover step
+// depends on it while a collective is resident).
 int r2_max_coop_ctas(int threads) {
   int dev = 0, nsm = 0, per = 0;
   cudaGetDevice(&dev);

@@ -67,27 +67,30 @@ void start_probe(r2_comm* c, int prober, int target, int channel, int slot, int 
   c->probe_res_host[idx] = -1;
   const RankPtrs& tgt = c->peers_host[l * c->n + target];
   const RankPtrs& me = c->peers_host[l * c->n + prober];
-  ProbeParams pp;
-  pp.target_mailbox = tgt.mailbox + prober * c->K + channel;
-  pp.ep_dead = me.ep_dead;
-  pp.link_dead = me.link_dead;
-  pp.prober = prober;
-  pp.target = target;
-  pp.channel = channel;
-  pp.n = c->n;
-  pp.K = c->K;
-  pp.token = ++c->probe_token;
-  if (pp.token == 0) pp.token = ++c->probe_token;
-  pp.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
-  pp.result = c->probe_res_dev + idx;
-  pp.t_start = c->probe_t0_dev + idx;
+  // a probe-flag store + read-back, run by the service lane of whatever kernel
+  // is resident (or the standalone service kernel): no second kernel has to
+  // run next to a stuck collective
+  SvcReq rq;
+  memset(&rq, 0, sizeof(rq));
+  rq.kind = SVC_PROBE;
+  rq.mailbox = (unsigned long long)(tgt.mailbox + prober * c->K + channel);
+  rq.ep_dead = (unsigned long long)me.ep_dead;
+  rq.link_dead = (unsigned long long)me.link_dead;
+  rq.prober = prober;
+  rq.target = target;
+  rq.channel = channel;
+  rq.n = c->n;
+  rq.K = c->K;
+  rq.token = ++c->probe_token;
+  if (rq.token == 0) rq.token = ++c->probe_token;
+  rq.timeout_ns = (unsigned long long)c->cfg.probe_timeout_us * 1000ull;
+  rq.result = (unsigned long long)(c->probe_res_dev + idx);
+  rq.t_start = (unsigned long long)(c->probe_t0_dev + idx);
   c->probe_t0_host[idx] = 0;
-  cudaStream_t ps = c->probe_stream[c->probe_stream_next];
-  c->probe_stream_next = (c->probe_stream_next + 1) % r2_comm::kProbeStreams;
-  int rc = r2_launch_probe(pp, ps);
-  R2LOG("probe launch %d->%d ch%d slot%d round %08x rc=%d", prober, target, channel, slot, round_id, rc);
+  const uint32_t tag = r2_svc_post(c, rq);
+  R2LOG("probe posted %d->%d ch%d slot%d round %08x tag %u", prober, target, channel, slot, round_id, tag);
   PendingProbe pr{prober, target, channel, slot, l, owner, round_id, seq, c->probe_res_host + idx, idx};
-  if (rc != 0) c->probe_res_host[idx] = R2_PROBE_NOT_RUN;
+  if (!tag) c->probe_res_host[idx] = R2_PROBE_NOT_RUN;
   c->probes.push_back(pr);
 }
 
@@ -204,8 +207,9 @@ bool progress_probes(r2_comm* c) {
 // poll the device mirror (DevCtrl, r2_internal.h) that this installs.
 void push_ctrl(r2_comm* c, int l, int mode) {
   const Ctrl* C = c->ctrl_host[l];
-  DevCtrl v;
-  memset(&v, 0, sizeof(v));
+  SvcReq rq;
+  memset(&rq, 0, sizeof(rq));
+  DevCtrl& v = rq.v;
   v.plan_seq = C->plan_seq;
   v.epoch = C->epoch;
   v.freeze = C->freeze;
@@ -214,8 +218,10 @@ void push_ctrl(r2_comm* c, int l, int mode) {
   v.nentries = C->nentries;
   memcpy(v.entries, (const void*)C->entries, sizeof(v.entries));
   const int r = c->first_rank + l;
-  int rc = r2_launch_ctrl_push(c->peers_host[l * c->n + r].dctrl, v, mode, c->mon_stream);
-  if (rc != 0) R2LOG("ctrl push failed rank %d: %d", r, rc);
+  rq.kind = SVC_MIRROR;
+  rq.mode = (unsigned)mode;
+  rq.dst = (unsigned long long)c->peers_host[l * c->n + r].dctrl;
+  if (!r2_svc_post(c, rq)) R2LOG("ctrl push failed rank %d", r);
 }
 
 void ctrl_init_for(r2_comm* c, int l, uint32_t seq) {
@@ -235,10 +241,10 @@ void ctrl_init_for(r2_comm* c, int l, uint32_t seq) {
   c->cur_plan[l].clear();
 }
 
-void set_abort(r2_comm* c, int l, uint32_t seq) {
+void set_abort(r2_comm* c, int l, uint32_t seq, int err) {
   ctrl_init_for(c, l, seq);
   Ctrl* C = c->ctrl_host[l];
-  C->abort = 1;
+  C->abort = (unsigned)(err ? err : R2_ERR_INTERNAL);   // the kernel reports it (Ctrl.fail_code)
   std::atomic_thread_fence(std::memory_order_seq_cst);
   push_ctrl(c, l, 1);
 }
@@ -247,7 +253,8 @@ void record_error(r2_comm* c, int err, uint32_t seq) {
   std::lock_guard<std::mutex> g(c->mu);
   c->last_error = err;
   c->last_error_seq = seq;
-  c->unreported_error = err;
+  // a collective r2_sync already covered reported its own kernel's outcome
+  if (seq > c->reported_seq) c->unreported_error = err;
 }
 
 // ------------------------------------------------------------------ verdicts
@@ -281,7 +288,7 @@ void on_verdict(r2_comm* c, const Msg& m) {
   const uint32_t from = (m.seq ? m.seq : (uint32_t)c->seq) + 1;
   for (int e : kill_ep) r2_declare_dead(c, 0, e, m.channel, from);
   if (kill_link && m.b == (m.a + 1) % n) r2_declare_dead(c, 1, m.a, m.channel, from);
-  r2_push_health(c);
+  r2_push_health_svc(c);
   R2LOG("verdict seq %u applied: health records pushed", m.seq);
   if (m.seq == 0) return;
   const LaunchInfo* li = launch_of(c, m.seq);
@@ -316,10 +323,42 @@ void on_verdict(r2_comm* c, const Msg& m) {
 // ------------------------------------------------------------------ messages
 bool handle_msg(r2_comm* c, const Msg& m) {
   switch (m.type) {
-    case MSG_NOTIFY:
-      // bilateral awareness: the peer learns the connection failed;
-      // its kernel keeps waiting on the canonical flags, which the
-      // sender's re-placement will deliver.
+    case MSG_NOTIFY: {
+      // bilateral awareness ("notifies both sides to avoid
+      // half-open states"): every rank -- the receiving endpoint a+1 above
+      // all -- learns that connection (a -> a+1, channel) failed in seq and
+      // acknowledges.  Its kernel keeps waiting on the canonical completion
+      // words, which the sender's re-placement delivers; its CTAs start
+      // reading the plan mirror (alert word) in case its own endpoint is
+      // condemned by the verdict.
+      for (int l = 0; l < c->nlocal; ++l) {
+        const RankPtrs& me = c->peers_host[l * c->n + c->first_rank + l];
+        SvcReq rq;
+        memset(&rq, 0, sizeof(rq));
+        rq.kind = SVC_STORE;
+        rq.dst = (unsigned long long)me.alert;
+        rq.nwords = m.seq;                           // the value stored
+        if (m.seq) r2_svc_post(c, rq);
+      }
+      Msg ack{};
+      ack.type = MSG_NOTIFY_ACK;
+      ack.seq = m.seq;
+      ack.a = m.a;
+      ack.b = m.b;
+      ack.channel = m.channel;
+      ack.prober = c->rank;                        // acknowledging process (sim: rank 0 for all)
+      r2_send_msg(c, m.src, ack);
+      break;
+    }
+    case MSG_NOTIFY_ACK:
+      for (NotifyState& ns : c->notifies)
+        if (ns.seq == m.seq && ns.a == m.a && ns.channel == m.channel && !(ns.acked_by >> (m.prober & 63) & 1ull)) {
+          ns.acked_by |= 1ull << (m.prober & 63);
+          ns.acks++;
+          ns.dirty = true;
+          if (c->sim || m.prober == (m.a + 1) % c->n) ns.peer_acked = true;
+          if (ns.acks >= ns.expected) ns.t_acked = r2_now_ns();
+        }
       break;
     case MSG_PROBE_REQ:
       if (is_local(c, m.prober)) start_probe(c, m.prober, m.target, m.channel, m.slot, m.round_owner, m.round_id, m.seq);
@@ -331,7 +370,7 @@ bool handle_msg(r2_comm* c, const Msg& m) {
       on_verdict(c, m);
       break;
     case MSG_ABORT:
-      for (int l = 0; l < c->nlocal; ++l) set_abort(c, l, m.seq);
+      for (int l = 0; l < c->nlocal; ++l) set_abort(c, l, m.seq, m.error ? m.error : R2_ERR_NO_BACKUP);
       record_error(c, m.error ? m.error : R2_ERR_NO_BACKUP, m.seq);
       break;
   }
@@ -393,6 +432,17 @@ bool scan_device_records(r2_comm* c) {
       nm.b = (r + 1) % c->n;
       nm.channel = k;
       nm.t_fire = e.t_fire;
+      {
+        NotifyState ns{};
+        ns.seq = s;
+        ns.a = r;
+        ns.channel = k;
+        ns.expected = c->sim ? 1 : c->n;            // one monitor serves all simulated ranks
+        ns.t_sent = ns.t_last_send = r2_now_ns();
+        ns.msg = nm;
+        c->notifies.push_back(ns);
+        while (c->notifies.size() > 64) c->notifies.erase(c->notifies.begin());
+      }
       broadcast(c, nm);
       uint32_t id;
       {
@@ -513,7 +563,7 @@ void publish_plan(r2_comm* c, Replan& rp) {
   // ledger follows without touching device memory.  Otherwise (an adopter
   // failed / static adoption): read the receiver's completion words.
   const bool from_keys = !rp.froze && dead == (1u << rp.channel);
-  const unsigned int* flags = c->flags_pinned;
+  const unsigned int* flags = c->flags_map_host;
   std::vector<unsigned long long> lane_key(c->W, ~0ull);   // a drained lane completed all its own chunks
   if (from_keys)
     for (int w = 0; w < c->W; ++w) {
@@ -523,16 +573,27 @@ void publish_plan(r2_comm* c, Replan& rp) {
       if (st == CTA_STOPPED) lane_key[w] = rec.stop_key;   // fenced before the state (post_state)
     }
   if (!from_keys) {
+    // the service lane copies the receiver's completion words into host-mapped
+    // memory (no copy-engine work that a profiler could serialise behind the
+    // stuck collective)
     const RankPtrs& nx = c->peers_host[l * c->n + r1];
-    cudaMemcpyAsync(c->flags_pinned, nx.flags, (size_t)steps * K * m * 4, cudaMemcpyDeviceToHost, c->mon_stream);
+    SvcReq rq;
+    memset(&rq, 0, sizeof(rq));
+    rq.kind = SVC_COPY;
+    rq.src = (unsigned long long)nx.flags;
+    rq.dst = (unsigned long long)c->flags_map_dev;
+    rq.nwords = (unsigned)((size_t)steps * K * m);
+    uint32_t tag = r2_svc_post(c, rq);
     if (li.local_step >= 0) {
       // LOCAL items keep their completion words in this rank's own memory
       // (reading R-5); the receiver has no words at that step
       const size_t o = (size_t)li.local_step * K * m;
-      cudaMemcpyAsync(c->flags_pinned + o, c->peers_host[l * c->n + r].flags + o, (size_t)K * m * 4,
-                      cudaMemcpyDeviceToHost, c->mon_stream);
+      rq.src = (unsigned long long)(c->peers_host[l * c->n + r].flags + o);
+      rq.dst = (unsigned long long)(c->flags_map_dev + o);
+      rq.nwords = (unsigned)((size_t)K * m);
+      tag = r2_svc_post(c, rq);
     }
-    r2_spin_sync(c->mon_stream);
+    if (!tag || !r2_svc_wait(c, tag, 2000000000ull)) R2LOG("replan seq %u rank %d: flag copy failed", rp.seq, r);
     R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
   }
   const int t_act = li.op == R2_OP_BROADCAST ? ((r - li.root) % c->n + c->n) % c->n : -1;
@@ -588,6 +649,7 @@ void publish_plan(r2_comm* c, Replan& rp) {
     ev.assignee = -1;
     ev.chain_pos = -1;
     ev.failover_ms = -1.0;
+    ev.notify_ack_ms = -1.0;
     ev.t_detect_host_ns = rp.t_detect;
     ev.t_verdict_host_ns = rp.t_verdict;
     ev.t_plan_host_ns = now;
@@ -619,7 +681,7 @@ void publish_plan(r2_comm* c, Replan& rp) {
     ents.push_back(pe);
   }
   if (nobackup || healthy == 0) {
-    set_abort(c, l, rp.seq);
+    set_abort(c, l, rp.seq, R2_ERR_NO_BACKUP);
     record_error(c, R2_ERR_NO_BACKUP, rp.seq);
     Msg m2{};
     m2.type = MSG_ABORT;
@@ -658,6 +720,15 @@ bool progress_replans(r2_comm* c) {
     Replan& rp = c->replans[i];
     const int l = rp.l;
     Ctrl* C = c->ctrl_host[l];
+    if ((int32_t)(C->done_seq - rp.seq) >= 0) {
+      // the collective already left the device (completed, or aborted by the
+      // watchdog): nothing is left to re-place
+      R2LOG("replan seq %u rank %d ch%d dropped: kernel done", rp.seq, c->first_rank + l, rp.channel);
+      std::lock_guard<std::mutex> g(c->mu);
+      c->replans.erase(c->replans.begin() + i);
+      busy = true;
+      continue;
+    }
     bool fault_channel = false;
     {
       std::lock_guard<std::mutex> g(c->mu);
@@ -714,6 +785,7 @@ bool progress_replans(r2_comm* c) {
     R2LOG("plan published seq %u rank %d ch%d epoch %u (device clock %lld)", rp.seq, c->first_rank + l, rp.channel,
           c->epoch[l], (long long)r2_now_ns() + c->clk_offset);
     busy = true;
+    std::lock_guard<std::mutex> g(c->mu);     // replans: monitor-owned; the lock documents it
     c->replans.erase(c->replans.begin() + i);
   }
   return busy;
@@ -855,6 +927,37 @@ bool progress_reprobes(r2_comm* c) {
   return busy;
 }
 
+// Acknowledged bilateral notification: a NOTIFY without every rank's
+// acknowledgement after 5 ms is sent again (up to 3 times); acknowledgement
+// counts and the notify -> last-ack latency go into the detector's failover
+// records.
+bool progress_notifies(r2_comm* c) {
+  bool busy = false;
+  const uint64_t now = r2_now_ns();
+  for (NotifyState& ns : c->notifies) {
+    if (!ns.t_acked && ns.resends < 3 && now - ns.t_last_send > 5000000ull) {
+      ns.resends++;
+      ns.t_last_send = now;
+      R2LOG("NOTIFY seq %u %d ch%d: %d of %d acks after %.1f ms, resending", ns.seq, ns.a, ns.channel, ns.acks,
+            ns.expected, (now - ns.t_sent) / 1e6);
+      broadcast(c, ns.msg);
+      busy = true;
+    }
+    if (!ns.dirty) continue;
+    std::lock_guard<std::mutex> g(c->mu);
+    bool found = false;
+    for (r2_event_t& ev : c->events)
+      if (ev.seq == ns.seq && ev.rank == ns.a && ev.stopped_channel == ns.channel) {
+        ev.notify_acks = ns.acks;
+        ev.notify_peer_acked = ns.peer_acked;
+        ev.notify_ack_ms = ns.t_acked ? (double)(ns.t_acked - ns.t_sent) / 1e6 : -1.0;
+        found = true;
+      }
+    if ((found && ns.t_acked) || now - ns.t_sent > 1000000000ull) ns.dirty = false;   // final (or no record)
+  }
+  return busy;
+}
+
 bool take_probe_requests(r2_comm* c) {
   std::pair<int, std::pair<int, int>> req;
   uint32_t id;
@@ -879,7 +982,96 @@ void r2_send_msg(r2_comm* c, int dst, Msg m) {
     deliver_local(c, m);
     return;
   }
-  c->oob.post(c->oob.ctx, dst, &m, sizeof(m));
+  // a full ring times the post out: keep serving our own inbox meanwhile
+  // (the peer may be waiting for us to drain ours) and retry; a message that
+  // still cannot be posted is a bootstrap error for this collective
+  for (int attempt = 0; attempt < 20; ++attempt) {
+    if (c->oob.post(c->oob.ctx, dst, &m, sizeof(m)) == 0) return;
+    R2LOG("oob post to %d failed (attempt %d), retrying", dst, attempt);
+  }
+  record_error(c, R2_ERR_BOOTSTRAP, m.seq);
+}
+
+// ------------------------------------------------------------------ service ring
+uint32_t r2_svc_post(r2_comm* c, SvcReq& r) {
+  const uint32_t tag = c->svc_posted + 1;
+  const uint32_t slot = (tag - 1) % R2_SVC_RING;
+  // the slot's previous request (tag - RING) must be done before it is reused
+  if (tag > R2_SVC_RING && !r2_svc_wait(c, tag - R2_SVC_RING, 2000000000ull)) return 0;
+  r.tag = tag;
+  SvcBlock* S = c->svc_host;
+  S->ack[slot] = 0;
+  memcpy((void*)&S->req[slot], &r, sizeof(SvcReq));
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  S->head = tag;                            // publishes the request (x86: in order)
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  c->svc_posted = tag;
+  c->svc_tpost[slot] = r2_now_ns();
+  return tag;
+}
+
+bool r2_svc_done(const r2_comm* c, uint32_t tag) {
+  return c->svc_host->ack[(tag - 1) % R2_SVC_RING] == tag;
+}
+
+// A resident collective's service lane serves the ring while its kernel runs
+// (alive word odd).  Otherwise -- no collective resident, or a request left
+// unserved for 300 us -- the standalone service kernel is launched (one at a
+// time; it exits once the ring is empty).
+void r2_svc_kick(r2_comm* c) {
+  const uint32_t posted = c->svc_posted;
+  if (!posted) return;
+  uint32_t oldest = 0;
+  const uint32_t lo = posted > R2_SVC_RING ? posted - R2_SVC_RING + 1 : 1;
+  for (uint32_t t = lo; t <= posted; ++t)
+    if (!r2_svc_done(c, t)) {
+      oldest = t;
+      break;
+    }
+  if (!oldest) return;
+  if (c->svc_launched) {
+    if (cudaEventQuery(c->svc_ev) == cudaErrorNotReady) return;
+    c->svc_launched = false;
+  }
+  const bool resident = (c->svc_host->alive & 1ull) != 0;
+  const uint64_t age = r2_now_ns() - c->svc_tpost[(oldest - 1) % R2_SVC_RING];
+  if (resident && age < 300000ull) return;
+  const RankPtrs& me0 = c->peers_host[c->first_rank];   // local rank 0's own arena
+  if (r2_launch_service(c->svc_dev, me0.misc, c->svc_stream) != 0) return;
+  cudaEventRecord(c->svc_ev, c->svc_stream);
+  c->svc_launched = true;
+  c->n_svc_kicks++;
+  R2LOG("service kernel launched (oldest request %u, age %.1f us, resident %d)", oldest, age / 1e3, (int)resident);
+}
+
+bool r2_svc_wait(r2_comm* c, uint32_t tag, uint64_t timeout_ns) {
+  const uint64_t t0 = r2_now_ns();
+  while (!r2_svc_done(c, tag)) {
+    r2_svc_kick(c);
+    if (r2_now_ns() - t0 > timeout_ns) return false;
+  }
+  return true;
+}
+
+// Health records into every local arena through the service ring (the
+// monitor's path; enqueue uses r2_push_health on the caller's thread).  The
+// caller holds c->mu; the staging buffer is stable until the copy is done.
+int r2_push_health_svc(r2_comm* c) {
+  const size_t words = c->health.size();
+  memcpy(c->health_map_host, c->health.data(), words * sizeof(uint32_t));
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  uint32_t tag = 0;
+  for (int l = 0; l < c->nlocal; ++l) {
+    SvcReq rq;
+    memset(&rq, 0, sizeof(rq));
+    rq.kind = SVC_COPY;
+    rq.src = (unsigned long long)c->health_map_dev;
+    rq.dst = (unsigned long long)c->peers_host[l * c->n + c->first_rank + l].health;
+    rq.nwords = (unsigned)words;
+    tag = r2_svc_post(c, rq);
+    if (!tag) return -1;
+  }
+  return r2_svc_wait(c, tag, 2000000000ull) ? 0 : -1;
 }
 
 void r2_monitor_main(r2_comm* c) {
@@ -896,6 +1088,8 @@ void r2_monitor_main(r2_comm* c) {
     busy |= progress_timings(c);
     busy |= take_probe_requests(c);
     busy |= progress_reprobes(c);
+    busy |= progress_notifies(c);
+    r2_svc_kick(c);
     if (!busy) std::this_thread::sleep_for(std::chrono::microseconds(10));
   }
 }

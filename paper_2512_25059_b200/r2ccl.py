@@ -76,7 +76,8 @@ class Event(C.Structure):
                 ("shares", C.c_int * MAX_CHANNELS), ("error", C.c_int),
                 ("t_fire_dev_ns", C.c_uint64), ("t_first_retx_dev_ns", C.c_uint64),
                 ("t_detect_host_ns", C.c_uint64), ("t_verdict_host_ns", C.c_uint64), ("t_plan_host_ns", C.c_uint64),
-                ("failover_ms", C.c_double)]
+                ("failover_ms", C.c_double), ("notify_acks", C.c_int), ("notify_peer_acked", C.c_int),
+                ("notify_ack_ms", C.c_double)]
 
     def as_dict(self, K: int) -> dict:
         d = {"seq": self.seq, "rank": self.rank, "origin": self.origin_channel,
@@ -85,7 +86,8 @@ class Event(C.Structure):
              "error": self.error, "failover_ms": self.failover_ms,
              "t_fire_dev_ns": self.t_fire_dev_ns, "t_first_retx_dev_ns": self.t_first_retx_dev_ns,
              "t_detect_host_ns": self.t_detect_host_ns, "t_verdict_host_ns": self.t_verdict_host_ns,
-             "t_plan_host_ns": self.t_plan_host_ns}
+             "t_plan_host_ns": self.t_plan_host_ns, "notify_acks": self.notify_acks,
+             "notify_peer_acked": bool(self.notify_peer_acked), "notify_ack_ms": self.notify_ack_ms}
         d.update(self.verdict.as_dict())
         if self.strategy == 0:
             d["assignee"], d["chain_pos"] = self.assignee, self.chain_pos
@@ -99,7 +101,7 @@ class Status(C.Structure):
                 ("n_events", C.c_int), ("world", C.c_int), ("nlocal", C.c_int), ("nchannels", C.c_int),
                 ("dead_endpoints", C.c_uint32 * (MAX_LOCAL * 4)), ("dead_links", C.c_uint32 * (MAX_LOCAL * 4)),
                 ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int),
-                ("n_readmits", C.c_int), ("n_reprobes", C.c_int)]
+                ("n_readmits", C.c_int), ("n_reprobes", C.c_int), ("n_service_kernels", C.c_int)]
 
 
 class Geometry(C.Structure):
@@ -345,7 +347,8 @@ class Comm:
                 "dead_links": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_links[r] >> c) & 1),
                 "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)],
                 "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE"),
-                "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes}
+                "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes,
+                "n_service_kernels": s.n_service_kernels}
 
     def events(self) -> list:
         st = Status()

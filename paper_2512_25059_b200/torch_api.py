@@ -52,7 +52,11 @@ def register(comm: R.Comm, t: torch.Tensor) -> int:
 
 def _count(comm: R.Comm, t: torch.Tensor, count: int | None) -> int:
     if not comm.sim:
-        return t.numel() if count is None else count
+        if count is None:
+            return t.numel()
+        if not 0 <= count <= t.numel():
+            raise ValueError(f"count {count} outside the tensor's {t.numel()} elements")
+        return count
     # sim mode: [k, row] with 16-byte aligned rows; count <= row elements
     if t.dim() != 2 or t.shape[0] != comm.n:
         raise ValueError(f"sim mode expects a [{comm.n}, row] tensor")
@@ -154,6 +158,8 @@ def broadcast(comm: R.Comm, send: torch.Tensor | None, recv: torch.Tensor, root:
         _rows_ok(comm, recv, count)
     else:
         count = recv.numel() if count is None else count
+        if not 0 <= count <= recv.numel() or (send is not recv and count > send.numel()):
+            raise ValueError(f"count {count} exceeds the send / recv tensors")
     s = stream if stream is not None else torch.cuda.current_stream()
     comm.broadcast(send.data_ptr(), recv.data_ptr(), count, r2_dtype(recv), root, s.cuda_stream)
     return recv

@@ -8,7 +8,8 @@ import torch
 import r2inputs
 from oracle import protocol as OP
 from oracle import semantic as OS
-from oracle.geometry import Geometry, effective_chunk_bytes
+from oracle.geometry import Geometry
+from tests.scenario import effective_chunk_bytes
 from paper_2512_25059_b200 import r2ccl as R
 from paper_2512_25059_b200 import torch_api as T
 

@@ -16,7 +16,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import r2inputs  # noqa: E402
 from oracle import protocol as OP  # noqa: E402
 from oracle import semantic as OS  # noqa: E402
-from oracle.geometry import Geometry, effective_chunk_bytes  # noqa: E402
+from oracle.geometry import Geometry  # noqa: E402
+from tests.scenario import effective_chunk_bytes  # noqa: E402
 from paper_2512_25059_b200 import r2ccl as R  # noqa: E402
 from paper_2512_25059_b200 import torch_api as T  # noqa: E402
 from tests.gpu_util import norm_event  # noqa: E402

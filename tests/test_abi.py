@@ -15,7 +15,8 @@ import r2inputs
 from oracle import balance as OB
 from oracle import ledger as OL
 from oracle import triangulation as OT
-from oracle.geometry import Geometry, effective_chunk_bytes
+from oracle.geometry import Geometry
+from tests.scenario import effective_chunk_bytes
 from paper_2512_25059_b200 import build as B
 from paper_2512_25059_b200 import r2ccl as R
 

@@ -11,7 +11,8 @@ import torch
 import r2inputs
 from oracle import protocol as OP
 from oracle import semantic as OS
-from oracle.geometry import Geometry, effective_chunk_bytes
+from oracle.geometry import Geometry
+from tests.scenario import effective_chunk_bytes
 from tests.gpu_util import check_result, norm_event, oracle_faults, run, same_bits, sim_comm
 from tests.test_gpu_rsag import check as check_op
 from tests.test_gpu_rsag import inputs as op_inputs

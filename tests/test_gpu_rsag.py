@@ -11,7 +11,8 @@ import torch
 import r2inputs
 from oracle import protocol as OP
 from oracle import semantic as OS
-from oracle.geometry import Geometry, effective_chunk_bytes
+from oracle.geometry import Geometry
+from tests.scenario import effective_chunk_bytes
 from tests.gpu_util import TD, norm_event, oracle_faults, same_bits, sim_comm, to_np
 from paper_2512_25059_b200 import build as B
 from paper_2512_25059_b200 import r2ccl as R

@@ -1,0 +1,126 @@
+"""The failover control plane needs no second kernel next to a stuck
+collective, and an unrecoverable collective is never reported as SUCCESS.
+
+* Deterministic error reporting (§3 "intercepts it to avoid
+  crashing"; SPEC.md:256 NoBackup; reading C-13 watchdog): a collective whose
+  kernel gives up (watchdog) returns R2_ERR_TIMEOUT from r2_sync every time.
+* Service lane (r2_kernels.cu service_main): probes, plan installs and
+  completion-word copies run inside the resident cooperative grid, so a fault
+  recovers bit-exact while another kernel holds every spare SM."""
+import os
+import subprocess
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import r2inputs
+from tests.gpu_util import check_result, oracle_geom, run, sim_comm, to_dev, poisoned, to_np
+from paper_2512_25059_b200 import build as B
+from paper_2512_25059_b200 import r2ccl as R
+from paper_2512_25059_b200 import torch_api as T
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def setup(cuda_required):
+    B.build()
+    torch.cuda.set_device(0)
+
+
+@pytest.fixture(scope="module")
+def spinner():
+    """tests/native/spinner.cu built with nvcc (test infrastructure only)."""
+    src = os.path.join(HERE, "native", "spinner.cu")
+    so = os.path.join(HERE, "native", "libr2t_spin.so")
+    if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        subprocess.run([B.NVCC, *B.ARCH, "-O2", "-shared", "-Xcompiler", "-fPIC", src, "-o", so], check=True)
+    lib = C.CDLL(so)
+    lib.r2t_spin.argtypes = [C.c_ulonglong, C.c_int, C.c_void_p]
+    lib.r2t_spin.restype = C.c_int
+    return lib
+
+
+def test_watchdog_abort_always_reported():
+    """50 collectives whose fault is detected (4 ms) only after the 1 ms
+    watchdog: every r2_sync returns TIMEOUT (never SUCCESS on a wrong
+    buffer); the communicator stays usable afterwards."""
+    n, N, dt = 4, 4096, "int32"
+    comm = sim_comm(n, K=4, W=1, chunk_bytes=4096, watchdog_ms=1)
+    xs = r2inputs.inputs(n, N, dt, seed=3)
+    g = oracle_geom(comm, N, dt)
+    codes = []
+    for i in range(50):
+        s = comm.status()["seq"] + 1
+        if i:
+            comm.inject_fault(at_seq=s, kind="REPAIR", src_rank=1, channel=0)
+            comm.inject_fault(at_seq=s, kind="HEAL", src_rank=1, channel=0)
+        comm.inject_fault(at_seq=s, kind="LINK", src_rank=1, channel=0, step=1, chunk=0, byte_offset=0,
+                          detect_delay_us=4000)
+        rc, out = run(comm, xs, dt)
+        if rc == R.SUCCESS:
+            check_result(out, xs, g, dt)       # SUCCESS must mean a complete result
+        codes.append(rc)
+    assert codes == [R.ERR_TIMEOUT] * 50, codes
+    st = comm.status()
+    assert st["last_error"] == R.ERR_TIMEOUT
+    s = st["seq"] + 1
+    comm.inject_fault(at_seq=s, kind="REPAIR", src_rank=1, channel=0)
+    comm.inject_fault(at_seq=s, kind="HEAL", src_rank=1, channel=0)
+    rc, out = run(comm, xs, dt)
+    assert rc == R.SUCCESS
+    check_result(out, xs, g, dt)
+    comm.finalize()
+
+
+@pytest.mark.parametrize("dtype", ["int32", "bfloat16"])
+def test_failover_with_spare_sms_held(spinner, dtype):
+    """The fault is detected 3 ms into the collective; by then a spinner fills
+    every SM the cooperative grid does not use (300 ms).  Probes, the verdict's
+    health records, the plan and the rollback read-back are served by the
+    resident service lane: the collective recovers bit-exact in ~1 ms."""
+    n, N = 4, (1 << 20) + 5
+    comm = sim_comm(n, K=2, W=2, chunk_bytes=64 * 1024)
+    xs = r2inputs.inputs(n, N, dtype, seed=11)
+    comm.inject_fault(at_seq=1, kind="LINK", src_rank=1, channel=0, step=1, chunk=1, byte_offset=4096,
+                      detect_delay_us=3000)
+    send = to_dev(xs, dtype)
+    recv = poisoned(n, N, dtype)
+    s_ar = torch.cuda.Stream()
+    s_spin = torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s_ar):
+        e0.record(s_ar)
+        T.allreduce(comm, send, recv, stream=s_ar, count=N)
+        e1.record(s_ar)
+    import time
+    time.sleep(0.001)                           # the collective is resident
+    kicks0 = comm.status()["n_service_kernels"]
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    assert spinner.r2t_spin(300_000_000, 2 * nsm, C.c_void_p(s_spin.cuda_stream)) == 0
+    rc = comm.sync()
+    ms = e0.elapsed_time(e1)
+    assert rc == R.SUCCESS
+    s_spin.synchronize()
+    out = to_np(recv, dtype)[:, :N]
+    check_result(out, xs, oracle_geom(comm, N, dtype), dtype)
+    ev = comm.events()
+    assert len(ev) == 1 and ev[0]["verdict"] == "LINK" and 0 < ev[0]["failover_ms"] < 5.0, ev
+    assert ms < 100.0, f"collective took {ms:.1f} ms: it waited for the spinner"
+    print(f"failover under held SMs: {ev[0]['failover_ms']:.3f} ms, collective {ms:.2f} ms, "
+          f"standalone service kernels {comm.status()['n_service_kernels'] - kicks0}")
+    comm.finalize()
+
+
+def test_probe_without_collective_uses_service_kernel():
+    """r2_probe with nothing resident: the standalone service kernel serves
+    the probe requests (healthy fabric -> NONE with all four probes S)."""
+    comm = sim_comm(4, K=2, W=1)
+    v = comm.probe(0, 1, 1)
+    assert v["verdict"] == "NONE" and v["outcomes"] == ("S", "S", "S", "S")
+    assert comm.status()["n_service_kernels"] >= 1
+    comm.finalize()

@@ -7,10 +7,13 @@ import json
 import os
 
 import numpy as np
+
+import r2inputs
 import pytest
 
 from oracle import balance as B
 from oracle import cost as C
+from oracle.geometry import Geometry
 from oracle import ledger as L
 from oracle import triangulation as T
 
@@ -219,13 +222,32 @@ def test_ystar_solves_t1_eq_t2_and_grid_argmin():
         assert np.all(tl[0] <= tl + 1e-12)
 
 
-def test_hbm_bytes_formula_by_counting():
-    """(5n-4)/n S from counting each step's reads/writes per shard unit."""
-    for n in range(2, 9):
-        reads = (n - 1) + (n - 2) + 2 + (n - 2)      # x, scratch, final add, AG forward
-        writes = (n - 1) + 1 + (n - 1)              # scratch in, own recv, recv in
-        assert C.hbm_bytes_per_gpu(n, n) == pytest.approx(reads + writes)
-        assert C.nvlink_bytes_per_gpu(n, n) == 2 * (n - 1)
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_traffic_formulas_against_executed_schedule(n):
+    """SURVEY §8(d) per-GPU traffic of the push ring ("must send
+    (n-1)/n D_total ... must receive the same amount"): the closed forms
+    2(n-1)/n S (NVLink) and (5n-4)/n S (HBM) equal the bytes the Layer-2
+    simulator actually moves when it executes the schedule -- per rank, for
+    every rank, with no padding (N a multiple of n*K*V)."""
+    from oracle import protocol as OP
+    K, E = 2, 4
+    N = n * K * 4 * 16
+    xs = r2inputs.inputs(n, N, "int32", seed=n)
+    res = OP.simulate(xs, Geometry(n, K, N, E, 64), "int32", seed=1)
+    S = N * E
+    for r in range(n):
+        assert res.bytes_sent[r].sum() == C.nvlink_bytes_per_gpu(S, n)
+        assert res.hbm_bytes[r] == C.hbm_bytes_per_gpu(S, n)
+
+
+def test_traffic_formulas_against_survey_table():
+    """SURVEY §8(d)'s printed table at S = 256 MiB: NVLink per direction
+    256 / 384 / 448 MiB and HBM total 768 / 1024 / 1152 MiB at n = 2 / 4 / 8."""
+    S = 256 * 2 ** 20
+    table = {2: (256, 768), 4: (384, 1024), 8: (448, 1152)}
+    for n, (nv, hbm) in table.items():
+        assert C.nvlink_bytes_per_gpu(S, n) == nv * 2 ** 20
+        assert C.hbm_bytes_per_gpu(S, n) == hbm * 2 ** 20
 
 
 @pytest.mark.parametrize("n", [2, 3, 5])

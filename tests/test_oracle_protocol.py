@@ -12,7 +12,8 @@ import pytest
 
 import r2inputs
 from oracle import semantic as S
-from oracle.geometry import Geometry, effective_chunk_bytes
+from oracle.geometry import Geometry
+from tests.scenario import effective_chunk_bytes
 from oracle.protocol import BALANCE, HOT_REPAIR, Fault, simulate
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))

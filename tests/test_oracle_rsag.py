@@ -18,7 +18,8 @@ import pytest
 
 import r2inputs
 from oracle import semantic as S
-from oracle.geometry import ALL_GATHER, REDUCE_SCATTER, Geometry, effective_chunk_bytes
+from oracle.geometry import ALL_GATHER, REDUCE_SCATTER, Geometry
+from tests.scenario import effective_chunk_bytes
 from oracle.protocol import BALANCE, HOT_REPAIR, Fault, simulate
 
 
