@@ -50,7 +50,9 @@ typedef enum {
 typedef enum { R2_INT32 = 0, R2_FLOAT32 = 1, R2_BFLOAT16 = 2 } r2_dtype_t;
 
 /* Collectives on the ring (SURVEY §8(f) f1 for the standalone halves). */
-typedef enum { R2_OP_ALLREDUCE = 0, R2_OP_REDUCE_SCATTER = 1, R2_OP_ALL_GATHER = 2, R2_OP_BROADCAST = 3 } r2_op_t;
+typedef enum { R2_OP_ALLREDUCE = 0, R2_OP_REDUCE_SCATTER = 1, R2_OP_ALL_GATHER = 2, R2_OP_BROADCAST = 3,
+               R2_OP_R2CC_STAGE2 = 4  /* internal: R²CCL-AllReduce stage 2 (tailored broadcast, reading R-9) */
+} r2_op_t;
 
 /* Single-failure strategies (P:57 HotRepair; P:73 R²CCL-Balance). */
 typedef enum { R2_HOT_REPAIR = 0, R2_BALANCE = 1 } r2_strategy_t;
@@ -157,7 +159,24 @@ typedef struct {
   int beta_mbps;
   int reprobe_us, reprobe_max_us;
   int channel_gbps;
+  int allreduce_algo;   /* r2_algo_t (default AUTO)                                  */
+  int alpha_launch_ns;  /* cost model: one more collective launch (R²CCL stage 2)    */
 } r2_config_t;
+
+/*
+ * AllReduce algorithm under a degraded rank (P:106-136,
+ * App. A).  RING: always the ring (Balance / HotRepair re-placement
+ * of the dead channels).  R2CC: R²CCL-AllReduce whenever it applies -- exactly
+ * one rank f has dead channel endpoints (no dead link), n >= 3, and App. A's
+ * planner gives Y > 0 (lost fraction X > n/(3n-2)): stage 1 runs the global
+ * ring on f's healthy channels over the first (1-Y) of the buffer concurrently
+ * with a partial ring over the n-1 healthy ranks on f's dead channels over the
+ * rest; stage 2 (a second launch, its own seq) is the tailored broadcast f ->
+ * f+1 (adds f's contribution) -> ... -> f-1 -> f (reading R-9).  AUTO: the
+ * alpha-beta cost model picks the faster of the two per call (reading R-11).
+ * A call that runs R²CCL-AllReduce enqueues two collectives (two seqs).
+ */
+typedef enum { R2_ALGO_AUTO = 0, R2_ALGO_RING = 1, R2_ALGO_R2CC = 2 } r2_algo_t;
 
 typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2 } r2_protocol_t;
 
@@ -235,6 +254,13 @@ typedef struct {
   int n_reprobes;             /* re-probe rounds run                              */
   int n_service_kernels;      /* standalone service-kernel launches (monitor work
                                  with no collective resident to serve it)         */
+  /* R²CCL-AllReduce (f2): calls that ran it, and the planner's choice for the
+     last one (degraded rank f, lost fraction X, partial share Y = App. A's
+     optimal partition, element split N_A + N_P, the seq of its stage 2)        */
+  int n_r2cc;
+  int r2cc_rank;
+  double r2cc_X, r2cc_Y;
+  uint64_t r2cc_NA, r2cc_NP, r2cc_seq;
 } r2_status_t;
 
 /* Fill *cfg with the defaults documented above. */

@@ -15,6 +15,8 @@ against SPEC's printed values, T1(Y*) = T2(Y*) and a grid argmin.
 """
 from __future__ import annotations
 
+import math
+
 
 def ring_allreduce_time(n: int, g: int, D: float, B: float) -> float:
     """P:121: 2(ng-1)/(ng) * D/B."""
@@ -75,6 +77,35 @@ def y_star(n: int, g: int, X: float) -> float:
 def optimal_partition(n: int, g: int, X: float) -> float:
     """App. A Step 3: Y = 0 if X <= threshold else Y*."""
     return 0.0 if X <= threshold(n, g) else y_star(n, g, X)
+
+
+def lost_fraction(weights, dead) -> float:
+    """X of P:121 on the box (reading R-9): the degraded rank's lost share of
+    its channel bandwidth, sum of its dead channels' weights over all."""
+    return sum(weights[c] for c in dead) / sum(weights)
+
+
+def r2cc_split(N: int, V: int, Y: float) -> tuple[int, int]:
+    """Reading R-9: the partial AllReduce takes the last N_P = floor(Y N / V) V
+    elements (whole 16-byte vectors), the global ring the first N_A = N - N_P."""
+    NP = math.floor(Y * N / V) * V
+    NP = min(NP, N // V * V)
+    return N - NP, NP
+
+
+def algo_times(n: int, X: float, Y: float, S: float, alpha: float, B: float, launch: float):
+    """Reading R-11 (the alpha-beta strategy choice of SURVEY §8(f) f3):
+    per-call time of the ring on the degraded communicator and of
+    R²CCL-AllReduce, each = (ring steps) x alpha + the paper's bandwidth terms
+    (P:121-130 with g = 1, B = per-GPU rate): the ring is throttled to
+    (1 - X) B at the degraded rank; R²CCL-AllReduce pays max(T1, T2) + T3 plus
+    the n steps and the launch of its stage 2.  Returns (t_ring, t_r2cc)."""
+    t_ring = (2 * n - 2) * alpha + ring_allreduce_time(n, 1, S, (1 - X) * B)
+    if Y <= 0:
+        return t_ring, float("inf")
+    T1, T2, T3 = stage_times(Y, n, 1, X, S, B)
+    # the partial ring has n - 1 members: P:123's (n-1)g ring factor
+    return t_ring, (2 * n - 2) * alpha + max(T1, T2) + n * alpha + T3 + launch
 
 
 def bottleneck_load(Y: float, D: float = 1.0) -> float:

@@ -52,6 +52,9 @@ def ceil_div(a: int, b: int) -> int:
 
 
 ALLREDUCE, REDUCE_SCATTER, ALL_GATHER, BROADCAST = "allreduce", "reduce_scatter", "all_gather", "broadcast"
+# R²CCL-AllReduce's stage 2, the tailored broadcast (reading R-9): a
+# chain from the degraded rank (root) once around the ring back to it
+STAGE2 = "r2cc_stage2"
 @dataclass(frozen=True)
 class Geometry:
     n: int
@@ -68,8 +71,12 @@ class Geometry:
         return 16 // self.elem_bytes
 
     @property
+    def chain(self) -> bool:
+        return self.op in (BROADCAST, STAGE2)
+
+    @property
     def Np(self) -> int:
-        if self.op == BROADCAST:
+        if self.chain:
             return self.shard
         if self.op != ALLREDUCE:
             return self.n * self.shard
@@ -87,23 +94,25 @@ class Geometry:
     @property
     def stride(self) -> int:
         """Distance between shards in the user buffers."""
-        return self.shard if self.op in (ALLREDUCE, BROADCAST) else self.N
+        return self.shard if self.op in (ALLREDUCE, BROADCAST, STAGE2) else self.N
 
     @property
     def total(self) -> int:
         """Elements of the n-shard user buffer (AllReduce / Broadcast: N)."""
-        return self.N if self.op in (ALLREDUCE, BROADCAST) else self.n * self.N
+        return self.N if self.op in (ALLREDUCE, BROADCAST, STAGE2) else self.n * self.N
 
     def shard_limit(self, s: int) -> int:
         """One past the last valid global element of shard s."""
         if self.op == ALLREDUCE:
             return min(self.N, (s + 1) * self.shard)
-        if self.op == BROADCAST:
+        if self.chain:
             return self.N
         return s * self.N + self.N
 
     def active(self, r: int, t: int) -> bool:
         """Does rank r send at step t?  (Broadcast: only at its chain position.)"""
+        if self.op == STAGE2:
+            return t == (r - self.root) % self.n
         if self.op != BROADCAST:
             return True
         return t == (r - self.root) % self.n and t <= self.n - 2
@@ -118,7 +127,7 @@ class Geometry:
         protocol's unpack of the last all-gather step (no connection used)."""
         if self.op == REDUCE_SCATTER:
             return t == self.n - 1
-        if self.op == BROADCAST:
+        if self.chain:
             return False
         return self.ll and t == self.steps - 1
 
@@ -137,7 +146,7 @@ class Geometry:
     @property
     def steps(self) -> int:
         base = {ALLREDUCE: 2 * self.n - 2, REDUCE_SCATTER: self.n, ALL_GATHER: self.n - 1,
-                BROADCAST: self.n - 1}[self.op]
+                BROADCAST: self.n - 1, STAGE2: self.n}[self.op]
         return base + (1 if self.ll and self.op != REDUCE_SCATTER else 0)
 
     def item_len(self, j: int) -> int:
@@ -149,7 +158,7 @@ class Geometry:
 
     def shard_sent(self, r: int, t: int) -> int:
         """Shard that rank r sends at (op-)step t (§8 header)."""
-        if self.op == BROADCAST:
+        if self.chain:
             return 0
         n = self.n
         ta = t + self.t0

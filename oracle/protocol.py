@@ -50,6 +50,17 @@ Broadcast (f1, reading R-8): a pipelined chain from the root along the ring;
 worker (r, c) holds only the items of r's chain position t_r, reads the
 root's input (t_r = 0) or its own received buffer, and writes the next rank's
 buffer.  Positions of other steps count as complete in r's ledger.
+
+R²CCL-AllReduce stage 2 (f2, "a broadcast initiated from the failure
+server node, a pipelined ring broadcast across the healthy servers, and the
+final delivery ... back to the failure node"; reading R-9): a chain of n
+steps from the degraded rank (root) around the ring back to it.  recv_init
+holds every rank's stage-1 result (the healthy ranks' partial AllReduce).
+Step 0: the root sends its input into the next rank's tailor buffer; step 1:
+that rank adds it to its partial result (acc (+) x, acc = the partial
+result), keeps the sum and sends it on; steps 2..n-1 forward the sum, the last
+one into the root's buffer.  (Stage 1's two rings are plain ring AllReduces
+over disjoint channel sets and are simulated as such.)
 """
 from __future__ import annotations
 
@@ -60,7 +71,7 @@ import numpy as np
 from . import balance as _bal
 from . import ledger as _led
 from . import triangulation as _tri
-from .geometry import ALL_GATHER, ALLREDUCE, BROADCAST, REDUCE_SCATTER, Geometry
+from .geometry import ALL_GATHER, ALLREDUCE, BROADCAST, REDUCE_SCATTER, STAGE2, Geometry
 from .semantic import hop_add, np_dtype
 
 HOT_REPAIR = "HOT_REPAIR"
@@ -119,7 +130,7 @@ class SimResult:
 
 class Simulator:
     def __init__(self, xs, geom: Geometry, dtype: str, faults=(), strategy=BALANCE,
-                 weights=None, health=None, seed=0, inplace=False, poison=True):
+                 weights=None, health=None, seed=0, inplace=False, poison=True, recv_init=None):
         self.g, self.dtype = geom, dtype
         self.n, self.K, self.m, self.V = geom.n, geom.K, geom.m, geom.V
         self.N = geom.N
@@ -154,6 +165,10 @@ class Simulator:
             self.recv = [self._poisoned(self.N, poison) for _ in range(n)]
             if inplace:
                 self.recv[geom.root] = np.array(xs[geom.root], dtype=dt, copy=True)
+        elif self.op == STAGE2:
+            self.x = [np.asarray(x, dtype=dt) for x in xs]
+            self.recv = [np.array(a, dtype=dt, copy=True) for a in recv_init]
+            self.tailor = [self._poisoned(geom.shard, poison) for _ in range(n)]
         elif self.op == ALL_GATHER:
             self.recv = [self._poisoned(n * self.N, poison) for _ in range(n)]
             if inplace:
@@ -266,6 +281,18 @@ class Simulator:
         r1 = (r + 1) % n
         nb = (e1 - e0) * g.elem_bytes                     # bytes of one operand of this part
         if g.local(t) and self.op != REDUCE_SCATTER:      # LL unpack: the data already landed here
+            return
+        if self.op == STAGE2:                             # tailored broadcast (reading R-9)
+            if t == 0:                                    # the degraded rank's input -> next rank's tailor buffer
+                self.tailor[r1][o0:o1] = self.xread(r, e0, e1, lim)
+                self.hbm[r] += nb
+                self.hbm[r1] += nb
+            elif t == 1:                                  # partial result (+) f's contribution
+                val = hop_add(self.rread(r, e0, e1, lim), self.tailor[r][o0:o1], self.dtype)
+                self.rwrite(r, e0, val, lim)
+                self.rwrite(r1, e0, val, lim)
+            else:
+                self.rwrite(r1, e0, self.rread(r, e0, e1, lim), lim)
             return
         if self.op == BROADCAST:                          # chain: root's input, else what arrived here
             val = self.xread(r, e0, e1, lim) if t == 0 else self.rread(r, e0, e1, lim)

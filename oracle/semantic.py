@@ -161,3 +161,30 @@ def normwise_rel_error(y: np.ndarray, xs: list[np.ndarray], dtype: str) -> float
     den = float(np.linalg.norm(ex))
     num = float(np.linalg.norm(as_float64(y, dtype) - ex))
     return num / den if den > 0 else num
+
+
+def r2cc_allreduce(xs: list[np.ndarray], dtype: str, f: int, NA: int, shard_A: int, shard_P: int) -> np.ndarray:
+    """R²CCL-AllReduce (P:106-136 §5.2 "Partial AllReduce" / "R²CCL-AllReduce";
+    DESIGN.md reading R-9): the result every rank holds.
+
+    * elements [0, NA): the global ring AllReduce over all n ranks (stage 1,
+      P:113 "a global AllReduce ... spans all servers") -- the Layer-1 fold
+      above with shards of shard_A elements;
+    * elements [NA, N): the partial AllReduce over the n-1 ranks other than
+      the degraded rank f ("the partial AllReduce excludes the failure
+      node"), a ring in rank order with f removed -- the same fold over that
+      rank list, shards of shard_P elements -- followed by the tailored
+      broadcast: f's contribution is added once, at the rank after f,
+      as one hop acc (+) x with acc = the partial result and x = x_f, and the
+      sum travels on unchanged.
+    """
+    n = len(xs)
+    N = len(xs[0])
+    y = np.empty(N, dtype=np_dtype(dtype))
+    if NA:
+        y[:NA] = allreduce([np.asarray(x)[:NA] for x in xs], shard_A, dtype)
+    if NA < N:
+        healthy = [np.asarray(xs[r])[NA:] for r in range(n) if r != f]
+        p = allreduce(healthy, shard_P, dtype)
+        y[NA:] = hop_add(p, np.asarray(xs[f])[NA:], dtype)
+    return y

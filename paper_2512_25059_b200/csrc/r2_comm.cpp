@@ -5,6 +5,7 @@
 #include "r2_comm.h"
 
 #include <cuda.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
@@ -27,13 +28,15 @@ constexpr int kMaxInflight = 16;   // outstanding collectives per communicator
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, size_t ll_max_bytes) {
+ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, size_t ll_max_bytes, bool with_r2cc) {
   ArenaLayout L{};
   const size_t q = (size_t)n * K * 16;
   L.slot_bytes = std::max<size_t>(align_up(std::max<size_t>(max_bytes, 16), q) / n, 16 * K);
   // chunks per channel slice: a Broadcast's slice is the whole buffer / K (n times an
   // AllReduce slice)
-  const size_t slice_cap = align_up(std::max<size_t>(max_bytes, 16), (size_t)K * 16) / K;
+  // a ring of any channel subset may carry the whole payload in one slice
+  // (R²CCL-AllReduce rings run on channel subsets; chains cap chunks at 128 KiB)
+  const size_t slice_cap = align_up(std::max<size_t>(max_bytes, 16), 16);
   const size_t bchunk = std::min<size_t>(chunk, (size_t)128 << 10);   // Broadcast chunk cap (r2_geometry_op)
   L.m_cap = (int)std::max<size_t>((slice_cap + bchunk - 1) / bchunk, (size_t)W);
   // LL: two 16-byte lines per 16-byte vector, one slot per ring step
@@ -58,25 +61,44 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, siz
   L.stage = take(L.slot_bytes);
   L.dctrl = take(sizeof(DevCtrl));
   L.health = take((size_t)4 * n * K * 4);
+  // ring 1 (R²CCL-AllReduce's partial ring over n-1 ranks, reading R-9) and the
+  // stage-2 buffer where the degraded rank's contribution lands
+  if (n >= 3 && with_r2cc) {
+    const size_t q1 = (size_t)(n - 1) * K * 16;
+    L.slot1_bytes = std::max<size_t>(align_up(std::max<size_t>(max_bytes, 16), q1) / (n - 1), 16 * K);
+    L.scratch1 = take((size_t)2 * (n - 2) * L.slot1_bytes);
+    L.flags1 = take((size_t)steps * K * L.m_cap * 4);
+    L.counters1 = take((size_t)steps * K * L.m_cap * 8);
+    L.misc1 = take(sizeof(MiscDev));
+    L.stage1 = take(L.slot1_bytes);
+    L.tailor_bytes = align_up(std::max<size_t>(max_bytes, 16), (size_t)K * 16);
+    L.tailor = take(L.tailor_bytes);
+  }
   L.total = align_up(off, 4096);
   return L;
 }
 
-RankPtrs ptrs_of(char* base, const ArenaLayout& L) {
+// region 0: the arena as ring 0 sees it; region 1: ring 1's own scratch,
+// flags, counters, misc and stage (per-rank state shared)
+RankPtrs ptrs_of(char* base, const ArenaLayout& L, int region = 0) {
   RankPtrs p;
-  p.scratch = base + L.scratch;
+  p.scratch = base + (region ? L.scratch1 : L.scratch);
   p.ll = base + L.ll;
-  p.flags = (unsigned int*)(base + L.flags);
-  p.counters = (unsigned long long*)(base + L.counters);
+  p.flags = (unsigned int*)(base + (region ? L.flags1 : L.flags));
+  p.counters = (unsigned long long*)(base + (region ? L.counters1 : L.counters));
   p.ep_dead = (unsigned int*)(base + L.ep_dead);
   p.link_dead = (unsigned int*)(base + L.link_dead);
   p.alert = (unsigned int*)(base + L.alert);
   p.mailbox = (unsigned int*)(base + L.mailbox);
   p.desc = (unsigned long long*)(base + L.desc);
-  p.misc = (MiscDev*)(base + L.misc);
-  p.stage = base + L.stage;
+  p.misc = (MiscDev*)(base + (region ? L.misc1 : L.misc));
+  p.stage = base + (region ? L.stage1 : L.stage);
   p.dctrl = (DevCtrl*)(base + L.dctrl);
   p.health = (unsigned int*)(base + L.health);
+  MiscDev* m0 = (MiscDev*)(base + L.misc);
+  p.abort = &m0->abort_seq;
+  p.bytes = m0->bytes;
+  p.tailor = L.tailor ? base + L.tailor : nullptr;
   return p;
 }
 
@@ -182,6 +204,7 @@ void release_resources(r2_comm* c) {
   if (c->health_map_host) cudaFreeHost(c->health_map_host);
   if (c->health_pinned) cudaFreeHost(c->health_pinned);
   if (c->peers_dev) cudaFree(c->peers_dev);
+  if (c->peers_dev1) cudaFree(c->peers_dev1);
   if (c->regtab_dev) cudaFree(c->regtab_dev);
   if (c->host_stage) cudaFree(c->host_stage);
   for (auto& ev : c->host_ev) cudaEventDestroy(ev);
@@ -246,6 +269,8 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->beta_mbps = 650000;         // per-GPU NVLink store rate at large sizes
   cfg->reprobe_us = 2000;
   cfg->reprobe_max_us = 200000;
+  cfg->allreduce_algo = R2_ALGO_AUTO;
+  cfg->alpha_launch_ns = 6000;     // one cooperative launch + prologue (profiles/r01_host_overhead_n4.log)
 }
 
 extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,
@@ -289,7 +314,12 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     delete c;
     return R2_ERR_INVALID_ARG;
   }
-  c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes, cfg.ll_max_bytes);
+  if (cfg.allreduce_algo < R2_ALGO_AUTO || cfg.allreduce_algo > R2_ALGO_R2CC) {
+    delete c;
+    return R2_ERR_INVALID_ARG;
+  }
+  c->lay = make_layout(c->n, c->K, c->W, cfg.chunk_bytes, cfg.max_bytes, cfg.ll_max_bytes,
+                       cfg.allreduce_algo != R2_ALGO_RING);
   auto fail = [&](r2_result_t e) {
     cudaDeviceSynchronize();
     release_resources(c);
@@ -342,11 +372,16 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
 
   // ---- map every peer's arena (multi-registration at init)
   c->peers_host.assign((size_t)c->nlocal * c->n, RankPtrs{});
+  c->peers_host1.assign((size_t)c->nlocal * c->n, RankPtrs{});
   if (c->sim) {
     for (int l = 0; l < c->nlocal; ++l)
-      for (int p = 0; p < c->n; ++p) c->peers_host[l * c->n + p] = ptrs_of(c->arena[p], c->lay);
+      for (int p = 0; p < c->n; ++p) {
+        c->peers_host[l * c->n + p] = ptrs_of(c->arena[p], c->lay);
+        c->peers_host1[l * c->n + p] = ptrs_of(c->arena[p], c->lay, 1);
+      }
   } else if (world == 1) {
     c->peers_host[0] = ptrs_of(c->arena[0], c->lay);
+    c->peers_host1[0] = ptrs_of(c->arena[0], c->lay, 1);
   } else {
     RegXchg mine{};
     if (cudaIpcGetMemHandle(&mine.h, c->arena[0]) != cudaSuccess) return fail(R2_ERR_CUDA);
@@ -364,12 +399,16 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
         b = (char*)op;
       }
       c->peers_host[p] = ptrs_of(b, c->lay);
+      c->peers_host1[p] = ptrs_of(b, c->lay, 1);
     }
   }
-  if (cudaMalloc(&c->peers_dev, sizeof(RankPtrs) * c->peers_host.size()) != cudaSuccess) return fail(R2_ERR_CUDA);
-  if (cudaMemcpy(c->peers_dev, c->peers_host.data(), sizeof(RankPtrs) * c->peers_host.size(),
-                 cudaMemcpyHostToDevice) != cudaSuccess)
-    return fail(R2_ERR_CUDA);
+  for (int region = 0; region < 2; ++region) {
+    std::vector<RankPtrs>& h = region ? c->peers_host1 : c->peers_host;
+    RankPtrs*& d = region ? c->peers_dev1 : c->peers_dev;
+    if (cudaMalloc(&d, sizeof(RankPtrs) * h.size()) != cudaSuccess) return fail(R2_ERR_CUDA);
+    if (cudaMemcpy(d, h.data(), sizeof(RankPtrs) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(R2_ERR_CUDA);
+  }
   c->regtab_host.assign((size_t)R2_MAX_REGS * c->n, 0ull);
   if (cudaMalloc(&c->regtab_dev, sizeof(unsigned long long) * c->regtab_host.size()) != cudaSuccess)
     return fail(R2_ERR_CUDA);
@@ -507,34 +546,58 @@ extern "C" r2_result_t r2_inject_fault(r2_comm_t c, const r2_fault_t* f) {
   return R2_SUCCESS;
 }
 
-// One ring collective (AllReduce, or the standalone ReduceScatter / AllGather
-// halves of SURVEY §8(f) f1).  `count`: AllReduce elements; RS recvcount; AG
-// sendcount.
-static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* recv, size_t count, r2_dtype_t dt,
-                                void* stream, int root = 0) {
+// One ring of a launch: which ranks in which order, on which channels, over
+// which part of the user buffers (r2_internal.h LaunchParams).
+struct RingSpec {
+  r2_op_t op = R2_OP_ALLREDUCE;
+  const void* send = nullptr;                // region start in the user buffers
+  void* recv = nullptr;
+  size_t count = 0;                          // elements of the region (op convention)
+  int root = 0;                              // chain collectives: root's ring position
+  std::vector<int> order;                    // global rank at each ring position
+  std::vector<int> chans;                    // global channels, ring-local order
+  int region = 0;                            // arena region set (0 / 1)
+  size_t peer_recv_off = 0;                  // bytes: region start inside a peer's registered recv
+  bool allow_ll = true;                      // the alpha-beta protocol choice may pick LL
+  size_t row_elems = 0;                      // sim mode: elements of a full rank row (0: the region's own)
+};
+
+RingSpec standard_ring(const r2_comm* c, r2_op_t op, const void* send, void* recv, size_t count, int root) {
+  RingSpec rs;
+  rs.op = op;
+  rs.send = send;
+  rs.recv = recv;
+  rs.count = count;
+  rs.root = root;
+  for (int r = 0; r < c->n; ++r) rs.order.push_back(r);
+  for (int k = 0; k < c->K; ++k) rs.chans.push_back(k);
+  return rs;
+}
+
+// Geometry, protocol and every LaunchParams field of one ring (no faults).
+r2_result_t prep_ring(r2_comm* c, const RingSpec& rs, r2_dtype_t dt, uint32_t seq, LaunchParams& p, RingInfo& ri) {
+  const r2_op_t op = rs.op;
   const int E = elem_bytes(dt);
-  if (c->n == 1) {
-    if (send != recv) CK(cudaMemcpyAsync(recv, send, count * E, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
-    c->last_stream = stream;
-    return R2_SUCCESS;
-  }
-  const uint64_t t_in = r2_debug >= 2 ? r2_now_ns() : 0;
+  const int n = (int)rs.order.size(), K = (int)rs.chans.size();
+  const size_t count = rs.count;
   r2_geometry_t g;
-  r2_result_t e = r2_geometry_op(op, count, dt, c->n, c->K, c->W, c->cfg.chunk_bytes, &g);
+  r2_result_t e = r2_geometry_op(op, count, dt, n, K, c->W, c->cfg.chunk_bytes, &g);
   if (e != R2_SUCCESS) return e;
-  if ((op != R2_OP_BROADCAST && g.shard * E > c->lay.slot_bytes) || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
-  const uint32_t seq = (uint32_t)(c->seq + 1);
+  const size_t slot = rs.region ? c->lay.slot1_bytes : c->lay.slot_bytes;
+  const bool chain = op == R2_OP_BROADCAST || op == R2_OP_R2CC_STAGE2;
+  if ((!chain && g.shard * E > slot) || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
+  if (op == R2_OP_R2CC_STAGE2 && g.Np * E > c->lay.tailor_bytes) return R2_ERR_INVALID_ARG;
   // protocol: alpha-beta model over the ring's steps; LL
   // moves twice the bytes but pays no fence per step (r2ccl.h "Protocols")
   bool ll = false;
-  const bool ll_fits = c->lay.ll_slot_bytes && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
-  if (op == R2_OP_BROADCAST) {
-    ll = false;                                        // always SIMPLE (r2ccl.h)
+  const bool ll_fits = rs.allow_ll && rs.region == 0 && c->lay.ll_slot_bytes && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
+  if (chain || !rs.allow_ll) {
+    ll = false;                                        // chains: always SIMPLE (r2ccl.h)
   } else if (c->cfg.protocol == R2_PROTO_LL) {
     if (!ll_fits) return R2_ERR_INVALID_ARG;
     ll = true;
   } else if (c->cfg.protocol == R2_PROTO_AUTO && ll_fits) {
-    const double wire = (double)(op == R2_OP_ALLREDUCE ? 2 : 1) * (c->n - 1) * (double)g.shard * E;
+    const double wire = (double)(op == R2_OP_ALLREDUCE ? 2 : 1) * (n - 1) * (double)g.shard * E;
     const double bpns = std::max(c->cfg.beta_mbps, 1) / 1000.0;
     const double t_simple = g.steps * (double)c->cfg.alpha_simple_ns + wire / bpns;
     const double t_ll = (g.steps + (op != R2_OP_REDUCE_SCATTER)) * (double)c->cfg.alpha_ll_ns + 2 * wire / bpns;
@@ -543,16 +606,22 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   const int steps = g.steps + (ll && op != R2_OP_REDUCE_SCATTER ? 1 : 0);   // + the LL unpack step
   const int local_step = ll && op != R2_OP_REDUCE_SCATTER ? steps - 1 : g.local_step;
 
-  LaunchParams p;
   memset(&p, 0, sizeof(p));
   p.seq = seq;
-  p.n = c->n;
-  p.K = c->K;
+  p.n = n;
+  p.K = K;
   p.W = c->W;
   p.m = g.m;
   p.steps = steps;
-  p.nlocal = c->nlocal;
   p.first_rank = c->first_rank;
+  p.ng = c->n;
+  p.Kg = c->K;
+  p.ring_id = rs.region;
+  for (int i = 0; i < n; ++i) p.ring[i] = rs.order[i];
+  for (int i = 0; i < K; ++i) p.chan[i] = rs.chans[i];
+  // participants: this process's ranks that are on the ring
+  for (int l = 0; l < c->nlocal; ++l)
+    if (std::find(rs.order.begin(), rs.order.end(), c->first_rank + l) != rs.order.end()) p.part_l[p.nlocal++] = l;
   p.dtype = dt == R2_INT32 ? R2D_INT32 : (dt == R2_FLOAT32 ? R2D_FLOAT32 : R2D_BF16);
   p.elem_bytes = E;
   p.V = g.V;
@@ -561,21 +630,23 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.local_step = local_step;
   p.fin_step = local_step >= 0 ? local_step - 1 : steps - 1;   // last step with incoming words
   p.peer_recv = !ll && op != R2_OP_REDUCE_SCATTER;
+  p.peer_recv_off = rs.peer_recv_off;
   p.ll = ll;
   p.ll_slot_bytes = c->lay.ll_slot_bytes;
   if (c->cfg.channel_gbps > 0)          // lane rate = channel rate / W
     p.lane_ps_per_byte = (unsigned int)((1000ull * c->W + c->cfg.channel_gbps / 2) / c->cfg.channel_gbps);
   p.sstride = g.stride;
   p.slen = op == R2_OP_ALLREDUCE ? g.shard : count;
-  // in-place (NCCL's convention for RS / AG: recv / send is the own shard)
   const size_t shard_bytes = count * (size_t)E;
+  const void* send = rs.send;
+  void* recv = rs.recv;
   p.inplace = op == R2_OP_ALLREDUCE && send == recv;
   if (op == R2_OP_ALL_GATHER && !c->sim)
     p.ag_inplace = (const char*)send == (const char*)recv + (size_t)c->rank * shard_bytes;
   if (c->sim && (op == R2_OP_REDUCE_SCATTER || op == R2_OP_ALL_GATHER) && (send == recv))
     return R2_ERR_INVALID_ARG;   // sim: out-of-place only
-  if (op == R2_OP_BROADCAST) {
-    p.root = root;
+  if (chain) {
+    p.root = rs.root;
     p.ag_inplace = send == recv;                       // root: no local copy
   }
   p.strategy = c->cfg.strategy;
@@ -585,23 +656,26 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   p.shard = g.shard;
   p.slice = g.slice;
   p.chunk = g.chunk;
-  p.slot_bytes = c->lay.slot_bytes;
+  p.slot_bytes = slot;
   p.watchdog_ns = (unsigned long long)c->cfg.watchdog_ms * 1000000ull;
   p.trace = c->trace;
-  for (int k = 0; k < c->K; ++k) p.weights[k] = c->weights[k];
-  p.peers = c->peers_dev;
+  for (int k = 0; k < K; ++k) p.weights[k] = c->weights[rs.chans[k]];
+  p.peers = rs.region ? c->peers_dev1 : c->peers_dev;
   p.regtab = c->regtab_dev;
+  p.svc = c->svc_dev;
+  p.grid_exited = &((MiscDev*)(c->arena[0] + c->lay.misc))->grid_exited;   // local rank 0, ring-0 misc
 
-  // recv publication (real mode) / rank buffers (sim mode: 16-B aligned rows)
-  const size_t full = align_up((size_t)g.N * E, 16), part = align_up(count * E, 16);
-  const size_t sstride = op == R2_OP_ALL_GATHER ? part : full;       // sim row strides
-  const size_t rstride = op == R2_OP_REDUCE_SCATTER ? part : full;
+  // rank buffers: sim mode rows of the FULL user buffers (16-B aligned); the
+  // region starts at send / recv of rank 0's row
+  const size_t full = align_up((size_t)rs.row_elems * E, 16);
+  const size_t part = align_up(count * E, 16);
+  const size_t sstride = rs.row_elems ? full : (op == R2_OP_ALL_GATHER ? part : align_up((size_t)g.N * E, 16));
+  const size_t rstride = rs.row_elems ? full : (op == R2_OP_REDUCE_SCATTER ? part : align_up((size_t)g.N * E, 16));
   for (int l = 0; l < c->nlocal; ++l) {
     p.send[l] = (const char*)send + (size_t)l * sstride;
     p.recv[l] = (char*)recv + (size_t)l * rstride;
     p.ctrl[l] = c->ctrl_dev[l];
   }
-  p.svc = c->svc_dev;
   if (!c->sim && p.peer_recv) {
     const size_t rbytes = (size_t)g.N * E;
     int found = -1;
@@ -617,6 +691,56 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     p.recv_off[0] = (unsigned long long)((char*)recv - c->regs[found].dptr);
   }
 
+  memset(&ri, 0, sizeof(ri));
+  ri.op = op;
+  ri.root = rs.root;
+  ri.local_step = local_step;
+  ri.ll = ll;
+  ri.m = g.m;
+  ri.steps = steps;
+  ri.V = g.V;
+  ri.slice = g.slice;
+  ri.chunk = g.chunk;
+  ri.n = n;
+  ri.K = K;
+  ri.region = rs.region;
+  for (int i = 0; i < n; ++i) ri.order[i] = rs.order[i];
+  for (int i = 0; i < K; ++i) {
+    ri.chans[i] = rs.chans[i];
+    ri.chan_mask |= 1u << rs.chans[i];
+  }
+  return R2_SUCCESS;
+}
+
+// One launch (one seq): its rings run concurrently in one cooperative grid
+// (+ the service CTA).  Faults armed for the seq go to the ring carrying
+// their channel (ring-local step / chunk / origin).
+r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt, void* stream) {
+  const uint64_t t_in = r2_debug >= 2 ? r2_now_ns() : 0;
+  const uint32_t seq = (uint32_t)(c->seq + 1);
+  LaunchSet S;
+  memset(&S, 0, sizeof(S));
+  LaunchInfo li{};
+  li.seq = seq;
+  S.nrings = 0;
+  unsigned int exit_target = 0;
+  for (size_t i = 0; i < rings.size(); ++i) {
+    LaunchParams& p = S.ring[S.nrings];
+    RingInfo& ri = li.ring[S.nrings];
+    r2_result_t e = prep_ring(c, rings[i], dt, seq, p, ri);
+    if (e != R2_SUCCESS) return e;
+    if (p.nlocal == 0) continue;                       // none of this process's ranks is on the ring
+    S.nctas[S.nrings] = p.nlocal * p.K * p.W;
+    exit_target += (unsigned)p.nlocal;
+    S.nrings++;
+  }
+  li.nrings = S.nrings;
+  if (S.nrings == 0) return R2_SUCCESS;
+  int total = 0;
+  for (int i = 0; i < S.nrings; ++i) total += S.nctas[i];
+  if (total > c->max_coop) return R2_ERR_INVALID_ARG;
+  for (int i = 0; i < S.nrings; ++i) S.ring[i].exit_target = exit_target;
+
   // faults armed for this seq; REPAIRs take effect before it (stand-in for
   // re-probe); HEALs only repair the emulated fabric (found by re-probing)
   std::vector<std::pair<int, int>> repairs, heals;
@@ -626,19 +750,34 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
       (f.kind == R2_FAULT_REPAIR ? repairs : heals).push_back({f.src_rank, f.channel});
       continue;
     }
-    if (f.step >= steps || f.chunk >= g.m || f.step == local_step) continue;   // no such send: never fires
-    if (op == R2_OP_BROADCAST && f.step != ((f.src_rank - root) % c->n + c->n) % c->n) continue;
-    if (p.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
-    FaultDev& d = p.faults[p.nfaults++];
-    d.rank = f.src_rank;
-    d.channel = f.channel;
-    d.origin = f.origin_channel < 0 ? f.channel : f.origin_channel;
-    d.kind = f.kind;
-    d.t = f.step;
-    d.j = f.chunk;
-    d.b = f.byte_offset;
-    d.detect_delay_us = f.detect_delay_us;
-    d.poison = f.poison;
+    const int origin = f.origin_channel < 0 ? f.channel : f.origin_channel;
+    for (int i = 0; i < S.nrings; ++i) {
+      LaunchParams& p = S.ring[i];
+      const RingInfo& ri = li.ring[i];
+      const int ci = ri.local_of(f.channel), oi = ri.local_of(origin);
+      if (ci < 0 || oi < 0 || ri.pos_of(f.src_rank) < 0) continue;       // not this ring's connection
+      if (f.step >= p.steps || f.chunk >= p.m || f.step == p.local_step) continue;   // no such send: never fires
+      const int pos = ri.pos_of(f.src_rank);
+      const bool std_link = ri.order[(pos + 1) % ri.n] == (f.src_rank + 1) % c->n;
+      if (f.kind == R2_FAULT_LINK && !std_link) continue;      // reading R-10: no such link
+      if ((p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2) &&
+          f.step != ((pos - p.root) % p.n + p.n) % p.n)
+        continue;
+      if (p.nfaults >= R2_MAXF || li.nfaults >= R2_MAXF) return R2_ERR_INVALID_ARG;
+      FaultDev& d = p.faults[p.nfaults++];
+      d.rank = f.src_rank;
+      d.channel = f.channel;                          // global (matched against the CTA's global channel)
+      d.origin = oi;                                  // ring-local (geometry)
+      d.kind = f.kind;
+      d.t = f.step;
+      d.j = f.chunk;
+      d.b = f.byte_offset;
+      d.detect_delay_us = f.detect_delay_us;
+      d.poison = f.poison;
+      FaultDev& h = li.faults[li.nfaults++];          // the monitor's copy: global ids
+      h = d;
+      h.origin = origin;
+    }
   }
   {
     std::lock_guard<std::mutex> gl(c->mu);
@@ -650,8 +789,16 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     for (auto& rc : c->readmit_pending) r2_declare_conn_repaired(c, rc.first, rc.second, seq);
     c->readmit_pending.clear();
     if ((!repairs.empty() || readmit) && r2_push_health(c) != 0) return R2_ERR_CUDA;
-    for (int l = 0; l < c->nlocal; ++l)
-      if (!r2_conn_mask_at(c, c->first_rank + l, seq)) return R2_ERR_NO_BACKUP;   // known exhausted
+    // a ring connection with no healthy channel left: the chain is exhausted
+    for (int i = 0; i < S.nrings; ++i) {
+      const RingInfo& ri = li.ring[i];
+      for (int j = 0; j < S.ring[i].nlocal; ++j) {
+        const int r = c->first_rank + S.ring[i].part_l[j], to = ri.next_of(r);
+        bool any = false;
+        for (int k = 0; k < ri.K; ++k) any |= r2_conn_ok_to(c, r, to, ri.chans[k], seq);
+        if (!any) return R2_ERR_NO_BACKUP;
+      }
+    }
   }
   // the emulated fabric heals in stream order
   for (auto& h : heals) repairs.push_back(h);
@@ -661,28 +808,14 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
       CK(cudaMemsetAsync(me.ep_dead + rc.first * c->K + rc.second, 0, 4, (cudaStream_t)stream));
       CK(cudaMemsetAsync(me.link_dead + rc.first * c->K + rc.second, 0, 4, (cudaStream_t)stream));
     }
-
-  LaunchInfo li{};
-  li.seq = seq;
-  li.local_step = local_step;
-  li.ll = ll;
-  li.op = op;
-  li.root = root;
-  li.m = g.m;
-  li.steps = steps;
-  li.V = g.V;
-  li.slice = g.slice;
-  li.chunk = g.chunk;
-  li.nfaults = p.nfaults;
-  for (int i = 0; i < p.nfaults; ++i) li.faults[i] = p.faults[i];
   {
     std::lock_guard<std::mutex> gl(c->mu);
     c->launches[seq] = li;
     while (c->launches.size() > 64) c->launches.erase(c->launches.begin());
   }
   // bounded run-ahead: a full device launch queue would block the monitor's
-  // probe-kernel launches behind a spinning collective (deadlock until the
-  // watchdog), so at most kMaxInflight collectives are outstanding
+  // standalone service kernel behind a spinning collective, so at most
+  // kMaxInflight collectives are outstanding
   const uint64_t t_win0 = r2_debug >= 2 ? r2_now_ns() : 0;
   {
     const uint64_t t0 = r2_now_ns();
@@ -699,12 +832,12 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
     }
   }
   c->seq = seq;
-  c->last_protocol = ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
+  c->last_protocol = S.ring[0].ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
   const uint64_t t_pre = r2_debug >= 2 ? r2_now_ns() : 0;
   static uint64_t sum_win = 0;
   if (r2_debug >= 2) sum_win += t_pre - t_win0;
-  // worker CTAs + the service CTA (r2_kernels.cu service_main)
-  int rc = r2_launch_allreduce(p, c->nlocal * c->K * c->W + 1, c->threads, stream);
+  // worker CTAs of every ring + the service CTA (r2_kernels.cu service_main)
+  int rc = r2_launch_allreduce(S, c->threads, stream);
   if (r2_debug >= 2) {                       // host enqueue cost breakdown (diagnostics)
     static uint64_t n_calls = 0, sum_pre = 0, sum_launch = 0;
     const uint64_t t_post = r2_now_ns();
@@ -720,6 +853,135 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   return R2_SUCCESS;
 }
 
+// One standard ring collective (AllReduce, or the standalone ReduceScatter /
+// AllGather halves of SURVEY §8(f) f1, or Broadcast).  `count`: AllReduce
+// elements; RS recvcount; AG sendcount.
+static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                                void* stream, int root = 0) {
+  const int E = elem_bytes(dt);
+  if (c->n == 1) {
+    if (send != recv) CK(cudaMemcpyAsync(recv, send, count * E, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    c->last_stream = stream;
+    return R2_SUCCESS;
+  }
+  std::vector<RingSpec> rings{standard_ring(c, op, send, recv, count, root)};
+  return launch_rings(c, rings, dt, stream);
+}
+
+// ---------------------------------------------------------------- R²CCL-AllReduce
+// SURVEY §8(f) f2 (App. A; reading R-9) and the strategy
+// choice of f3 (reading R-11).
+struct R2ccPlan {
+  bool applies = false;
+  int f = -1;                                // the degraded rank
+  double X = 0, Y = 0;                       // lost bandwidth fraction, partial-AllReduce share
+  size_t NA = 0, NP = 0;                     // elements: global ring prefix / partial ring suffix
+  std::vector<int> A, P;                     // f's healthy / dead channels (global ids)
+};
+
+// App. A (g = 1 GPU per "server"): threshold n/(3n-2); above it
+// Y* = X + X(1-X) / (X + (n-2) n) (Step 1 with g = 1), else 0 (Step 3).
+double r2cc_partition(int n, double X) {
+  const double th = (double)n / (3.0 * n - 2.0);
+  if (X <= th) return 0.0;
+  return X + X * (1.0 - X) / (X + (double)(n - 2) * n);
+}
+
+R2ccPlan r2cc_plan(r2_comm* c, size_t count, r2_dtype_t dt, uint32_t q) {
+  R2ccPlan pl;
+  const int n = c->n, K = c->K;
+  if (n < 3 || c->cfg.allreduce_algo == R2_ALGO_RING || !c->lay.tailor) return pl;
+  std::lock_guard<std::mutex> g(c->mu);
+  for (int r = 0; r < n; ++r)
+    for (int k = 0; k < K; ++k) {
+      if (r2_link_dead_at(c, r, k, q)) return pl;          // a dead link: not the single-degraded-rank case
+      if (r2_ep_dead_at(c, r, k, q)) {
+        if (pl.f >= 0 && pl.f != r) return pl;             // two degraded ranks: Balance (f4 territory)
+        pl.f = r;
+      }
+    }
+  if (pl.f < 0) return pl;
+  double wd = 0, wt = 0;
+  for (int k = 0; k < K; ++k) {
+    wt += c->weights[k];
+    if (r2_ep_dead_at(c, pl.f, k, q)) {
+      wd += c->weights[k];
+      pl.P.push_back(k);
+    } else {
+      pl.A.push_back(k);
+    }
+  }
+  if (pl.A.empty()) return pl;                             // NO_BACKUP: left to the ring path
+  pl.X = wd / wt;
+  pl.Y = r2cc_partition(n, pl.X);
+  const size_t V = 16 / (size_t)elem_bytes(dt);
+  // N_P = floor(Y N / V) V (vector-aligned split, reading R-9), N_A = N - N_P
+  pl.NP = (size_t)floor(pl.Y * (double)count / (double)V) * V;
+  if (pl.NP > count) pl.NP = count / V * V;
+  pl.NA = count - pl.NP;
+  pl.applies = pl.Y > 0 && pl.NP > 0 && pl.NA > 0;
+  return pl;
+}
+
+// alpha-beta cost of the two algorithms on the degraded communicator (reading
+// R-11): the ring is throttled to (1-X) of the per-GPU rate at the degraded
+// rank; R²CCL-AllReduce pays max(T1, T2) + T3 (the paper's model
+// with B = beta) plus its extra ring steps and the second launch.
+bool r2cc_faster(const r2_comm* c, const R2ccPlan& pl, size_t count, r2_dtype_t dt) {
+  const int n = c->n;
+  const double S = (double)count * elem_bytes(dt);
+  const double B = std::max(c->cfg.beta_mbps, 1) / 1000.0;            // bytes per ns
+  const double a = c->cfg.alpha_simple_ns;
+  const double X = pl.X, Y = (double)pl.NP / (double)count;
+  const double t_ring = (2 * n - 2) * a + 2.0 * (n - 1) / n * S / ((1 - X) * B);
+  const double T1 = 2.0 * (n - 1) / n * (1 - Y) * S / ((1 - X) * B);
+  const double T2 = 2.0 * (n - 2) / (n - 1) * Y * S / (X * B);
+  const double T3 = Y * S / (X * B);
+  const double t_r2cc = (2 * n - 2) * a + std::max(T1, T2) + n * a + T3 + c->cfg.alpha_launch_ns;
+  return t_r2cc < t_ring;
+}
+
+// Stage 1 (one launch): global ring over [0, N_A) on f's healthy channels
+// concurrently with the partial ring over [N_A, N) among the n-1 healthy ranks
+// on f's dead channels.  Stage 2 (a second launch): the tailored broadcast of
+// [N_A, N) from f around the ring.
+r2_result_t r2cc_enqueue(r2_comm* c, const R2ccPlan& pl, const void* send, void* recv, size_t count, r2_dtype_t dt,
+                         void* stream) {
+  const size_t E = (size_t)elem_bytes(dt);
+  const size_t shiftb = pl.NA * E;
+  std::vector<RingSpec> st1;
+  RingSpec g = standard_ring(c, R2_OP_ALLREDUCE, send, recv, pl.NA, 0);
+  g.chans = pl.A;
+  g.allow_ll = false;
+  g.row_elems = count;
+  st1.push_back(g);
+  RingSpec pr = standard_ring(c, R2_OP_ALLREDUCE, (const char*)send + shiftb, (char*)recv + shiftb, pl.NP, 0);
+  pr.order.erase(std::find(pr.order.begin(), pr.order.end(), pl.f));
+  pr.chans = pl.P;
+  pr.region = 1;
+  pr.peer_recv_off = shiftb;
+  pr.allow_ll = false;
+  pr.row_elems = count;
+  st1.push_back(pr);
+  r2_result_t e = launch_rings(c, st1, dt, stream);
+  if (e != R2_SUCCESS) return e;
+  std::vector<RingSpec> st2{standard_ring(c, R2_OP_R2CC_STAGE2, (const char*)send + shiftb, (char*)recv + shiftb,
+                                          pl.NP, pl.f)};
+  st2[0].row_elems = count;
+  st2[0].allow_ll = false;
+  e = launch_rings(c, st2, dt, stream);
+  if (e != R2_SUCCESS) return e;
+  std::lock_guard<std::mutex> gl(c->mu);
+  c->last_r2cc.seq = c->seq;
+  c->last_r2cc.f = pl.f;
+  c->last_r2cc.X = pl.X;
+  c->last_r2cc.Y = pl.Y;
+  c->last_r2cc.NA = pl.NA;
+  c->last_r2cc.NP = pl.NP;
+  c->n_r2cc++;
+  return R2_SUCCESS;
+}
+
 extern "C" r2_result_t r2_allreduce(r2_comm_t c, const void* send, void* recv, size_t count, r2_dtype_t dt,
                                     void* stream) {
   if (!c) return R2_ERR_INVALID_ARG;
@@ -730,6 +992,12 @@ extern "C" r2_result_t r2_allreduce(r2_comm_t c, const void* send, void* recv, s
   if (!send || !recv || ((uintptr_t)send & 15) || ((uintptr_t)recv & 15)) return R2_ERR_INVALID_ARG;
   if (count * (size_t)elem_bytes(dt) > c->cfg.max_bytes) return R2_ERR_INVALID_ARG;
   if (cudaSetDevice(c->dev) != cudaSuccess) return R2_ERR_CUDA;
+  if (c->n > 1 && c->cfg.allreduce_algo != R2_ALGO_RING) {
+    // the planner reads the health records of the next seq
+    const R2ccPlan pl = r2cc_plan(c, count, dt, (uint32_t)c->seq + 1);
+    if (pl.applies && (c->cfg.allreduce_algo == R2_ALGO_R2CC || r2cc_faster(c, pl, count, dt)))
+      return r2cc_enqueue(c, pl, send, recv, count, dt, stream);
+  }
   return enqueue_coll(c, R2_OP_ALLREDUCE, send, recv, count, dt, stream);
 }
 
@@ -950,6 +1218,13 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->n_readmits = c->n_readmits;
     out->n_reprobes = c->n_reprobes;
     out->n_service_kernels = c->n_svc_kicks;
+    out->n_r2cc = c->n_r2cc;
+    out->r2cc_rank = c->last_r2cc.f;
+    out->r2cc_X = c->last_r2cc.X;
+    out->r2cc_Y = c->last_r2cc.Y;
+    out->r2cc_NA = c->last_r2cc.NA;
+    out->r2cc_NP = c->last_r2cc.NP;
+    out->r2cc_seq = c->last_r2cc.seq;
     const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {

@@ -48,15 +48,41 @@ struct Reg {
   std::vector<void*> opened;                 // IPC bases opened for this reg (to close)
 };
 
-struct LaunchInfo {                          // what the monitor needs about a seq
-  uint32_t seq;
+struct RingInfo {                            // one ring of a launch (r2_internal.h LaunchParams)
+  int op, root;                              // r2_op_t; chain root (ring position)
   int local_step;                            // LOCAL step (own completion words) or -1
   bool ll;                                   // LL protocol
-  int op, root;                              // r2_op_t; Broadcast root
   int m, steps, V;
   unsigned long long slice, chunk;
+  int n, K, region;                          // positions, channels, region set (0 / 1)
+  int order[R2_MAXR];                        // global rank at ring position
+  int chans[R2_MAXK];                        // global channel of ring-local channel
+  uint32_t chan_mask;                        // global channels of this ring
+  int pos_of(int r) const {
+    for (int i = 0; i < n; ++i)
+      if (order[i] == r) return i;
+    return -1;
+  }
+  int next_of(int r) const { const int p = pos_of(r); return p < 0 ? -1 : order[(p + 1) % n]; }
+  int local_of(int cg) const {
+    for (int i = 0; i < K; ++i)
+      if (chans[i] == cg) return i;
+    return -1;
+  }
+};
+
+struct LaunchInfo {                          // what the monitor needs about a seq
+  uint32_t seq;
+  int nrings;
+  RingInfo ring[R2_MAXRINGS];
   int nfaults;
-  FaultDev faults[R2_MAXF];
+  FaultDev faults[R2_MAXF];                  // global rank / channel / origin channel
+  // the ring carrying global channel cg (nullptr: none)
+  const RingInfo* ring_of(int cg) const {
+    for (int i = 0; i < nrings; ++i)
+      if (ring[i].chan_mask >> cg & 1u) return &ring[i];
+    return nullptr;
+  }
 };
 
 struct Round {                               // one triangulation round
@@ -113,6 +139,8 @@ struct r2_comm {
   int K = 8, W = 4, threads = 512;
   int trace = 0;                             // R2_TRACE=1: record the device timeline (r2_trace)
   int last_protocol = 0;                     // r2_protocol_t of the last enqueued collective
+  struct { uint64_t seq; int f; double X, Y; size_t NA, NP; } last_r2cc{0, -1, 0, 0, 0, 0};   // (mu)
+  int n_r2cc = 0;                                                                        // (mu)
   // re-probing of dead connections ("periodically reprobes to detect
   // component recovery ... adapting probe frequency")
   struct Reprobe { int r, ch; uint64_t next_ns, interval_ns; uint32_t round_id; };
@@ -129,8 +157,13 @@ struct r2_comm {
   // per local rank
   std::vector<char*> arena;                  // own arenas (device)
   std::vector<Ctrl*> ctrl_host, ctrl_dev;
-  std::vector<RankPtrs> peers_host;          // [nlocal][n]
+  std::vector<RankPtrs> peers_host;          // [nlocal][n]  ring-0 region set
   RankPtrs* peers_dev = nullptr;
+  std::vector<RankPtrs> peers_host1;         // [nlocal][n]  ring-1 region set (R²CCL-AllReduce partial ring)
+  RankPtrs* peers_dev1 = nullptr;
+  const RankPtrs& rp(int region, int l, int q) const {
+    return (region ? peers_host1 : peers_host)[(size_t)l * n + q];
+  }
   std::vector<void*> peer_arena_opened;      // real mode: IPC-opened peer arenas
   unsigned long long* regtab_dev = nullptr;  // [R2_MAX_REGS][n]
   std::vector<unsigned long long> regtab_host;
@@ -251,6 +284,7 @@ uint64_t r2_now_ns();
 // r2_hostlogic.cpp (internal helpers; health calls need comm->mu held)
 int r2_first_healthy_in_chain(int origin, uint32_t mask, int K);
 bool r2_conn_ok_at(const r2_comm* comm, int r, int c, uint32_t q);     // connection r->r+1 on c, seq q
+bool r2_conn_ok_to(const r2_comm* comm, int r, int to, int c, uint32_t q);   // connection r->to (reading R-10)
 uint32_t r2_conn_mask_at(const r2_comm* comm, int r, uint32_t q);
 bool r2_ep_dead_at(const r2_comm* comm, int r, int c, uint32_t q);
 bool r2_link_dead_at(const r2_comm* comm, int r, int c, uint32_t q);

@@ -74,33 +74,35 @@ extern "C" r2_result_t r2_geometry_op(r2_op_t op, uint64_t count, r2_dtype_t dt,
                                       size_t chunk_bytes, r2_geometry_t* g) {
   if (!g || n < 1 || K < 1 || W < 1 || chunk_bytes < 16 || chunk_bytes % 16) return R2_ERR_INVALID_ARG;
   if (dt != R2_INT32 && dt != R2_FLOAT32 && dt != R2_BFLOAT16) return R2_ERR_INVALID_ARG;
-  if (op != R2_OP_ALLREDUCE && op != R2_OP_REDUCE_SCATTER && op != R2_OP_ALL_GATHER && op != R2_OP_BROADCAST)
+  if (op != R2_OP_ALLREDUCE && op != R2_OP_REDUCE_SCATTER && op != R2_OP_ALL_GATHER && op != R2_OP_BROADCAST &&
+      op != R2_OP_R2CC_STAGE2)
     return R2_ERR_INVALID_ARG;
+  const bool chain = op == R2_OP_BROADCAST || op == R2_OP_R2CC_STAGE2;   // one shard: the whole buffer
   const int E = elem_bytes_of(dt), V = 16 / E;
   const uint64_t Nmin = count ? count : 1;
   uint64_t Np_cap;
   if (op == R2_OP_ALLREDUCE) {
     const uint64_t q = (uint64_t)n * K * V;
     Np_cap = (Nmin + q - 1) / q * q;
-  } else if (op == R2_OP_BROADCAST) {
+  } else if (chain) {
     const uint64_t q = (uint64_t)K * V;              // one shard: the whole buffer
     Np_cap = (Nmin + q - 1) / q * q;
   } else {
     const uint64_t q = (uint64_t)K * V;              // each shard padded for the channel split
     Np_cap = (uint64_t)n * ((Nmin + q - 1) / q * q);
   }
-  const uint64_t slice = Np_cap / ((uint64_t)(op == R2_OP_BROADCAST ? 1 : n) * K);
+  const uint64_t slice = Np_cap / ((uint64_t)(chain ? 1 : n) * K);
   const uint64_t slice_bytes = slice * E;
   uint64_t per_worker = ((slice_bytes + W - 1) / W + 15) / 16 * 16;
   // a Broadcast chain pipelines per chunk (fill = (n-2) chunk hops): 128 KiB cap (reading R-8)
-  const uint64_t cap = op == R2_OP_BROADCAST && chunk_bytes > (128u << 10) ? (128u << 10) : chunk_bytes;
+  const uint64_t cap = chain && chunk_bytes > (128u << 10) ? (128u << 10) : chunk_bytes;
   uint64_t chunkb = cap < per_worker ? cap : per_worker;
   if (chunkb < 16) chunkb = 16;
   memset(g, 0, sizeof(*g));
-  g->N = (op == R2_OP_ALLREDUCE || op == R2_OP_BROADCAST) ? count : (uint64_t)n * count;
+  g->N = (op == R2_OP_ALLREDUCE || chain) ? count : (uint64_t)n * count;
   g->Np = count ? Np_cap : 0;
-  g->shard = op == R2_OP_BROADCAST ? g->Np : g->Np / n;
-  g->stride = (op == R2_OP_ALLREDUCE || op == R2_OP_BROADCAST) ? g->shard : count;
+  g->shard = chain ? g->Np : g->Np / n;
+  g->stride = (op == R2_OP_ALLREDUCE || chain) ? g->shard : count;
   g->t0 = op == R2_OP_ALL_GATHER ? n - 1 : 0;
   g->local_step = op == R2_OP_REDUCE_SCATTER ? n - 1 : -1;
   g->slice = count ? slice : 0;
@@ -110,7 +112,11 @@ extern "C" r2_result_t r2_geometry_op(r2_op_t op, uint64_t count, r2_dtype_t dt,
   g->W = W;
   g->V = V;
   g->m = count ? (int)((g->slice + g->chunk - 1) / g->chunk) : 0;
-  g->steps = op == R2_OP_ALLREDUCE ? 2 * n - 2 : (op == R2_OP_REDUCE_SCATTER ? n : n - 1);   // AG, BCAST: n-1
+  // AG, BCAST: n-1; R²CCL stage 2: n (the chain returns to the degraded rank, reading R-9)
+  g->steps = op == R2_OP_ALLREDUCE ? 2 * n - 2
+             : op == R2_OP_REDUCE_SCATTER ? n
+             : op == R2_OP_R2CC_STAGE2 ? n
+                                       : n - 1;
   return R2_SUCCESS;
 }
 
@@ -140,6 +146,13 @@ bool r2_link_dead_at(const r2_comm* c, int r, int k, uint32_t q) {
 bool r2_conn_ok_at(const r2_comm* c, int r, int k, uint32_t q) {
   const int r1 = (r + 1) % c->n;
   return !r2_ep_dead_at(c, r, k, q) && !r2_ep_dead_at(c, r1, k, q) && !r2_link_dead_at(c, r, k, q);
+}
+
+// Reading R-10: a LINK record is the standard ring's link r -> r+1; any other
+// pair of ranks (a re-ranked or partial ring) is dead only with an endpoint.
+bool r2_conn_ok_to(const r2_comm* c, int r, int to, int k, uint32_t q) {
+  if (to == (r + 1) % c->n) return r2_conn_ok_at(c, r, k, q);
+  return !r2_ep_dead_at(c, r, k, q) && !r2_ep_dead_at(c, to, k, q);
 }
 
 uint32_t r2_conn_mask_at(const r2_comm* c, int r, uint32_t q) {

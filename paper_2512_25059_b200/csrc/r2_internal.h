@@ -24,6 +24,8 @@
 #define R2_MAXF 8
 #define R2_MAX_REGS 64
 #define R2_MAX_CTAS_PER_RANK (R2_MAXK * R2_MAXW)
+#define R2_MAXR 64          // ranks of a communicator (R2_MAX_LOCAL * 4)
+#define R2_MAXRINGS 2       // rings of one launch (R²CCL-AllReduce stage 1: global + partial)
 
 enum { R2D_INT32 = 0, R2D_FLOAT32 = 1, R2D_BF16 = 2 };
 
@@ -69,7 +71,12 @@ struct DevCtrl {
   PlanEntry entries[R2_MAXK];
 };
 
-struct RankPtrs {            // one rank's arena as seen from some process
+// One rank's arena as seen from some process.  A launch runs up to two rings
+// (r2_internal.h LaunchSet); each ring has its own table whose per-ring
+// regions (scratch, ll, flags, counters, misc, stage) are disjoint, while the
+// per-rank state (fabric, alert, mailbox, desc, dctrl, health, abort word,
+// byte counters, tailored-broadcast buffer) is the same memory in both.
+struct RankPtrs {
   char* scratch;
   char* ll;                  // LL line slots [2 parities][2n-2 steps][ll_slot_bytes]
   unsigned int* flags;
@@ -83,6 +90,9 @@ struct RankPtrs {            // one rank's arena as seen from some process
   char* stage;
   DevCtrl* dctrl;            // plan/stop/abort mirror polled by the CTAs
   unsigned int* health;      // [4][n*K] host health records: ep dead/repair seq, link dead/repair seq
+  unsigned int* abort;       // per-rank abort word (= seq: a CTA of this rank timed out; ring-0 misc)
+  unsigned long long* bytes; // [K] bytes pushed per global channel (ring-0 misc)
+  char* tailor;              // R²CCL-AllReduce stage 2: the degraded rank's contribution lands here
 };
 
 // Health records are seq-indexed so that collectives enqueued ahead of a
@@ -101,6 +111,10 @@ inline __host__ __device__ bool r2_dead_at(unsigned int dseq, unsigned int rseq,
 
 struct ArenaLayout {
   size_t scratch, ll, flags, counters, ep_dead, link_dead, alert, mailbox, desc, misc, stage, dctrl, health, total;
+  // ring 1 (R²CCL-AllReduce's partial ring over n-1 ranks) and stage 2's buffer
+  size_t scratch1, flags1, counters1, misc1, stage1, tailor;
+  size_t slot1_bytes;         // one ring-1 scratch slot (>= max_bytes / (n-1))
+  size_t tailor_bytes;        // stage-2 buffer (>= max_bytes)
   size_t slot_bytes;          // one RS scratch slot (>= max shard bytes)
   size_t ll_slot_bytes;       // one LL slot (2 x the largest LL shard)
   int m_cap;
@@ -175,9 +189,23 @@ struct FaultDev {
   unsigned long long b;
 };
 
+// One ring of a launch.  Positions 0..n-1 of the ring hold global ranks
+// ring[pos] (the standard ring: ring[pos] = pos); the ring runs on K of the
+// communicator's Kg channels, ring-local channel ci being global channel
+// chan[ci].  Geometry (shards, slices, flags, plan entries in the kernel) is in
+// ring positions / ring-local channels; fabric state, health records, fault
+// table, control block and byte counters are in global ranks / channels.
 struct LaunchParams {
   unsigned int seq;
-  int n, K, W, m, steps, nlocal, first_rank;
+  int n, K, W, m, steps, nlocal, first_rank;   // nlocal: participating local ranks of this ring
+  int ng, Kg;                            // communicator ranks / channels
+  int ring_id;                           // 0 / 1: which region set (RankPtrs table)
+  int ring[R2_MAXR];                     // global rank at ring position
+  int chan[R2_MAXK];                     // global channel of ring-local channel
+  int part_l[R2_MAXL];                   // process-local index of participant i (sim mode: its global rank)
+  unsigned long long peer_recv_off;      // bytes added to a downstream rank's registered recv (ring region)
+  unsigned int* grid_exited;             // local rank 0's ring-0 misc: (ring, rank) pairs done
+  unsigned int exit_target;              // (ring, local rank) pairs of the whole launch
   int dtype, elem_bytes, V, inplace, strategy, sim;
   int op;                                // r2_op_t
   int t0;                                // AllReduce step of op-step 0 (AllGather: n-1)
@@ -207,6 +235,12 @@ struct LaunchParams {
   SvcBlock* svc;                         // device alias of the host-mapped service ring
 };
 
+struct LaunchSet {                       // the kernel's parameter: rings + service CTA
+  int nrings;
+  int nctas[R2_MAXRINGS];                // worker CTAs of each ring (grid = sum + 1 service CTA)
+  LaunchParams ring[R2_MAXRINGS];
+};
+
 struct ProbeParams {
   unsigned int* target_mailbox;          // &mailbox[prober][channel] in target arena
   const unsigned int* ep_dead;           // prober's replicated fabric state
@@ -222,7 +256,7 @@ struct ProbeParams {
 #ifdef __cplusplus
 extern "C++" {
 #endif
-int r2_launch_allreduce(const LaunchParams& p, int nctas, int threads, void* stream);
+int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream);
 int r2_launch_probe(const ProbeParams& p, void* stream);
 int r2_kernel_smem_bytes();
 int r2_max_coop_ctas(int threads);

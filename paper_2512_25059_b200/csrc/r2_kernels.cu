@@ -75,14 +75,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // rank only, plain stores (one lane's undisturbed timeline)
 #define TRACE_MIN(k, i)                                                                  \
   do {                                                                                   \
-    if ((k).p->trace == 1) atomicMin(&(k).me.misc->trace[(i)], gtimer());                \
-    else if ((k).p->trace == 2 && (k).cta_in_rank == 0 && (k).me.misc->trace[(i)] == ~0ull) \
-      (k).me.misc->trace[(i)] = gtimer();                                                \
+    if ((k).p->trace == 1) atomicMin(&(k).me->misc->trace[(i)], gtimer());                \
+    else if ((k).p->trace == 2 && (k).cta_in_rank == 0 && (k).me->misc->trace[(i)] == ~0ull) \
+      (k).me->misc->trace[(i)] = gtimer();                                                \
   } while (0)
 #define TRACE_MAX(k, i)                                                                  \
   do {                                                                                   \
-    if ((k).p->trace == 1) atomicMax(&(k).me.misc->trace[(i)], gtimer());                \
-    else if ((k).p->trace == 2 && (k).cta_in_rank == 0) (k).me.misc->trace[(i)] = gtimer(); \
+    if ((k).p->trace == 1) atomicMax(&(k).me->misc->trace[(i)], gtimer());                \
+    else if ((k).p->trace == 2 && (k).cta_in_rank == 0) (k).me->misc->trace[(i)] = gtimer(); \
   } while (0)
 __device__ __forceinline__ uint4 ld_cg(const void* p) {
   uint4 v;
@@ -239,7 +239,11 @@ struct Shared {
 
 struct Cta {
   const LaunchParams* p;
-  int l, r, r1, c, w, tid, nthr, cta_in_rank;
+  // l: process-local rank index (send/recv/ctrl/peers rows); r, r1: global
+  // ranks of this CTA and of its ring successor; pos: ring position (shard
+  // arithmetic); c: ring-local channel (geometry, flags, plan entries);
+  // cg: global channel (fabric, health, faults, control block, counters)
+  int l, r, r1, pos, c, cg, w, tid, nthr, cta_in_rank;
   unsigned int seq;
   int par;
   bool fault_channel;
@@ -247,7 +251,8 @@ struct Cta {
   unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
   bool all_healthy;         // conn_mask covers every channel (LL speculation allowed)
   int t_act;                // Broadcast: this rank's chain position (sends only at that step); else -1
-  RankPtrs me, nx;
+  const RankPtrs* me;        // this rank's / the ring successor's arena (global peers table)
+  const RankPtrs* nx;
   Ctrl* ctrl;
   unsigned int total_items;
   unsigned long long own_next_key;
@@ -432,12 +437,12 @@ __device__ int poll_control(const Cta& k, Shared& sh) {
   sh.t_prev_poll = sh.t_poll;
   sh.t_poll = gtimer();
   sh.npoll++;
-  if (ld_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq) == k.seq) return ST_ABORT;
+  if (ld_relaxed_sys(k.me->abort) == k.seq) return ST_ABORT;
   if (!sh.alerted) {
-    if (ld_relaxed_sys(k.me.alert) == k.seq) sh.alerted = 1;
+    if (ld_relaxed_sys(k.me->alert) == k.seq) sh.alerted = 1;
   }
   if (sh.alerted) {
-    DevCtrl* C = k.me.dctrl;
+    DevCtrl* C = k.me->dctrl;
     if (ld_relaxed_sys(&C->plan_seq) == k.seq) {
       const unsigned int ab = ld_relaxed_sys(&C->abort);
       if (ab) {
@@ -445,7 +450,7 @@ __device__ int poll_control(const Cta& k, Shared& sh) {
         sh.abort_code = ab;
         return ST_ABORT;
       }
-      if (ld_relaxed_sys(&C->stop_mask) >> k.c & 1u) {
+      if (ld_relaxed_sys(&C->stop_mask) >> k.cg & 1u) {
         sh.cause = STOP_HOST;
         return ST_STOP;
       }
@@ -458,8 +463,10 @@ __device__ int poll_control(const Cta& k, Shared& sh) {
 __device__ __forceinline__ bool conn_phys_dead(const Cta& k) {
   if (k.fault_channel) return false;   // deterministic stop rule applies instead
   const LaunchParams& p = *k.p;
-  return ld_relaxed_sys(k.me.ep_dead + k.r * p.K + k.c) | ld_relaxed_sys(k.me.ep_dead + k.r1 * p.K + k.c) |
-         ld_relaxed_sys(k.me.link_dead + k.r * p.K + k.c);
+  // a LINK is the standard ring's r -> r+1 (reading R-10): other pairs only die with an endpoint
+  const bool std_link = k.r1 == (k.r + 1) % p.ng;
+  return ld_relaxed_sys(k.me->ep_dead + k.r * p.Kg + k.cg) | ld_relaxed_sys(k.me->ep_dead + k.r1 * p.Kg + k.cg) |
+         (std_link ? ld_relaxed_sys(k.me->link_dead + k.r * p.Kg + k.cg) : 0u);
 }
 
 // watchdog: returns true when expired
@@ -478,11 +485,11 @@ __device__ bool try_recv_next(const Cta& k, Shared& sh) {
     sh.recv_next = p.recv[k.r1 - p.first_rank];
     return true;
   }
-  const volatile unsigned long long* d = k.nx.desc + k.par * 4;
+  const volatile unsigned long long* d = k.nx->desc + k.par * 4;
   if ((unsigned int)ld_relaxed_sys64(d) != k.seq) return false;
   fence_sys();
   unsigned long long reg = ld_relaxed_sys64(d + 1), off = ld_relaxed_sys64(d + 2);
-  sh.recv_next = (char*)(p.regtab[reg * p.n + k.r1] + off);
+  sh.recv_next = (char*)(p.regtab[reg * p.ng + k.r1] + off + p.peer_recv_off);
   return true;
 }
 
@@ -491,22 +498,22 @@ __device__ void fire_fault(const Cta& k, const FaultDev& f, int t, int o, int j)
   const LaunchParams& p = *k.p;
   unsigned long long t_fire = gtimer();
   fence_sys();
-  for (int q = 0; q < p.n; ++q) {
-    const RankPtrs& rp = p.peers[k.l * p.n + q];
-    if (f.kind == 2) st_relaxed_sys(rp.link_dead + k.r * p.K + k.c, 1u);        // LINK
-    else if (f.kind == 0) st_relaxed_sys(rp.ep_dead + k.r * p.K + k.c, 1u);     // LOCAL
-    else st_relaxed_sys(rp.ep_dead + k.r1 * p.K + k.c, 1u);                     // REMOTE
+  for (int q = 0; q < p.ng; ++q) {
+    const RankPtrs& rp = p.peers[k.l * p.ng + q];
+    if (f.kind == 2) st_relaxed_sys(rp.link_dead + k.r * p.Kg + k.cg, 1u);        // LINK
+    else if (f.kind == 0) st_relaxed_sys(rp.ep_dead + k.r * p.Kg + k.cg, 1u);     // LOCAL
+    else st_relaxed_sys(rp.ep_dead + k.r1 * p.Kg + k.cg, 1u);                     // REMOTE
   }
   fence_sys();
-  for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peers[k.l * p.n + q].alert, k.seq);
+  for (int q = 0; q < p.ng; ++q) st_relaxed_sys(p.peers[k.l * p.ng + q].alert, k.seq);
   fence_sys();
   // the sender's transport error surfaces after detect_delay_us (reading C-17)
   unsigned long long delay = (unsigned long long)f.detect_delay_us * 1000ull;
   while (gtimer() - t_fire < delay) {
   }
-  ErrRec& e = k.ctrl->err[k.c];
+  ErrRec& e = k.ctrl->err[k.cg];
   e.cause = STOP_FAULT_FIRED;
-  e.origin = (unsigned int)o;
+  e.origin = (unsigned int)p.chan[o];
   e.q = (unsigned int)(t * p.m + j);
   e.t_fire = t_fire;
   __threadfence_system();
@@ -522,7 +529,7 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
   bool last = true;
   const size_t fi = fidx(p, t, o, j);
   if (parts > 1) {
-    unsigned long long* ctr = k.me.counters + fi;
+    unsigned long long* ctr = k.me->counters + fi;
     const unsigned long long tag = (unsigned long long)(((k.seq & 0xFFFFFFu) << 8) | (epoch & 0xFFu)) << 32;
     unsigned long long old = *(volatile unsigned long long*)ctr, prev, nw;
     unsigned int cnt;
@@ -539,10 +546,10 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
   if (last) {
     // the completion word lives with its consumer: the receiver, or this rank
     // itself for a LOCAL item (ReduceScatter's final add, reading R-5)
-    st_relaxed_sys((local ? k.me.flags : k.nx.flags) + fi, k.seq);
-    atomicAdd(&k.me.misc->delivered, 1u);
+    st_relaxed_sys((local ? k.me->flags : k.nx->flags) + fi, k.seq);
+    atomicAdd(&k.me->misc->delivered, 1u);
   }
-  if (!local) atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)nbytes);
+  if (!local) atomicAdd(&k.me->bytes[k.cg], (unsigned long long)nbytes);
   if (!own && sh.first_adopt == 0) {
     // failover latency endpoint: first retransmitted chunk's flag
     sh.first_adopt = gtimer();
@@ -658,7 +665,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         // re-placed chunks: exactly those without a completion (reading C-7);
         // the origin's own lanes have quiesced and no part of an older plan
         // is in flight (freeze), so the receiver's flags are stable evidence
-        if (dyn && (int)(ld_relaxed_sys((t == p.local_step ? k.me.flags : k.nx.flags) + fidx(p, t, o, j)) - k.seq) >= 0)
+        if (dyn && (int)(ld_relaxed_sys((t == p.local_step ? k.me->flags : k.nx->flags) + fidx(p, t, o, j)) - k.seq) >= 0)
           continue;
         const unsigned int Vj =
             (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
@@ -703,7 +710,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   const unsigned long long key = keyof(it.t, it.o, it.j);
   for (int i = 0; i < p.nfaults; ++i) {
     const FaultDev& f = p.faults[i];
-    if ((int)f.rank != k.r || (int)f.channel != k.c || f.kind > 2) continue;
+    if ((int)f.rank != k.r || (int)f.channel != k.cg || f.kind > 2) continue;
     const unsigned long long kf = keyof(f.t, f.origin, f.j);
     // own-origin faults: deterministic "dead from k* on" for every lane of the
     // channel (reading R-1); adopted-chunk faults fire when (and if) carried
@@ -745,12 +752,13 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   // Once alerted, items wait for the completion word again (an adopted
   // residual must never queue behind a spinning item that needs it).
   const bool spec = p.ll && k.all_healthy && !sh.alerted && !sh.dynamic;
-  if (it.t > 0 && !spec && (int)(ld_relaxed_sys(k.me.flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0)
+  if (it.t > 0 && !spec && (int)(ld_relaxed_sys(k.me->flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0)
     return ST_NOTREADY;
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
-  if (p.peer_recv && (ta >= n - 1 || p.op == R2_OP_BROADCAST) && !local && !try_recv_next(k, sh))
+  if (p.peer_recv && (ta >= n - 1 || p.op == R2_OP_BROADCAST || (p.op == R2_OP_R2CC_STAGE2 && t > 0)) && !local &&
+      !try_recv_next(k, sh))
     return ST_NOTREADY;
   if (p.lane_ps_per_byte && !local) {
     // channel bandwidth model (r2ccl.h channel_gbps): a token bucket per lane
@@ -761,8 +769,8 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   }
 
   const int E = p.elem_bytes, V = p.V;
-  const int s_ = p.op == R2_OP_BROADCAST ? 0
-               : (ta <= n - 2) ? ((k.r - 1 - ta) % n + n) % n : ((k.r - (ta - n + 1)) % n + n) % n;
+  const bool chain = p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2;
+  const int s_ = chain ? 0 : (ta <= n - 2) ? ((k.pos - 1 - ta) % n + n) % n : ((k.pos - (ta - n + 1)) % n + n) % n;
   const unsigned long long off =
       (unsigned long long)it.o * p.slice + (unsigned long long)it.j * p.chunk + (unsigned long long)it.lo * V;
   const unsigned long long sbase = (unsigned long long)s_ * p.sstride;
@@ -778,7 +786,30 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   d.lim = sbase + p.slen < p.N ? sbase + p.slen : p.N;
   d.rs = ta <= n - 2;
   d.src_ll = 0;
-  if (p.op == R2_OP_BROADCAST) {
+  if (p.op == R2_OP_R2CC_STAGE2) {
+    // R²CCL-AllReduce's tailored broadcast (reading R-9): the degraded
+    // rank (position 0) sends its input into the next rank's tailor buffer;
+    // position 1 adds it to its partial result (IEEE addition commutes:
+    // hop_add(p, x_f) bit for bit), keeps the sum and sends it on; the chain
+    // forwards it back around to the degraded rank
+    d.rs = 0;
+    d.s_in = nullptr;
+    d.d_loc = nullptr;
+    d.loc_user = 1;
+    if (t == 0) {
+      d.src = p.send[k.l] + off * E;
+      d.d_rem = k.nx->tailor + off * E;
+      d.rs = 1;                                       // library memory: whole vectors
+    } else {
+      d.src = (const char*)p.recv[k.l] + off * E;
+      d.d_rem = sh.recv_next + off * E;
+      if (t == 1) {
+        d.s_in = k.me->tailor + off * E;
+        d.d_loc = p.recv[k.l] + off * E;
+      }
+    }
+    d.rem_user = !d.rs;
+  } else if (p.op == R2_OP_BROADCAST) {
     // chain: the root's input (t = 0), else what arrived here; into the next rank's recv
     d.rs = 0;
     d.src = (t == 0 ? p.send[k.l] : (const char*)p.recv[k.l]) + off * E;
@@ -794,37 +825,37 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     d.rs = 1;                                         // d_rem is library scratch
     if (ta <= n - 2) {                                // reduce-scatter hop
       d.src = p.send[k.l] + e0 * E;
-      d.s_in = t > 0 ? ll_slot(k.me, p, k.par, ta - 1) + lo : nullptr;
-      d.d_rem = ll_slot(k.nx, p, k.par, ta) + lo;
+      d.s_in = t > 0 ? ll_slot(*k.me, p, k.par, ta - 1) + lo : nullptr;
+      d.d_rem = ll_slot(*k.nx, p, k.par, ta) + lo;
       d.d_loc = nullptr;
       d.loc_user = 0;
     } else if (ta == n - 1 && p.op == R2_OP_ALLREDUCE) {   // final add + first all-gather send
       d.src = p.send[k.l] + e0 * E;
-      d.s_in = ll_slot(k.me, p, k.par, n - 2) + lo;
-      d.d_rem = ll_slot(k.nx, p, k.par, n - 1) + lo;
-      d.d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
+      d.s_in = ll_slot(*k.me, p, k.par, n - 2) + lo;
+      d.d_rem = ll_slot(*k.nx, p, k.par, n - 1) + lo;
+      d.d_loc = p.inplace ? (k.me->stage + off * E) : (p.recv[k.l] + e0 * E);
       d.loc_user = !p.inplace;
     } else if (ta == n - 1 && p.op == R2_OP_REDUCE_SCATTER) {   // final add into the own output
       d.src = p.send[k.l] + e0 * E;
-      d.s_in = ll_slot(k.me, p, k.par, n - 2) + lo;
+      d.s_in = ll_slot(*k.me, p, k.par, n - 2) + lo;
       d.d_rem = nullptr;
       d.d_loc = p.recv[k.l] + off * E;
       d.loc_user = 1;
     } else if (ta == n - 1) {                         // all-gather: the owner sends its own shard
       d.src = p.send[k.l] + off * E;
       d.s_in = nullptr;
-      d.d_rem = ll_slot(k.nx, p, k.par, n - 1) + lo;
+      d.d_rem = ll_slot(*k.nx, p, k.par, n - 1) + lo;
       d.d_loc = p.ag_inplace ? nullptr : (p.recv[k.l] + e0 * E);
       d.loc_user = 1;
     } else if (!local) {                              // all-gather forward: unpack + send on
-      d.src = ll_slot(k.me, p, k.par, ta - 1) + lo;
+      d.src = ll_slot(*k.me, p, k.par, ta - 1) + lo;
       d.src_ll = 1;
       d.s_in = nullptr;
-      d.d_rem = ll_slot(k.nx, p, k.par, ta) + lo;
+      d.d_rem = ll_slot(*k.nx, p, k.par, ta) + lo;
       d.d_loc = p.recv[k.l] + e0 * E;
       d.loc_user = 1;
     } else {                                          // the last all-gather step, unpacked locally
-      d.src = ll_slot(k.me, p, k.par, ta - 1) + lo;
+      d.src = ll_slot(*k.me, p, k.par, ta - 1) + lo;
       d.src_ll = 1;
       d.s_in = nullptr;
       d.d_rem = nullptr;
@@ -834,21 +865,21 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     d.rem_user = 0;
   } else if (ta <= n - 2) {                           // reduce-scatter hop
     d.src = p.send[k.l] + e0 * E;
-    d.s_in = t > 0 ? scratch_slot(k.me, p, k.par, t - 1) + off * E : nullptr;
-    d.d_rem = scratch_slot(k.nx, p, k.par, t) + off * E;
+    d.s_in = t > 0 ? scratch_slot(*k.me, p, k.par, t - 1) + off * E : nullptr;
+    d.d_rem = scratch_slot(*k.nx, p, k.par, t) + off * E;
     d.rem_user = 0;
     d.d_loc = nullptr;
     d.loc_user = 0;
   } else if (ta == n - 1 && p.op == R2_OP_ALLREDUCE) {   // final add + first all-gather send
     d.src = p.send[k.l] + e0 * E;
-    d.s_in = scratch_slot(k.me, p, k.par, n - 2) + off * E;
+    d.s_in = scratch_slot(*k.me, p, k.par, n - 2) + off * E;
     d.d_rem = sh.recv_next + e0 * E;
     d.rem_user = 1;
-    d.d_loc = p.inplace ? (k.me.stage + off * E) : (p.recv[k.l] + e0 * E);
+    d.d_loc = p.inplace ? (k.me->stage + off * E) : (p.recv[k.l] + e0 * E);
     d.loc_user = !p.inplace;
   } else if (ta == n - 1 && p.op == R2_OP_REDUCE_SCATTER) {   // final add into the own output (LOCAL)
     d.src = p.send[k.l] + e0 * E;
-    d.s_in = scratch_slot(k.me, p, k.par, n - 2) + off * E;
+    d.s_in = scratch_slot(*k.me, p, k.par, n - 2) + off * E;
     d.d_rem = nullptr;
     d.rem_user = 0;
     d.d_loc = p.recv[k.l] + off * E;
@@ -881,7 +912,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   m.own = it.own;
   m.fault = fire - 1;
   mbar_arrive(&sh.full[u]);
-  if (p.trace == 2 && k.cta_in_rank == 0 && sh.pub < 8) k.me.misc->trace[24 + sh.pub] = gtimer();  // publish i
+  if (p.trace == 2 && k.cta_in_rank == 0 && sh.pub < 8) k.me->misc->trace[24 + sh.pub] = gtimer();  // publish i
   sh.pub++;
   if (it.own) {
     k.own_next_key = key + 1;
@@ -892,20 +923,46 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   return ST_OK;
 }
 
+// Thread 0: the monitor's plan entries (global channel ids, both rings of a
+// launch) -> this ring's entries in ring-local channel ids (origins of other
+// rings dropped; masks and assignees translated).
+__device__ void load_entries(const Cta& k, Shared& sh, int nent) {
+  const LaunchParams& p = *k.p;
+  const volatile unsigned int* src = (const volatile unsigned int*)k.me->dctrl->entries;
+  int out = 0;
+  for (int e = 0; e < nent && e < R2_MAXK; ++e) {
+    const unsigned int og = ld_relaxed_sys(src + 4 * e + 0), mode = ld_relaxed_sys(src + 4 * e + 1);
+    const unsigned int ag = ld_relaxed_sys(src + 4 * e + 2), gmask = ld_relaxed_sys(src + 4 * e + 3);
+    int o = -1, a = 0;
+    unsigned int mask = 0;
+    for (int ci = 0; ci < p.K; ++ci) {
+      if ((unsigned int)p.chan[ci] == og) o = ci;
+      if ((unsigned int)p.chan[ci] == ag) a = ci;
+      if (gmask >> p.chan[ci] & 1u) mask |= 1u << ci;
+    }
+    if (o < 0) continue;
+    sh.ent[out].origin = (unsigned int)o;
+    sh.ent[out].mode = mode;
+    sh.ent[out].assignee = (unsigned int)a;
+    sh.ent[out].mask = mask;
+    ++out;
+  }
+  sh.nent = out;
+}
+
 // Control lane: apply a new plan epoch in place (no pipeline drain: chunks
 // already published have their inputs and complete on their own).  A freeze
 // is acknowledged once no adopted chunk of the old plan is in flight.
 __device__ void apply_plan(const Cta& k, Shared& sh) {
-  DevCtrl* C = k.me.dctrl;
+  DevCtrl* C = k.me->dctrl;
   const unsigned int e = ld_acquire_gpu(&C->epoch);
   sh.seen_epoch = e;
   sh.freeze = (int)ld_relaxed_sys(&C->freeze);
-  sh.nent = (int)ld_relaxed_sys(&C->nentries);
+  const int nent = (int)ld_relaxed_sys(&C->nentries);
+  sh.nent = 0;
   sh.first_adopt = 0;
   if (!sh.freeze) {
-    const int words = (int)(sizeof(PlanEntry) / 4);
-    for (int i = 0; i < sh.nent * words; ++i)
-      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)C->entries) + i);
+    load_entries(k, sh, nent);
     sh.dynamic = 1;
     k.ctrl->cta[k.cta_in_rank].t_apply = gtimer();
     k.ctrl->cta[k.cta_in_rank].t_prev_poll = sh.t_prev_poll;
@@ -991,13 +1048,13 @@ __device__ int control_run(Cta& k, Shared& sh) {
           complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes, m.local != 0);
           if (m.own && m.t < 28) TRACE_MAX(k, 4 + m.t);
         } else if (m.kind == META_FIRE) {
-          atomicAdd(&k.me.misc->bytes[k.c], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
+          atomicAdd(&k.me->bytes[k.cg], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
           fire_fault(k, p.faults[m.fault], m.t, m.o, m.j);
         }
       }
       if (p.trace == 2 && k.cta_in_rank == 0)
         for (unsigned int i = 0; i < nd; ++i)
-          if (sh.fin + i < 8) k.me.misc->trace[16 + sh.fin + i] = gtimer();   // retire i
+          if (sh.fin + i < 8) k.me->misc->trace[16 + sh.fin + i] = gtimer();   // retire i
       sh.fin += nd;
       progress = true;
     }
@@ -1008,9 +1065,8 @@ __device__ int control_run(Cta& k, Shared& sh) {
       ack_epoch = 0;
     }
     // 2b. an abort / timeout also releases data warps spinning on LL lines
-    if ((pending == ST_ABORT || pending == ST_TIMEOUT) && sh.fin != sh.pub &&
-        ld_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq) != k.seq)
-      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
+    if ((pending == ST_ABORT || pending == ST_TIMEOUT) && sh.fin != sh.pub && ld_relaxed_sys(k.me->abort) != k.seq)
+      st_relaxed_sys(k.me->abort, k.seq);
     // 3. done: everything published is retired -> END releases the data warps
     if ((!have || pending != ST_OK) && sh.fin == sh.pub && !ack_epoch) {
       const unsigned int u = sh.pub % NSLOT;
@@ -1058,7 +1114,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
           if (cur.t > 0) {
             const size_t fi = fidx(p, cur.t - 1, cur.o, cur.j);
             rec.wait_idx = (unsigned int)fi;
-            rec.wait_val = k.me.flags[fi];
+            rec.wait_val = k.me->flags[fi];
           } else {
             rec.wait_idx = 0x40000000u;
             rec.wait_val = 0;
@@ -1081,7 +1137,7 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     mbar_wait(&sh.full[u], ph);
     ++dcount;
     if (p.trace == 2 && k.cta_in_rank == 0 && k.tid == 32 && dcount <= 8)
-      k.me.misc->trace[40 + dcount - 1] = gtimer();   // data warps take item dcount-1
+      k.me->misc->trace[40 + dcount - 1] = gtimer();   // data warps take item dcount-1
     const Slot d = sh.slot[u];
     if (d.status == SLOT_END) {
       __syncwarp();
@@ -1090,7 +1146,7 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     }
     if (p.ll)
       move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
-                  d.lim, d.aligned != 0, k.seq, &k.me.misc->abort_seq);
+                  d.lim, d.aligned != 0, k.seq, k.me->abort);
     else
       move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
                d.aligned != 0);
@@ -1112,7 +1168,7 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     }
     __syncwarp();
     if (p.trace == 2 && k.cta_in_rank == 0 && k.tid == 32 && dcount <= 8)
-      k.me.misc->trace[48 + dcount - 1] = gtimer();   // warp 1 done with item dcount-1
+      k.me->misc->trace[48 + dcount - 1] = gtimer();   // warp 1 done with item dcount-1
     if (lane == 0) mbar_arrive(&sh.empty[u]);
   }
 }
@@ -1137,19 +1193,18 @@ __device__ void post_state(const Cta& k, const Shared& sh, unsigned int state, u
 // all threads: pull the dynamic plan from the control block
 __device__ void load_plan(Cta& k, Shared& sh) {
   if (k.tid == 0) {
-    DevCtrl* C = k.me.dctrl;
+    DevCtrl* C = k.me->dctrl;
     unsigned int e = ld_acquire_gpu(&C->epoch);
     sh.seen_epoch = e;
     sh.freeze = (int)ld_relaxed_sys(&C->freeze);
-    sh.nent = (int)ld_relaxed_sys(&C->nentries);
+    sh.flag = (int)ld_relaxed_sys(&C->nentries);
+    sh.nent = 0;
     sh.first_adopt = 0;
   }
   __syncthreads();
   if (!sh.freeze) {
-    const int words = (int)(sizeof(PlanEntry) / 4);
-    for (int i = k.tid; i < sh.nent * words; i += k.nthr)
-      ((unsigned int*)sh.ent)[i] = ld_relaxed_sys(((volatile unsigned int*)k.me.dctrl->entries) + i);
     if (k.tid == 0) {
+      load_entries(k, sh, sh.flag);
       sh.dynamic = 1;
       k.ctrl->cta[k.cta_in_rank].t_apply = gtimer();
       k.ctrl->cta[k.cta_in_rank].t_prev_poll = sh.t_prev_poll;
@@ -1177,7 +1232,7 @@ __device__ int drain(Cta& k, Shared& sh) {
       int st = poll_control(k, sh);
       int cand = 0;
       if (st == ST_OK) {
-        const unsigned int dl = ld_relaxed_sys((volatile unsigned int*)&k.me.misc->delivered);
+        const unsigned int dl = ld_relaxed_sys((volatile unsigned int*)&k.me->misc->delivered);
         cand = dl >= k.total_items;
         if (!cand) {
           if (watchdog(k, sh)) {
@@ -1204,8 +1259,10 @@ __device__ int drain(Cta& k, Shared& sh) {
     const int nf = p.K * p.m;
     // the root of a Broadcast receives nothing; under LL the last incoming step
     // is consumed by this rank's own unpack items (already delivered)
-    const int fs = p.op == R2_OP_BROADCAST ? k.t_act - 1 : (p.ll && p.local_step >= 0 ? -1 : p.fin_step);
-    const unsigned int* fin = k.me.flags + fidx(p, fs < 0 ? 0 : fs, 0, 0);
+    const int fs = p.op == R2_OP_BROADCAST      ? k.t_act - 1
+                   : p.op == R2_OP_R2CC_STAGE2 ? (k.t_act == 0 ? p.n - 1 : k.t_act - 1)
+                   : (p.ll && p.local_step >= 0 ? -1 : p.fin_step);
+    const unsigned int* fin = k.me->flags + fidx(p, fs < 0 ? 0 : fs, 0, 0);
     for (int i = k.tid; fs >= 0 && i < nf; i += k.nthr)
       if ((int)(ld_relaxed_sys(fin + i) - k.seq) < 0) ok = 0;
     if (__syncthreads_and(ok)) {
@@ -1235,21 +1292,21 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
   const unsigned long long npieces = (shard_vec + PIECE - 1) / PIECE;
   __threadfence();
   for (;;) {
-    if (k.tid == 0) sh.piece = atomicAdd(&k.me.misc->copy_next, 1u);
+    if (k.tid == 0) sh.piece = atomicAdd(&k.me->misc->copy_next, 1u);
     __syncthreads();
     const unsigned long long pc = sh.piece;
     __syncthreads();
     if (pc >= npieces) break;
     const unsigned long long v0 = pc * PIECE;
     const unsigned int nv = (unsigned int)min((unsigned long long)PIECE, shard_vec - v0);
-    const unsigned long long e0 = (unsigned long long)k.r * p.shard + v0 * p.V;
+    const unsigned long long e0 = (unsigned long long)k.pos * p.shard + v0 * p.V;
     if (e0 >= p.N) continue;
     for (unsigned int v = k.tid; v < nv; v += k.nthr) {
       long long ev = (long long)(e0 + (unsigned long long)v * p.V);
       long long left = (long long)p.N - ev;
       int valid = left <= 0 ? 0 : (left >= p.V ? p.V : (int)left);
       if (!valid) continue;
-      uint4 a = ld_cg(k.me.stage + (v0 + v) * 16);
+      uint4 a = ld_cg(k.me->stage + (v0 + v) * 16);
       st_user(p.recv[k.l] + (size_t)ev * p.elem_bytes, a, valid, p.elem_bytes);
     }
   }
@@ -1262,13 +1319,13 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
 __device__ void last_out(const Cta& k) {
   const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
   TRACE_MAX(k, 62);
-  if (atomicAdd(&k.me.misc->exited, 1u) == per_rank - 1) {
-    k.me.misc->delivered = 0;
-    k.me.misc->copy_next = 0;
+  if (atomicAdd(&k.me->misc->exited, 1u) == per_rank - 1) {
+    k.me->misc->delivered = 0;
+    k.me->misc->copy_next = 0;
     __threadfence();
-    atomicExch(&k.me.misc->exited, 0u);
+    atomicExch(&k.me->misc->exited, 0u);
     __threadfence();
-    atomicAdd(&k.p->peers[k.p->first_rank].misc->grid_exited, 1u);   // local rank 0's arena
+    atomicAdd(k.p->grid_exited, 1u);                  // one (ring, rank) pair done (service_main)
   }
 }
 
@@ -1289,7 +1346,7 @@ __device__ void cta_main(Cta& k, Shared& sh) {
     // every outgoing channel of this rank is dead: the chain is exhausted
     // before the collective starts -- abort, the monitor reports it
     if (k.tid == 0) {
-      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
+      st_relaxed_sys(k.me->abort, k.seq);
       k.ctrl->cta[k.cta_in_rank].cause = STOP_NOBACKUP;
       post_failure(k, R2_ERR_NO_BACKUP);
       k.ctrl->cta[k.cta_in_rank].ss = R2_SS(k.seq, CTA_EXITED);
@@ -1327,7 +1384,7 @@ __device__ void cta_main(Cta& k, Shared& sh) {
     exit_state = (st == ST_STOP) ? CTA_STOPPED : CTA_EXITED;
     if (st == ST_TIMEOUT) {
       // local abort: the rest of this rank stops waiting too
-      st_relaxed_sys((volatile unsigned int*)&k.me.misc->abort_seq, k.seq);
+      st_relaxed_sys(k.me->abort, k.seq);
     }
     if (st == ST_TIMEOUT || st == ST_ABORT)
       post_failure(k, st == ST_ABORT && sh.abort_code ? sh.abort_code : (unsigned int)R2_ERR_TIMEOUT);
@@ -1335,11 +1392,11 @@ __device__ void cta_main(Cta& k, Shared& sh) {
       // bilateral awareness starts at the detecting sender; the
       // surviving CTAs of every rank must start reading the control block
       const LaunchParams& p = *k.p;
-      for (int q = 0; q < p.n; ++q) st_relaxed_sys(p.peers[k.l * p.n + q].alert, k.seq);
-      ErrRec& e = k.ctrl->err[k.c];
+      for (int q = 0; q < p.ng; ++q) st_relaxed_sys(p.peers[k.l * p.ng + q].alert, k.seq);
+      ErrRec& e = k.ctrl->err[k.cg];
       if (e.seq != k.seq) {
         e.cause = STOP_DEATH;
-        e.origin = (unsigned int)k.c;
+        e.origin = (unsigned int)k.cg;
         e.q = 0;
         e.t_fire = gtimer();
         __threadfence_system();
@@ -1508,7 +1565,7 @@ __device__ void service_main(const LaunchParams& p) {
   __shared__ SvcShared ss;
   const unsigned int lane = threadIdx.x & 31u;
   SvcBlock* S = p.svc;
-  MiscDev* m0 = p.peers[p.first_rank].misc;
+  MiscDev* m0 = p.peers[p.first_rank].misc;             // local rank 0's ring-0 misc (svc lock / tail)
   if (lane == 0) {
     ss.nactive = 0;
     for (int i = 0; i < R2_SVC_MAXPROBES; ++i) ss.pr[i].active = 0;
@@ -1537,13 +1594,13 @@ __device__ void service_main(const LaunchParams& p) {
     if (ss.nactive) svc_probes(S, ss, lane);
     int out = 0;
     if (lane == 0)
-      out = ss.nactive == 0 && ld_relaxed_sys((const volatile unsigned int*)&m0->grid_exited) == (unsigned)p.nlocal;
+      out = ss.nactive == 0 && ld_relaxed_sys((const volatile unsigned int*)p.grid_exited) == p.exit_target;
     out = __shfl_sync(0xFFFFFFFFu, out, 0);
     if (out) break;
     __nanosleep(100);
   }
   if (lane == 0) {
-    m0->grid_exited = 0;                              // nobody else touches it in this launch
+    *p.grid_exited = 0;                               // nobody else touches it in this launch
     __threadfence();
     S->alive = R2_SS(p.seq, 0);
     for (int l = 0; l < p.nlocal; ++l) p.ctrl[l]->done_seq = p.seq;
@@ -1575,31 +1632,39 @@ __global__ void r2_service_kernel(SvcBlock* S, MiscDev* m0) {
   }
 }
 
-__global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_constant__ LaunchParams p) {
+// Worker CTA (participant i, ring-local channel ci, lane w) of ring RI; the
+// ring index is a template argument so that every parameter access is a
+// constant-bank load at a fixed offset (a run-time ring index made them
+// indexed and cost registers: spills in the data path).
+template <int RI>
+__device__ __forceinline__ void worker_main(const LaunchSet& S, unsigned int b) {
+  const LaunchParams& p = S.ring[RI];
   const int per_rank = p.K * p.W;
-  if (blockIdx.x == (unsigned)(p.nlocal * per_rank)) {   // the service CTA (last in the grid)
-    if (threadIdx.x < 32) service_main(p);
-    return;
-  }
   __shared__ Shared sh;
   Cta k;
   k.p = &p;
-  k.l = blockIdx.x / per_rank;
-  k.cta_in_rank = blockIdx.x % per_rank;
-  k.c = k.cta_in_rank / p.W;
-  k.w = k.cta_in_rank % p.W;
+  k.l = p.part_l[b / per_rank];
+  k.c = (int)(b % per_rank) / p.W;
+  k.w = (int)(b % per_rank) % p.W;
+  k.cg = p.chan[k.c];
+  k.cta_in_rank = k.cg * p.W + k.w;                      // control-block record: global channel
   k.r = p.first_rank + k.l;
-  k.r1 = (k.r + 1) % p.n;
+  k.pos = 0;
+  for (int q = 0; q < p.n; ++q)
+    if (p.ring[q] == k.r) k.pos = q;
+  k.r1 = p.ring[(k.pos + 1) % p.n];
   k.tid = threadIdx.x;
   k.nthr = blockDim.x;
   k.seq = p.seq;
   k.par = (int)(p.seq & 1u);
-  k.me = p.peers[k.l * p.n + k.r];
-  k.nx = p.peers[k.l * p.n + k.r1];
+  k.me = &p.peers[k.l * p.ng + k.r];
+  k.nx = &p.peers[k.l * p.ng + k.r1];
   k.ctrl = p.ctrl[k.l];
-  k.t_act = p.op == R2_OP_BROADCAST ? ((k.r - p.root) % p.n + p.n) % p.n : -1;
-  k.total_items = p.op == R2_OP_BROADCAST ? (k.t_act <= p.n - 2 ? (unsigned int)(p.K * p.m) : 0u)
-                                          : (unsigned int)(p.steps * p.K * p.m);
+  // chain collectives: this rank's position in the chain from the root
+  k.t_act = (p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2) ? ((k.pos - p.root) % p.n + p.n) % p.n : -1;
+  k.total_items = p.op == R2_OP_BROADCAST     ? (k.t_act <= p.n - 2 ? (unsigned int)(p.K * p.m) : 0u)
+                  : p.op == R2_OP_R2CC_STAGE2 ? (unsigned int)(p.K * p.m)
+                                              : (unsigned int)(p.steps * p.K * p.m);
   if (k.tid == 0) TRACE_MIN(k, 0);
   // plan-time placement: read the host's health records for this seq;
   // every CTA of the rank computes the same mask (records for this seq are
@@ -1607,16 +1672,18 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   {
     // all records loaded up front (independent loads in flight together; the
     // short-circuit form issued them one dependent round trip at a time)
-    const unsigned int nk = (unsigned int)(p.n * p.K);
-    const unsigned int* h = k.me.health;
+    const unsigned int nk = (unsigned int)(p.ng * p.Kg);
+    const unsigned int* h = k.me->health;
+    const bool std_link = k.r1 == (k.r + 1) % p.ng;       // reading R-10
     unsigned int mask = 0;
 #pragma unroll 4
     for (int c = 0; c < p.K; ++c) {
-      const unsigned int a = k.r * p.K + c, b = k.r1 * p.K + c;
+      const unsigned int a = k.r * p.Kg + p.chan[c], b2 = k.r1 * p.Kg + p.chan[c];
       const unsigned int ead = h[R2_H_EP_DEAD * nk + a], ear = h[R2_H_EP_REP * nk + a];
-      const unsigned int ebd = h[R2_H_EP_DEAD * nk + b], ebr = h[R2_H_EP_REP * nk + b];
+      const unsigned int ebd = h[R2_H_EP_DEAD * nk + b2], ebr = h[R2_H_EP_REP * nk + b2];
       const unsigned int lad = h[R2_H_LINK_DEAD * nk + a], lar = h[R2_H_LINK_REP * nk + a];
-      const bool dead = r2_dead_at(ead, ear, k.seq) | r2_dead_at(ebd, ebr, k.seq) | r2_dead_at(lad, lar, k.seq);
+      const bool dead = r2_dead_at(ead, ear, k.seq) | r2_dead_at(ebd, ebr, k.seq) |
+                        (std_link && r2_dead_at(lad, lar, k.seq));
       if (!dead) mask |= 1u << c;
     }
     k.conn_mask = mask;
@@ -1626,7 +1693,7 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   k.own_next_key = 0;
   k.fault_channel = false;
   for (int i = 0; i < p.nfaults; ++i)
-    if ((int)p.faults[i].rank == k.r && (int)p.faults[i].channel == k.c && p.faults[i].kind <= 2 &&
+    if ((int)p.faults[i].rank == k.r && (int)p.faults[i].channel == k.cg && p.faults[i].kind <= 2 &&
         (int)p.faults[i].origin == k.c)
       k.fault_channel = true;
   if (k.tid == 0) {
@@ -1655,9 +1722,9 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];
     rec.cause = 0;
     rec.ss = R2_SS(k.seq, CTA_RUNNING);
-    if (!p.sim && p.peer_recv && k.cta_in_rank == 0) {
-      // publish our recv (registration id, offset) for the upstream rank
-      volatile unsigned long long* d = k.me.desc + k.par * 4;
+    if (!p.sim && p.peer_recv && p.ring_id == 0 && k.c == 0 && k.w == 0) {
+      // publish our recv (registration id, offset) for the upstream rank(s)
+      volatile unsigned long long* d = k.me->desc + k.par * 4;
       d[1] = (unsigned long long)p.recv_reg[k.l];
       d[2] = p.recv_off[k.l];
       fence_sys();
@@ -1669,6 +1736,22 @@ __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_const
   if (p.dtype == R2D_INT32) cta_main<R2D_INT32>(k, sh);
   else if (p.dtype == R2D_FLOAT32) cta_main<R2D_FLOAT32>(k, sh);
   else cta_main<R2D_BF16>(k, sh);
+}
+
+// Grid: ring 0's worker CTAs, ring 1's (R²CCL-AllReduce stage 1 only), then
+// the service CTA.
+__global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_constant__ LaunchSet S) {
+  unsigned int b = blockIdx.x;
+  if (b < (unsigned)S.nctas[0]) {
+    worker_main<0>(S, b);
+    return;
+  }
+  b -= (unsigned)S.nctas[0];
+  if (S.nrings > 1 && b < (unsigned)S.nctas[1]) {
+    worker_main<1>(S, b);
+    return;
+  }
+  if (threadIdx.x < 32) service_main(S.ring[0]);        // the service CTA (last in the grid)
 }
 
 // ------------------------------------------------------------ probe kernel
@@ -1707,8 +1790,10 @@ __global__ void r2_probe_kernel(const __grid_constant__ ProbeParams p) {
 
 }  // namespace
 
-int r2_launch_allreduce(const LaunchParams& p, int nctas, int threads, void* stream) {
-  void* args[] = {(void*)&p};
+int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream) {
+  void* args[] = {(void*)&s};
+  int nctas = 1;                                         // + the service CTA
+  for (int i = 0; i < s.nrings; ++i) nctas += s.nctas[i];
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
                                               (cudaStream_t)stream);
   return (int)e;

@@ -296,8 +296,11 @@ void on_verdict(r2_comm* c, const Msg& m) {
   for (int l = 0; l < c->nlocal; ++l) {
     const int r = c->first_rank + l;
     for (int k = 0; k < K; ++k) {
-      if (!r2_conn_ok_at(c, r, k, m.seq)) continue;       // statically adopted already
-      if (r2_conn_ok_at(c, r, k, m.seq + 1)) continue;   // not condemned
+      const RingInfo* R = li->ring_of(k);
+      if (!R || R->pos_of(r) < 0) continue;                // no connection of r on k in this launch
+      const int to = R->next_of(r);
+      if (!r2_conn_ok_to(c, r, to, k, m.seq)) continue;    // statically adopted already
+      if (r2_conn_ok_to(c, r, to, k, m.seq + 1)) continue;   // not condemned
       auto key = std::make_pair(m.seq, l * K + k);
       if (c->planned.count(key)) continue;
       // a connection this rank detected itself waits for its own round
@@ -419,17 +422,21 @@ bool scan_device_records(r2_comm* c) {
       R2LOG("detect seq %u rank %d ch%d cause %u origin %u q %u (fire -> host detect %.1f us)", s, r, k, e.cause,
             e.origin, e.q, ((double)(long long)r2_now_ns() - ((double)(long long)e.t_fire - (double)c->clk_offset)) / 1e3);
       const uint64_t now = r2_now_ns();
+      int peer = (r + 1) % c->n;                       // the connection's other endpoint
       {
         std::lock_guard<std::mutex> g(c->mu);
         // remember that this rank detected (seq, l, k) itself -> use own round
         c->planned[std::make_pair(s, -(l * K + k) - 1)] = 1;
+        const LaunchInfo* li = launch_of(c, s);
+        const RingInfo* R = li ? li->ring_of(k) : nullptr;
+        if (R && R->next_of(r) >= 0) peer = R->next_of(r);   // re-ranked / partial ring
       }
       // bilateral awareness
       Msg nm{};
       nm.type = MSG_NOTIFY;
       nm.seq = s;
       nm.a = r;
-      nm.b = (r + 1) % c->n;
+      nm.b = peer;
       nm.channel = k;
       nm.t_fire = e.t_fire;
       {
@@ -449,7 +456,7 @@ bool scan_device_records(r2_comm* c) {
         std::lock_guard<std::mutex> g(c->pmu);
         id = ((uint32_t)r << 24) | (++c->round_counter & 0xFFFFFF);
       }
-      start_round(c, id, s, r, (r + 1) % c->n, k);
+      start_round(c, id, s, r, peer, k);
       (void)now;
     }
     // watchdog expiries -> abort everywhere
@@ -532,8 +539,22 @@ bool freeze_acked(r2_comm* c, int l, uint32_t seq, uint32_t epoch) {
   return true;
 }
 
+// First healthy channel after global origin o in the ring's failover chain
+// (ring-local cyclic order, reading C-2); -1 if none.  *pos: chain position.
+int first_healthy_in_ring(const RingInfo& R, int o, uint32_t healthy, int* pos = nullptr) {
+  const int oi = R.local_of(o);
+  for (int d = 1; d < R.K; ++d) {
+    const int cg = R.chans[(oi + d) % R.K];
+    if (healthy >> cg & 1u) {
+      if (pos) *pos = d - 1;
+      return cg;
+    }
+  }
+  return -1;
+}
+
 void publish_plan(r2_comm* c, Replan& rp) {
-  const int l = rp.l, K = c->K, r = c->first_rank + l, r1 = (r + 1) % c->n;
+  const int l = rp.l, K = c->K, r = c->first_rank + l;
   Ctrl* C = c->ctrl_host[l];
   LaunchInfo li;
   {
@@ -542,17 +563,25 @@ void publish_plan(r2_comm* c, Replan& rp) {
     if (!p) return;
     li = *p;
   }
-  const int m = li.m, steps = li.steps;
+  // the ring carrying the stopped channel (R²CCL-AllReduce stage 1 runs two)
+  const RingInfo* RP = li.ring_of(rp.channel);
+  if (!RP || RP->pos_of(r) < 0) return;
+  const RingInfo& R = *RP;
+  const int r1 = R.next_of(r);
+  const int m = R.m, steps = R.steps, Kr = R.K;
   // healthy: assignable channels; dead: origins re-placed now (statically
   // dead, or known dead AND quiesced -- a known-dead channel whose CTAs are
-  // still draining items below its fault point waits for its own re-plan)
+  // still draining items below its fault point waits for its own re-plan).
+  // Masks in global channel bits, restricted to the ring's channels.
   uint32_t healthy = 0, dead = 0, static_mask = 0;
   {
     std::lock_guard<std::mutex> g(c->mu);
-    static_mask = r2_conn_mask_at(c, r, rp.seq);          // what the kernel planned with
+    for (int k = 0; k < K; ++k)
+      if ((R.chan_mask >> k & 1u) && r2_conn_ok_to(c, r, r1, k, rp.seq)) static_mask |= 1u << k;   // the kernel's plan
     for (int k = 0; k < K; ++k) {
+      if (!(R.chan_mask >> k & 1u)) continue;
       const bool stat_ok = static_mask >> k & 1u;
-      const bool known_ok = stat_ok && r2_conn_ok_at(c, r, k, rp.seq + 1);
+      const bool known_ok = stat_ok && r2_conn_ok_to(c, r, r1, k, rp.seq + 1);
       if (known_ok && !channel_stopped(c, l, k, rp.seq)) healthy |= 1u << k;
       if (!stat_ok || (!known_ok && channel_quiesced(c, l, k, rp.seq))) dead |= 1u << k;
     }
@@ -576,34 +605,37 @@ void publish_plan(r2_comm* c, Replan& rp) {
     // the service lane copies the receiver's completion words into host-mapped
     // memory (no copy-engine work that a profiler could serialise behind the
     // stuck collective)
-    const RankPtrs& nx = c->peers_host[l * c->n + r1];
+    const RankPtrs& nx = c->rp(R.region, l, r1);
     SvcReq rq;
     memset(&rq, 0, sizeof(rq));
     rq.kind = SVC_COPY;
     rq.src = (unsigned long long)nx.flags;
     rq.dst = (unsigned long long)c->flags_map_dev;
-    rq.nwords = (unsigned)((size_t)steps * K * m);
+    rq.nwords = (unsigned)((size_t)steps * Kr * m);
     uint32_t tag = r2_svc_post(c, rq);
-    if (li.local_step >= 0) {
+    if (R.local_step >= 0) {
       // LOCAL items keep their completion words in this rank's own memory
       // (reading R-5); the receiver has no words at that step
-      const size_t o = (size_t)li.local_step * K * m;
-      rq.src = (unsigned long long)(c->peers_host[l * c->n + r].flags + o);
+      const size_t o = (size_t)R.local_step * Kr * m;
+      rq.src = (unsigned long long)(c->rp(R.region, l, r).flags + o);
       rq.dst = (unsigned long long)(c->flags_map_dev + o);
-      rq.nwords = (unsigned)((size_t)K * m);
+      rq.nwords = (unsigned)((size_t)Kr * m);
       tag = r2_svc_post(c, rq);
     }
     if (!tag || !r2_svc_wait(c, tag, 2000000000ull)) R2LOG("replan seq %u rank %d: flag copy failed", rp.seq, r);
     R2LOG("replan seq %u rank %d ch%d: flags read", rp.seq, r, rp.channel);
   }
-  const int t_act = li.op == R2_OP_BROADCAST ? ((r - li.root) % c->n + c->n) % c->n : -1;
+  const bool chain_op = R.op == R2_OP_BROADCAST || R.op == R2_OP_R2CC_STAGE2;
+  const int t_act = chain_op ? ((R.pos_of(r) - R.root) % R.n + R.n) % R.n : -1;
+  // o: global origin channel; geometry (flags, keys) is ring-local
   auto done = [&](int t, int o, int j) {
-    if (t_act >= 0 && t != t_act) return true;         // Broadcast: this rank sends only at t_act
+    if (t_act >= 0 && t != t_act) return true;         // chains: this rank sends only at t_act
+    const int oi = R.local_of(o);
     if (from_keys) {
-      const unsigned long long key = ((unsigned long long)t << 40) | ((unsigned long long)o << 32) | (unsigned)j;
+      const unsigned long long key = ((unsigned long long)t << 40) | ((unsigned long long)oi << 32) | (unsigned)j;
       return key < lane_key[j % c->W];
     }
-    return (int)(flags[((size_t)t * K + o) * m + j] - rp.seq) >= 0;
+    return (int)(flags[((size_t)t * Kr + oi) * m + j] - rp.seq) >= 0;
   };
   // what did the stopped channel carry under the previous plan?
   auto carried_by = [&](int k, int o) -> bool {
@@ -613,7 +645,7 @@ void publish_plan(r2_comm* c, Replan& rp) {
       return false;
     }
     if (static_mask >> o & 1u) return false;
-    if (c->cfg.strategy == R2_HOT_REPAIR) return r2_first_healthy_in_chain(o, static_mask, K) == k;
+    if (c->cfg.strategy == R2_HOT_REPAIR) return first_healthy_in_ring(R, o, static_mask) == k;
     return static_mask >> k & 1u;
   };
   std::vector<PlanEntry> ents;
@@ -654,20 +686,21 @@ void publish_plan(r2_comm* c, Replan& rp) {
     ev.t_verdict_host_ns = rp.t_verdict;
     ev.t_plan_host_ns = now;
     if (c->cfg.strategy == R2_HOT_REPAIR) {
-      int a = r2_first_healthy_in_chain(o, healthy, K);
+      int pos = -1;
+      int a = first_healthy_in_ring(R, o, healthy, &pos);
       if (a < 0) nobackup = true;
       pe.mode = PLAN_HOT;
       pe.assignee = a < 0 ? 0 : a;
       pe.mask = healthy;
       ev.assignee = a;
-      ev.chain_pos = a < 0 ? -1 : ((a - o - 1) % K + K) % K;
+      ev.chain_pos = a < 0 ? -1 : pos;
     } else {
       pe.mode = PLAN_BAL;
       pe.mask = healthy;
       uint64_t sh[R2_MAX_CHANNELS];
       int w[R2_MAX_CHANNELS];
       for (int k = 0; k < K; ++k) w[k] = (int)c->weights[k];
-      if (r2_balance_shares(li.chunk / li.V, w, healthy, K, sh) != R2_SUCCESS) nobackup = true;
+      if (r2_balance_shares(R.chunk / R.V, w, healthy, K, sh) != R2_SUCCESS) nobackup = true;
       else
         for (int k = 0; k < K; ++k) ev.shares[k] = (int)sh[k];
     }
@@ -695,6 +728,9 @@ void publish_plan(r2_comm* c, Replan& rp) {
     }
     return;
   }
+  // the other ring's entries of this launch stay in force
+  for (const PlanEntry& e : c->cur_plan[l])
+    if (!(R.chan_mask >> e.origin & 1u) && ents.size() < R2_MAXK) ents.push_back(e);
   // publish: entries, unfreeze, new epoch.  The adopters re-place exactly the
   // chunks without a completion word (checked on the device, reading C-7).
   for (size_t i = 0; i < ents.size(); ++i) memcpy((void*)&C->entries[i], &ents[i], sizeof(PlanEntry));
@@ -755,8 +791,13 @@ bool progress_replans(r2_comm* c) {
       bool need_freeze = c->epoch[l] > 0;
       {
         std::lock_guard<std::mutex> g(c->mu);
-        const uint32_t full = (c->K >= 32) ? 0xFFFFFFFFu : ((1u << c->K) - 1u);
-        if (r2_conn_mask_at(c, c->first_rank + l, rp.seq) != full) need_freeze = true;   // static adoption
+        const LaunchInfo* li = launch_of(c, rp.seq);
+        const RingInfo* R = li ? li->ring_of(rp.channel) : nullptr;
+        const int r = c->first_rank + l;
+        if (R && R->pos_of(r) >= 0)
+          for (int k = 0; k < c->K; ++k)
+            if ((R->chan_mask >> k & 1u) && !r2_conn_ok_to(c, r, R->next_of(r), k, rp.seq))
+              need_freeze = true;                      // static adoption on this ring
       }
       if (need_freeze) {
         C->freeze = 1;

@@ -47,10 +47,12 @@ class Config(C.Structure):
                 ("channel_w", C.c_int * MAX_CHANNELS), ("use_channel_w", C.c_int), ("sim_ranks", C.c_int),
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
                 ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
-                ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int)]
+                ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int), ("allreduce_algo", C.c_int),
+                ("alpha_launch_ns", C.c_int)]
 
 
 PROTO_AUTO, PROTO_SIMPLE, PROTO_LL = 0, 1, 2
+ALGO_AUTO, ALGO_RING, ALGO_R2CC = 0, 1, 2
 
 
 class Fault(C.Structure):
@@ -101,7 +103,9 @@ class Status(C.Structure):
                 ("n_events", C.c_int), ("world", C.c_int), ("nlocal", C.c_int), ("nchannels", C.c_int),
                 ("dead_endpoints", C.c_uint32 * (MAX_LOCAL * 4)), ("dead_links", C.c_uint32 * (MAX_LOCAL * 4)),
                 ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int),
-                ("n_readmits", C.c_int), ("n_reprobes", C.c_int), ("n_service_kernels", C.c_int)]
+                ("n_readmits", C.c_int), ("n_reprobes", C.c_int), ("n_service_kernels", C.c_int),
+                ("n_r2cc", C.c_int), ("r2cc_rank", C.c_int), ("r2cc_X", C.c_double), ("r2cc_Y", C.c_double),
+                ("r2cc_NA", C.c_uint64), ("r2cc_NP", C.c_uint64), ("r2cc_seq", C.c_uint64)]
 
 
 class Geometry(C.Structure):
@@ -188,6 +192,8 @@ def config_default(**kw) -> Config:
             cfg.strategy = {"HOT_REPAIR": HOT_REPAIR, "BALANCE": BALANCE}[v]
         elif k == "protocol" and isinstance(v, str):
             cfg.protocol = {"AUTO": PROTO_AUTO, "SIMPLE": PROTO_SIMPLE, "LL": PROTO_LL}[v]
+        elif k == "allreduce_algo" and isinstance(v, str):
+            cfg.allreduce_algo = {"AUTO": ALGO_AUTO, "RING": ALGO_RING, "R2CC": ALGO_R2CC}[v]
         else:
             setattr(cfg, k, v)
     return cfg
@@ -348,7 +354,9 @@ class Comm:
                 "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)],
                 "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE"),
                 "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes,
-                "n_service_kernels": s.n_service_kernels}
+                "n_service_kernels": s.n_service_kernels,
+                "r2cc": {"calls": s.n_r2cc, "rank": s.r2cc_rank, "X": s.r2cc_X, "Y": s.r2cc_Y,
+                         "NA": int(s.r2cc_NA), "NP": int(s.r2cc_NP), "seq": int(s.r2cc_seq)}}
 
     def events(self) -> list:
         st = Status()

@@ -7,9 +7,10 @@ collective, and an unrecoverable collective is never reported as SUCCESS.
 * Service lane (r2_kernels.cu service_main): probes, plan installs and
   completion-word copies run inside the resident cooperative grid, so a fault
   recovers bit-exact while another kernel holds every spare SM."""
+import ctypes as C
 import os
 import subprocess
-import ctypes as C
+import time
 
 import numpy as np
 import pytest
@@ -65,6 +66,11 @@ def test_watchdog_abort_always_reported():
         if rc == R.SUCCESS:
             check_result(out, xs, g, dt)       # SUCCESS must mean a complete result
         codes.append(rc)
+        # let the monitor finish the (late) triangulation round of this seq, so
+        # that the REPAIR armed for the next seq is ordered after its verdict
+        t0 = time.time()
+        while (1, 0) not in comm.status()["dead_links"] and time.time() - t0 < 0.5:
+            time.sleep(0.002)
     assert codes == [R.ERR_TIMEOUT] * 50, codes
     st = comm.status()
     assert st["last_error"] == R.ERR_TIMEOUT
@@ -97,7 +103,6 @@ def test_failover_with_spare_sms_held(spinner, dtype):
         e0.record(s_ar)
         T.allreduce(comm, send, recv, stream=s_ar, count=N)
         e1.record(s_ar)
-    import time
     time.sleep(0.001)                           # the collective is resident
     kicks0 = comm.status()["n_service_kernels"]
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
