@@ -557,7 +557,62 @@ def run_multi(a):
     if not a.no_fault and world >= 2 and a.bw_model_gbps > 0:
         res["fault_bw_model"] = guarded(lambda: bw_model_section(
             a, T, R, mk, send, recv, ref, S, world, K, W, g.m, stream, barrier, reduce_max, gather))
+    if not a.no_fault and world >= 3 and a.bw_model_gbps > 0:
+        res["r2cc_allreduce"] = guarded(lambda: r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier,
+                                                             reduce_max))
     return res, rank
+
+
+def degrade(c, T, R, f, chans, send, recv, barrier):
+    """Kill endpoint (f, c) for c in chans as a real failure would: a LOCAL
+    fault mid-collective, triangulated to LOCAL_ENDPOINT(f) by the monitors
+    (dead from the next collective on)."""
+    import time as _t
+    for ch in chans:
+        s = c.status()["seq"] + 1
+        c.inject_fault(at_seq=s, kind="LOCAL", src_rank=f, channel=ch, step=0, chunk=0, byte_offset=0)
+        T.allreduce(c, send[:4096], recv[:4096])
+        assert c.sync() == R.SUCCESS
+        t0 = _t.time()
+        while (f, ch) not in c.status()["dead_endpoints"] and _t.time() - t0 < 10:
+            _t.sleep(0.002)
+        barrier()
+
+
+def r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier, reduce_max):
+    """one rank f loses d of its K channels (X = d/K lost
+    bandwidth, channels as bandwidth units via channel_gbps).  Above App. A's
+    threshold n/(3n-2) the planner runs R²CCL-AllReduce (global ring on f's
+    healthy channels + partial ring of the healthy ranks on f's dead ones, then
+    the tailored broadcast); compared with the Balance ring on the same
+    degraded communicator.  Times are max over ranks of the CUDA-event mean."""
+    f = 1 % world
+    out = {"channel_gbps": a.bw_model_gbps, "degraded_rank": f, "threshold_X": world / (3 * world - 2), "cases": []}
+    for d in (K // 2, 3 * K // 4):
+        row = {"dead_channels": d, "X": d / K}
+        for algo in ("RING", "R2CC"):
+            c = T.comm_from_env(R.config_default(
+                nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+                strategy="BALANCE", protocol="SIMPLE", channel_gbps=a.bw_model_gbps, allreduce_algo=algo))
+            T.register(c, recv)
+            degrade(c, T, R, f, list(range(d)), send, recv, barrier)
+            step = lambda cc=c: T.allreduce(cc, send, recv)  # noqa: E731
+            for _ in range(3):
+                step()
+            barrier()
+            ms = reduce_max(timed(step, 20, stream))
+            assert c.sync() == R.SUCCESS
+            st = c.status()
+            row[algo.lower()] = {"ms": ms, "busbw_per_rank": 2 * (world - 1) / world * S / (ms * 1e-3) / 1e9,
+                                 "r2cc_calls": st["r2cc"]["calls"]}
+            if algo == "R2CC":
+                row["Y"] = st["r2cc"]["Y"]
+                row["NA_NP"] = [st["r2cc"]["NA"], st["r2cc"]["NP"]]
+            c.finalize()
+            barrier()
+        row["r2cc_speedup_over_ring"] = row["ring"]["ms"] / row["r2cc"]["ms"]
+        out["cases"].append(row)
+    return out
 
 
 def bw_model_section(a, T, R, mk_default, send, recv, ref, S, world, K, W, m, stream, barrier, reduce_max, gather):
@@ -663,6 +718,8 @@ def report(a, res, n_gpus, n_ranks, mode):
         line["successive_failover"] = res["successive"]
     if "fault_bw_model" in res:
         line["fault_bandwidth_model"] = res["fault_bw_model"]
+    if "r2cc_allreduce" in res:
+        line["r2cc_allreduce"] = res["r2cc_allreduce"]
     return line
 
 

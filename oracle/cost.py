@@ -86,11 +86,13 @@ def lost_fraction(weights, dead) -> float:
 
 
 def r2cc_split(N: int, V: int, Y: float) -> tuple[int, int]:
-    """Reading R-9: the partial AllReduce takes the last N_P = floor(Y N / V) V
-    elements (whole 16-byte vectors), the global ring the first N_A = N - N_P."""
-    NP = math.floor(Y * N / V) * V
-    NP = min(NP, N // V * V)
-    return N - NP, NP
+    """Reading R-9: the global ring takes the first N_A elements, the partial
+    AllReduce the last N_P = N - N_A, where N_A = N - floor(Y N / V) V rounded
+    up to whole 16-byte vectors (so that the partial region starts 16-byte
+    aligned; its own tail may be ragged), at most N."""
+    NP0 = math.floor(Y * N / V) * V
+    NA = min(N, -(-(N - NP0) // V) * V)
+    return NA, N - NA
 
 
 def algo_times(n: int, X: float, Y: float, S: float, alpha: float, B: float, launch: float):

@@ -915,10 +915,11 @@ R2ccPlan r2cc_plan(r2_comm* c, size_t count, r2_dtype_t dt, uint32_t q) {
   pl.X = wd / wt;
   pl.Y = r2cc_partition(n, pl.X);
   const size_t V = 16 / (size_t)elem_bytes(dt);
-  // N_P = floor(Y N / V) V (vector-aligned split, reading R-9), N_A = N - N_P
-  pl.NP = (size_t)floor(pl.Y * (double)count / (double)V) * V;
-  if (pl.NP > count) pl.NP = count / V * V;
-  pl.NA = count - pl.NP;
+  // reading R-9: N_A = N - floor(Y N / V) V rounded up to whole vectors (the
+  // partial region starts 16-byte aligned), at most N; N_P = N - N_A
+  const size_t np0 = (size_t)floor(pl.Y * (double)count / (double)V) * V;
+  pl.NA = std::min(count, (count - std::min(np0, count) + V - 1) / V * V);
+  pl.NP = count - pl.NA;
   pl.applies = pl.Y > 0 && pl.NP > 0 && pl.NA > 0;
   return pl;
 }

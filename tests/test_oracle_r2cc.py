@@ -86,11 +86,17 @@ def test_y_zero_is_the_plain_ring():
 
 
 def test_split_rule():
-    """Reading R-9: N_P = floor(Y N / V) V, N_A = N - N_P."""
+    """Reading R-9: N_A = N - floor(Y N / V) V rounded up to a vector (<= N),
+    N_P = N - N_A: the partial region starts on a 16-byte boundary."""
     assert C.r2cc_split(1000, 4, 0.5) == (500, 500)
-    assert C.r2cc_split(1001, 8, 0.5) == (505, 496)
-    assert C.r2cc_split(10, 4, 0.99) == (2, 8)
+    assert C.r2cc_split(1001, 8, 0.5) == (512, 489)
+    assert C.r2cc_split(1001, 4, 0.5294) == (476, 525)
+    assert C.r2cc_split(10, 4, 0.99) == (4, 6)
     assert C.r2cc_split(7, 8, 0.9) == (7, 0)
+    for N in range(1, 200):
+        for V in (4, 8):
+            NA, NP = C.r2cc_split(N, V, 0.61)
+            assert NA + NP == N and NA % V == 0 or NA == N
 
 
 def stage2(xs, p, n, K, N, f, E, chunk, dtype, **kw):
