@@ -645,8 +645,13 @@ def bw_model_section(a, T, R, mk_default, send, recv, ref, S, world, K, W, m, st
 
 def ncu_traffic(a, n_ranks, W):
     """DRAM bytes per launch from the committed ncu --set full capture of this
-    exact workload (profiles/r01_ncu_traffic.json), else None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_traffic.json")
+    exact workload (the newest profiles/rNN_ncu_traffic.json, tools/ncu_traffic.py), else None."""
+    import glob
+    found = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                          "r[0-9][0-9]_ncu_traffic.json")))
+    if not found:
+        return None, None
+    path = found[-1]
     if not (n_ranks == 8 and a.bytes == 256 * MIB and a.channels == 8 and W == 2 and a.chunk == 512 * 1024):
         return None, None
     try:
