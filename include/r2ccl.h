@@ -35,6 +35,7 @@ extern "C" {
 
 #define R2_MAX_CHANNELS 16   /* K upper bound                                   */
 #define R2_MAX_LOCAL 16      /* simulated ranks per process upper bound         */
+#define R2_MAX_RANKS 64      /* ranks of a communicator upper bound             */
 
 typedef enum {
   R2_SUCCESS = 0,
@@ -113,11 +114,13 @@ typedef struct {
  *   sim_ranks         world == 1 only: k >= 1 simulated ranks on one GPU
  *                     (send/recv then hold k rank buffers back to back)
  *   protocol          R2_PROTO_AUTO (default): per call, the alpha-beta model
- *                     below picks SIMPLE or LL;
- *                     R2_PROTO_SIMPLE / R2_PROTO_LL force one
- *   ll_max_bytes      largest per-rank payload the LL protocol may carry
- *                     (sizes its scratch: 4 x payload per rank; default 32 MiB,
- *                     0 disables LL)
+ *                     below picks SIMPLE, LL or LL128;
+ *                     R2_PROTO_SIMPLE / R2_PROTO_LL / R2_PROTO_LL128 force one
+ *                     (a forced LL/LL128 call whose payload exceeds the line
+ *                     scratch returns R2_ERR_INVALID_ARG)
+ *   ll_max_bytes      largest per-rank payload the LL / LL128 protocols may
+ *                     carry (sizes their shared line scratch: 4 x payload per
+ *                     rank; default 128 MiB, 0 disables both)
  *   reprobe_us        first re-probe of a dead connection after this many
  *                     microseconds, then exponential back-off ("adapting
  *                     probe frequency"); default 2000, 0 disables re-probing
@@ -127,10 +130,11 @@ typedef struct {
  *                     a bandwidth unit like the paper's NIC (reading C-1: without
  *                     it channels share the GPU's NVLink ports and a dead channel
  *                     only removes CTAs)
- *   alpha_simple_ns, alpha_ll_ns, beta_mbps
+ *   alpha_simple_ns, alpha_ll_ns, alpha_ll128_ns, beta_mbps
  *                     cost model: T = (#ring steps) * alpha + (wire bytes per
- *                     rank) / beta, LL moving twice the bytes (defaults from
- *                     profiles/r01_pingpong.log and r01_sizes_n4.jsonl)
+ *                     rank) / beta, LL moving twice the bytes and LL128 8/7 of
+ *                     them (defaults from profiles/r01_pingpong.log,
+ *                     r01_sizes_n4.jsonl and the round-2 protocol sweeps)
  *
  * Protocols.  SIMPLE: 16-byte vectors straight into the peer's memory, one
  * fence.acq_rel.sys per retired batch, then the completion word (P:33's
@@ -138,8 +142,11 @@ typedef struct {
  * vector travels as two 16-byte lines {w0, seq, w1, seq}, {w2, seq, w3, seq}
  * into library scratch, self-validating at the receiver, so the completion
  * word needs no fence; the receiver unpacks the last all-gather step locally
- * (reading R-6).  Both keep the per-chunk completion words, rollback and
- * re-placement unchanged.
+ * (reading R-6).  LL128 (mid sizes, reading R-12): a chunk travels as
+ * 128-byte lines of 7 payload vectors + 1 flag vector {seq x 4}, each line
+ * written by one warp store instruction and accepted by the receiver when its
+ * flag vector equals seq: 8/7 of the bytes and no fence per step.  All three
+ * keep the per-chunk completion words, rollback and re-placement unchanged.
  */
 typedef struct {
   int nchannels;
@@ -161,6 +168,7 @@ typedef struct {
   int channel_gbps;
   int allreduce_algo;   /* r2_algo_t (default AUTO)                                  */
   int alpha_launch_ns;  /* cost model: one more collective launch (R²CCL stage 2)    */
+  int alpha_ll128_ns;   /* cost model: per ring step under LL128                     */
 } r2_config_t;
 
 /*
@@ -178,7 +186,7 @@ typedef struct {
  */
 typedef enum { R2_ALGO_AUTO = 0, R2_ALGO_RING = 1, R2_ALGO_R2CC = 2 } r2_algo_t;
 
-typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2 } r2_protocol_t;
+typedef enum { R2_PROTO_AUTO = 0, R2_PROTO_SIMPLE = 1, R2_PROTO_LL = 2, R2_PROTO_LL128 = 3 } r2_protocol_t;
 
 /*
  * An injected channel fault.  Fires in collective number
@@ -429,6 +437,17 @@ void r2_failover_chain(int c, int K, int* out);
 
 /* Rollback on a completion ledger. */
 void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
+
+/* Topology-aware logical re-ranking: Algorithm 1 (App. D, §6
+ * P:726 "pairs of neighbors whose rail overlap falls below a bandwidth
+ * threshold are separated by inserting 'bridge' nodes").  ring_in[0..n): the
+ * ring order (a permutation of ranks 0..n-1); rails[u]: bitmask of the
+ * channels whose endpoint on rank u is alive (the rail set S_u, reading
+ * C-1); dead_links[u] (may be NULL): channels whose standard link u -> u+1
+ * mod n is dead (reading R-13: an edge's capacity excludes them).  Writes
+ * R' to ring_out[0..n) (caller-owned).  Returns the number of relocations,
+ * or -1 on invalid arguments (n outside 1..R2_MAX_RANKS, NULL pointers). */
+int r2_rerank(int n, const int* ring_in, const uint32_t* rails, const uint32_t* dead_links, int* ring_out);
 
 /* Geometry of one collective (SURVEY §8 header, reading C-3).
  * AllReduce: N = count, shards of Np/n at stride shard.

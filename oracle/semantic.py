@@ -188,3 +188,12 @@ def r2cc_allreduce(xs: list[np.ndarray], dtype: str, f: int, NA: int, shard_A: i
         p = allreduce(healthy, shard_P, dtype)
         y[NA:] = hop_add(p, np.asarray(xs[f])[NA:], dtype)
     return y
+
+
+def allreduce_ring(xs: list[np.ndarray], order: list[int], shard_elems: int, dtype: str) -> np.ndarray:
+    """AllReduce on a re-ranked ring ("most collective algorithms are
+    symmetric and agnostic to node ordering, enabling safe reordering";
+    Algorithm 1's R'): the Layer-1 fold with ring position p held by rank
+    order[p] -- shard s is folded over the ranks at positions s+1, s+2, ...,
+    s, as in `allreduce`, so only the order of the hops changes."""
+    return allreduce([xs[r] for r in order], shard_elems, dtype)

@@ -39,8 +39,16 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, siz
   const size_t slice_cap = align_up(std::max<size_t>(max_bytes, 16), 16);
   const size_t bchunk = std::min<size_t>(chunk, (size_t)128 << 10);   // Broadcast chunk cap (r2_geometry_op)
   L.m_cap = (int)std::max<size_t>((slice_cap + bchunk - 1) / bchunk, (size_t)W);
-  // LL: two 16-byte lines per 16-byte vector, one slot per ring step
-  L.ll_slot_bytes = ll_max_bytes ? 2 * std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K) : 0;
+  // LL: two 16-byte lines per 16-byte vector, one slot per ring step.  LL128
+  // (reading R-12): each chunk owns whole 128-byte lines of 7 payload vectors,
+  // so a slot needs <= K * (slice / 112 + chunks per slice + 1) lines; the
+  // slot is sized for the larger of the two
+  if (ll_max_bytes) {
+    const size_t shard = std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K);
+    const size_t slice = shard / K;
+    const size_t mmax = std::max<size_t>((size_t)W, (slice + chunk - 1) / chunk) + 1;
+    L.ll_slot_bytes = std::max<size_t>(2 * shard, (size_t)K * ((slice + 111) / 112 + mmax) * 128);
+  }
   const int steps = n > 1 ? 2 * n - 1 : 1;     // + the LL unpack step
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -261,7 +269,7 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
   cfg->sim_ranks = 1;
   cfg->protocol = R2_PROTO_AUTO;
-  cfg->ll_max_bytes = (size_t)32 << 20;   // covers the n = 8 crossover (~26 MB)
+  cfg->ll_max_bytes = (size_t)128 << 20;  // covers the LL128 / SIMPLE crossovers (reading R-12)
   // fitted to the forced-protocol sweeps at n = 2 and 4 (profiles/r01_protocols_n{2,4}.jsonl):
   // T(n=2) / T(n=4) = c + steps * alpha, crossovers 5 MB (n=2) and 12 MB (n=4)
   cfg->alpha_simple_ns = 7150;     // per ring step, SIMPLE (fence + completion word + publish)
@@ -271,6 +279,7 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->reprobe_max_us = 200000;
   cfg->allreduce_algo = R2_ALGO_AUTO;
   cfg->alpha_launch_ns = 6000;     // one cooperative launch + prologue (profiles/r01_host_overhead_n4.log)
+  cfg->alpha_ll128_ns = 2300;      // per ring step, LL128 (one 128-byte line flight + the warp's flag check)
 }
 
 extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,
@@ -310,7 +319,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     c->oob = *oob;
     c->has_oob = world > 1;
   }
-  if (cfg.protocol < R2_PROTO_AUTO || cfg.protocol > R2_PROTO_LL) {
+  if (cfg.protocol < R2_PROTO_AUTO || cfg.protocol > R2_PROTO_LL128) {
     delete c;
     return R2_ERR_INVALID_ARG;
   }
@@ -588,20 +597,34 @@ r2_result_t prep_ring(r2_comm* c, const RingSpec& rs, r2_dtype_t dt, uint32_t se
   if ((!chain && g.shard * E > slot) || g.m > c->lay.m_cap) return R2_ERR_INVALID_ARG;
   if (op == R2_OP_R2CC_STAGE2 && g.Np * E > c->lay.tailor_bytes) return R2_ERR_INVALID_ARG;
   // protocol: alpha-beta model over the ring's steps; LL
-  // moves twice the bytes but pays no fence per step (r2ccl.h "Protocols")
-  bool ll = false;
-  const bool ll_fits = rs.allow_ll && rs.region == 0 && c->lay.ll_slot_bytes && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
+  // moves twice the bytes, LL128 8/7 of them, but neither pays a fence per
+  // step (r2ccl.h "Protocols").  ll: 0 SIMPLE, 1 LL, 2 LL128
+  int ll = 0;
+  const bool lines_ok = rs.allow_ll && rs.region == 0 && c->lay.ll_slot_bytes;
+  const bool ll_fits = lines_ok && 2 * g.shard * (size_t)E <= c->lay.ll_slot_bytes;
+  const size_t lc = (g.chunk / g.V + 6) / 7;                       // LL128 lines per chunk
+  const bool l128_fits = lines_ok && (size_t)K * g.m * lc * 128 <= c->lay.ll_slot_bytes;
   if (chain || !rs.allow_ll) {
-    ll = false;                                        // chains: always SIMPLE (r2ccl.h)
+    ll = 0;                                            // chains: always SIMPLE (r2ccl.h)
   } else if (c->cfg.protocol == R2_PROTO_LL) {
     if (!ll_fits) return R2_ERR_INVALID_ARG;
-    ll = true;
-  } else if (c->cfg.protocol == R2_PROTO_AUTO && ll_fits) {
+    ll = 1;
+  } else if (c->cfg.protocol == R2_PROTO_LL128) {
+    if (!l128_fits) return R2_ERR_INVALID_ARG;
+    ll = 2;
+  } else if (c->cfg.protocol == R2_PROTO_AUTO && (ll_fits || l128_fits)) {
     const double wire = (double)(op == R2_OP_ALLREDUCE ? 2 : 1) * (n - 1) * (double)g.shard * E;
     const double bpns = std::max(c->cfg.beta_mbps, 1) / 1000.0;
-    const double t_simple = g.steps * (double)c->cfg.alpha_simple_ns + wire / bpns;
-    const double t_ll = (g.steps + (op != R2_OP_REDUCE_SCATTER)) * (double)c->cfg.alpha_ll_ns + 2 * wire / bpns;
-    ll = t_ll < t_simple;
+    const int unpack = op != R2_OP_REDUCE_SCATTER;
+    double best = g.steps * (double)c->cfg.alpha_simple_ns + wire / bpns;
+    if (ll_fits) {
+      const double t = (g.steps + unpack) * (double)c->cfg.alpha_ll_ns + 2 * wire / bpns;
+      if (t < best) best = t, ll = 1;
+    }
+    if (l128_fits) {
+      const double t = (g.steps + unpack) * (double)c->cfg.alpha_ll128_ns + 8.0 / 7.0 * wire / bpns;
+      if (t < best) best = t, ll = 2;
+    }
   }
   const int steps = g.steps + (ll && op != R2_OP_REDUCE_SCATTER ? 1 : 0);   // + the LL unpack step
   const int local_step = ll && op != R2_OP_REDUCE_SCATTER ? steps - 1 : g.local_step;
@@ -832,7 +855,7 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
     }
   }
   c->seq = seq;
-  c->last_protocol = S.ring[0].ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
+  c->last_protocol = S.ring[0].ll == 2 ? R2_PROTO_LL128 : S.ring[0].ll ? R2_PROTO_LL : R2_PROTO_SIMPLE;
   const uint64_t t_pre = r2_debug >= 2 ? r2_now_ns() : 0;
   static uint64_t sum_win = 0;
   if (r2_debug >= 2) sum_win += t_pre - t_win0;

@@ -4,7 +4,10 @@
 //   r2_failover_chain   ordered backups (C-2)
 //   r2_rollback         sender resume / receiver floor
 //   r2_geometry         shards / slices / chunks (SURVEY §8 header, C-3)
+//   r2_rerank           bridge-based logical re-ranking (Algorithm 1; C-19, R-13)
 #include <string.h>
+
+#include <algorithm>
 
 #include "r2_comm.h"
 
@@ -242,4 +245,75 @@ extern "C" const char* r2_strerror(r2_result_t r) {
     case R2_ERR_INTERNAL: return "internal error";
   }
   return "unknown error";
+}
+
+// Algorithm 1 (§6): bridge-based repair of a ring order.
+// Rails of rank u = channels whose endpoint on u is alive; the capacity of
+// the ring edge u -> v is the number of channels alive at both whose link
+// u -> v is alive (reading R-13; only standard links u -> u+1 mod n have link
+// state, reading R-10).  Scan order, tie-breaks and skipped pairs: reading
+// C-19 / R-13.
+namespace {
+struct RerankCtx {
+  int n;
+  const uint32_t* rails;
+  const uint32_t* dead_links;
+  int cap(int u, int v) const {
+    uint32_t m = rails[u] & rails[v];
+    if (dead_links && v == (u + 1) % n) m &= ~dead_links[u];
+    return __builtin_popcount(m);
+  }
+};
+int ring_index(const int* R, int n, int u) {
+  for (int i = 0; i < n; ++i)
+    if (R[i] == u) return i;
+  return -1;
+}
+}  // namespace
+
+extern "C" int r2_rerank(int n, const int* ring_in, const uint32_t* rails, const uint32_t* dead_links,
+                         int* ring_out) {
+  if (n <= 0 || n > R2_MAX_RANKS || !ring_in || !rails || !ring_out) return -1;
+  RerankCtx cx{n, rails, dead_links};
+  int R[R2_MAX_RANKS];
+  for (int i = 0; i < n; ++i) R[i] = ring_out[i] = ring_in[i];
+  if (n < 3) return 0;
+  int B = 1 << 30;                                   // line 2: B_global = min |S_u|
+  for (int i = 0; i < n; ++i) B = std::min(B, __builtin_popcount(rails[ring_in[i]]));
+  // lines 3-9: candidate edges of the input ring, gap descending, position ascending
+  int cu[R2_MAX_RANKS], cv[R2_MAX_RANKS], gap[R2_MAX_RANKS], nc = 0;
+  for (int i = 0; i < n; ++i) {
+    const int u = ring_in[i], v = ring_in[(i + 1) % n], c = cx.cap(u, v);
+    if (c >= B) continue;
+    int at = nc++;
+    while (at > 0 && gap[at - 1] < B - c) {          // stable insertion: ties keep position order
+      cu[at] = cu[at - 1], cv[at] = cv[at - 1], gap[at] = gap[at - 1];
+      --at;
+    }
+    cu[at] = u, cv[at] = v, gap[at] = B - c;
+  }
+  int moved = 0;
+  for (int k = 0; k < nc; ++k) {
+    const int u = cu[k], v = cv[k];
+    int iu = ring_index(R, n, u);
+    if (R[(iu + 1) % n] != v && R[(iu + n - 1) % n] != v) continue;   // already separated
+    int best = -1;
+    for (int i = 0; i < n && best < 0; ++i) {        // line 13: R' index order from position 0
+      const int w = R[i];
+      if (w == u || w == v) continue;
+      const int x = R[(i + n - 1) % n], y = R[(i + 1) % n];
+      if (std::min(cx.cap(u, w), cx.cap(w, v)) >= B && cx.cap(x, y) >= B) best = w;   // lines 15-19
+    }
+    if (best < 0) continue;
+    // Relocate(best, between u and v)
+    int ib = ring_index(R, n, best);
+    for (int i = ib; i < n - 1; ++i) R[i] = R[i + 1];
+    iu = ring_index(R, n - 1, u);
+    const int at = R[(iu + 1) % (n - 1)] == v ? iu + 1 : iu;
+    for (int i = n - 1; i > at; --i) R[i] = R[i - 1];
+    R[at] = best;
+    ++moved;
+  }
+  for (int i = 0; i < n; ++i) ring_out[i] = R[i];
+  return moved;
 }

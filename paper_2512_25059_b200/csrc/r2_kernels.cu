@@ -200,6 +200,7 @@ struct Slot {                 // read by the data warps
                               // AllGather shards at a ragged stride may not be)
   unsigned long long e0;
   unsigned long long lim;     // one past the last valid element of the item's shard
+  unsigned int lo_c, cvec;    // LL128: the part's first vector in its chunk / vectors of the chunk
 };
 
 struct Meta {                 // read by the control warp at retirement
@@ -425,6 +426,105 @@ __device__ void move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
     if (d_loc) {
       if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E, aligned);
       else st_v4(d_loc + (size_t)v * 16, a);
+    }
+  }
+}
+
+// ------------------------------------------------------------ LL128 protocol
+// (reading R-12; r2ccl.h "Protocols").  A chunk's vectors travel in 128-byte
+// lines of 7 payload vectors + one flag vector {seq, seq, seq, seq}: line L of
+// a chunk holds its vectors 7L .. 7L+6 (the last line zero-padded).  Eight
+// consecutive lanes of a warp own one line, so ONE warp-wide 16-byte store
+// instruction writes four whole lines and one 16-byte load instruction reads
+// them back: the receiver accepts a line when its flag vector equals the
+// collective's seq, which relies on a 128-byte line written by one warp store
+// being observed whole across NVLink (the property NCCL's LL128 relies on;
+// checked by tools/ll128_tear.cu).  Every line a part touches is written
+// WHOLE by that part (vectors outside the part are recomputed from the same
+// inputs, so two parts sharing a boundary line write identical bytes).
+#define LL128_PAY 7
+template <int U>
+__device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
+                                               const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
+                                               const volatile unsigned int* abort_word) {
+  const unsigned int pos = lane & 7u;
+  for (unsigned int spins = 0;; ++spins) {
+    bool ok = true;
+    bool okl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool f = !act[u] || (x[u].x == seq && x[u].y == seq && x[u].z == seq && x[u].w == seq);
+      okl[u] = __shfl_sync(0xFFFFFFFFu, f, lane | 7u);      // the line's flag lane decides
+      ok &= okl[u];
+    }
+    if (__all_sync(0xFFFFFFFFu, ok)) return;
+    if ((spins & 0x3FFu) == 0x3FFu) {
+      const int ab = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (int)(*abort_word == seq) : 0, 0);
+      if (ab) return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (!okl[u]) x[u] = ll_line(q + (size_t)L[u] * 128 + pos * 16);
+  }
+}
+
+// Part [lo, lo + nvec) of a chunk of cvec vectors.  src: user memory at the
+// part's first vector, or (src_ll) the chunk's lines in an LL128 slot; s_in:
+// the chunk's lines (or null); d_rem: the chunk's lines at the peer (or null);
+// d_loc: user memory / stage at the part's first vector (or null).  dtid / dn:
+// thread index / count over the data warps (multiples of 32).
+template <int DT>
+__device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned int dn, const char* src, bool src_ll,
+                           const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
+                           unsigned int lo, unsigned int nvec, unsigned int cvec, unsigned long long lim,
+                           bool aligned, unsigned int seq, const volatile unsigned int* abort_word) {
+  constexpr int U = 4;                    // line groups per warp per iteration (memory-level parallelism)
+  const int E = p.elem_bytes, V = p.V;
+  const unsigned int lane = dtid & 31u, wid = dtid >> 5, nw = dn >> 5;
+  const unsigned int pos = lane & 7u;
+  const unsigned int L0 = lo / LL128_PAY, L1 = (lo + nvec + LL128_PAY - 1) / LL128_PAY;
+  const uint4 flag = make_uint4(seq, seq, seq, seq);
+  for (unsigned int base = L0 + wid * 4u * U; base < L1; base += nw * 4u * U) {
+    uint4 a[U], b[U];
+    bool act[U];
+    unsigned int L[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      L[u] = base + (unsigned int)u * 4u + (lane >> 3);
+      act[u] = L[u] < L1;
+      const unsigned int vc = L[u] * LL128_PAY + pos;
+      a[u] = make_uint4(0u, 0u, 0u, 0u);
+      b[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (!act[u]) continue;
+      if (src_ll) {
+        a[u] = ll_line(src + (size_t)L[u] * 128 + pos * 16);
+      } else if (pos < LL128_PAY && vc < cvec) {
+        const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
+        const long long left = (long long)lim - ev;
+        const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+        a[u] = ld_user(src + ((long long)vc - (long long)lo) * 16, valid, E, aligned);
+      }
+      if (s_in) b[u] = ll_line(s_in + (size_t)L[u] * 128 + pos * 16);
+    }
+    if (src_ll) ll128_validate<U>(a, act, src, L, lane, seq, abort_word);
+    if (s_in) ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned int vc = L[u] * LL128_PAY + pos;
+      const bool pay = pos < LL128_PAY && vc < cvec;
+      uint4 v = pay ? a[u] : make_uint4(0u, 0u, 0u, 0u);
+      if (pay && s_in) v = vadd<DT>(b[u], v);
+      if (d_rem && act[u]) st_v4(d_rem + (size_t)L[u] * 128 + pos * 16, pos == LL128_PAY ? flag : v);
+      if (d_loc && act[u] && pay && vc >= lo && vc < lo + nvec) {
+        const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
+        if (loc_user) {
+          const long long left = (long long)lim - ev;
+          const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+          st_user(d_loc + (size_t)(vc - lo) * 16, v, valid, E, aligned);
+        } else {
+          st_v4(d_loc + (size_t)(vc - lo) * 16, v);
+        }
+      }
     }
   }
 }
@@ -764,7 +864,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     // channel bandwidth model (r2ccl.h channel_gbps): a token bucket per lane
     const unsigned long long now = gtimer();
     if (now < sh.pace_next) return ST_NOTREADY;
-    const unsigned long long wire = (unsigned long long)(it.hi - it.lo) * 16ull * (p.ll ? 2ull : 1ull);
+    const unsigned long long wire = (unsigned long long)(it.hi - it.lo) * (p.ll == 2 ? 18ull : p.ll ? 32ull : 16ull);
     sh.pace_next = (now > sh.pace_next ? now : sh.pace_next) + wire * p.lane_ps_per_byte / 1000ull;
   }
 
@@ -820,8 +920,17 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     d.loc_user = 1;
   } else if (p.ll) {
     // LL: scratch traffic as lines; slot index = the AllReduce step that sends
-    // into it (RS hops 0..n-2, AG sends n-1..2n-3), offsets doubled
-    const unsigned long long lo = off * E * 2;
+    // into it (RS hops 0..n-2, AG sends n-1..2n-3), offsets doubled.  LL128:
+    // each chunk owns ceil(chunk vectors / 7) whole lines of the slot; the
+    // slot pointers address the chunk's first line, the user pointers the
+    // part's first vector (move_ll128)
+    const unsigned long long cvec_full = p.chunk / V;
+    const unsigned long long lo =
+        p.ll == 2 ? ((unsigned long long)it.o * p.m + it.j) * ((cvec_full + LL128_PAY - 1) / LL128_PAY) * 128ull
+                  : off * E * 2;
+    const unsigned long long c0 = (unsigned long long)it.j * p.chunk;
+    d.cvec = (unsigned int)((p.slice - c0 < p.chunk ? p.slice - c0 : p.chunk) / V);
+    d.lo_c = it.lo;
     d.rs = 1;                                         // d_rem is library scratch
     if (ta <= n - 2) {                                // reduce-scatter hop
       d.src = p.send[k.l] + e0 * E;
@@ -1144,13 +1253,22 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
       if (lane == 0) mbar_arrive(&sh.empty[u]);
       return;
     }
-    if (p.ll)
+    if (p.ll == 2)
+      move_ll128<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.lo_c,
+                     d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort);
+    else if (p.ll)
       move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
                   d.lim, d.aligned != 0, k.seq, k.me->abort);
     else
       move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
                d.aligned != 0);
-    if (d.poison && d.d_rem && p.ll) {
+    if (d.poison && d.d_rem && p.ll == 2) {
+      // LL128: whole lines after the delivered prefix arrive invalid (flag ~0)
+      const unsigned int Lf = (d.lo_c + d.nvec + LL128_PAY - 1) / LL128_PAY;
+      const unsigned int Le = (d.lo_c + d.total + LL128_PAY - 1) / LL128_PAY;
+      for (unsigned int x = Lf * 8 + dtid; x < Le * 8; x += dn)
+        st_v4(d.d_rem + (size_t)x * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+    } else if (d.poison && d.d_rem && p.ll) {
       // LL: the rest of the faulted part arrives as invalid lines (reading C-6)
       for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {
         st_v4(d.d_rem + (size_t)v * 32, make_uint4(~0u, ~0u, ~0u, ~0u));

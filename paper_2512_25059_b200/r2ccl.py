@@ -48,10 +48,10 @@ class Config(C.Structure):
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
                 ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
                 ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int), ("allreduce_algo", C.c_int),
-                ("alpha_launch_ns", C.c_int)]
+                ("alpha_launch_ns", C.c_int), ("alpha_ll128_ns", C.c_int)]
 
 
-PROTO_AUTO, PROTO_SIMPLE, PROTO_LL = 0, 1, 2
+PROTO_AUTO, PROTO_SIMPLE, PROTO_LL, PROTO_LL128 = 0, 1, 2, 3
 ALGO_AUTO, ALGO_RING, ALGO_R2CC = 0, 1, 2
 
 
@@ -146,6 +146,8 @@ EXPORTS = {
     "r2_balance_shares": (C.c_int, [C.c_uint64, C.POINTER(C.c_int), C.c_uint32, C.c_int, C.POINTER(C.c_uint64)]),
     "r2_failover_chain": (None, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "r2_rollback": (None, [C.POINTER(C.c_uint8), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "r2_rerank": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                            C.POINTER(C.c_int)]),
     "r2_geometry": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t, C.POINTER(Geometry)]),
     "r2_geometry_op": (C.c_int, [C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_size_t,
                                  C.POINTER(Geometry)]),
@@ -191,7 +193,7 @@ def config_default(**kw) -> Config:
         elif k == "strategy" and isinstance(v, str):
             cfg.strategy = {"HOT_REPAIR": HOT_REPAIR, "BALANCE": BALANCE}[v]
         elif k == "protocol" and isinstance(v, str):
-            cfg.protocol = {"AUTO": PROTO_AUTO, "SIMPLE": PROTO_SIMPLE, "LL": PROTO_LL}[v]
+            cfg.protocol = {"AUTO": PROTO_AUTO, "SIMPLE": PROTO_SIMPLE, "LL": PROTO_LL, "LL128": PROTO_LL128}[v]
         elif k == "allreduce_algo" and isinstance(v, str):
             cfg.allreduce_algo = {"AUTO": ALGO_AUTO, "RING": ALGO_RING, "R2CC": ALGO_R2CC}[v]
         else:
@@ -222,6 +224,19 @@ def failover_chain(c: int, K: int) -> list:
     out = (C.c_int * max(K - 1, 1))()
     lib().r2_failover_chain(c, K, out)
     return list(out[: K - 1])
+
+
+def rerank(ring, rails, dead_links=None) -> list:
+    """Algorithm 1 (r2ccl.h r2_rerank): ring order, per-rank alive-channel
+    masks, optional per-rank dead standard-link masks -> R'."""
+    n = len(ring)
+    rin = (C.c_int * n)(*ring)
+    rm = (C.c_uint32 * n)(*rails)
+    dl = (C.c_uint32 * n)(*dead_links) if dead_links is not None else None
+    out = (C.c_int * n)()
+    if lib().r2_rerank(n, rin, rm, dl, out) < 0:
+        raise ValueError("r2_rerank: invalid arguments")
+    return list(out)
 
 
 def rollback(completed) -> tuple:
@@ -352,7 +367,7 @@ class Comm:
                 "dead_endpoints": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_endpoints[r] >> c) & 1),
                 "dead_links": sorted((r, c) for r in range(n) for c in range(K) if (s.dead_links[r] >> c) & 1),
                 "bytes": [[int(s.bytes[l][c]) for c in range(K)] for l in range(s.nlocal)],
-                "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL"}.get(s.last_protocol, "NONE"),
+                "last_protocol": {PROTO_SIMPLE: "SIMPLE", PROTO_LL: "LL", PROTO_LL128: "LL128"}.get(s.last_protocol, "NONE"),
                 "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes,
                 "n_service_kernels": s.n_service_kernels,
                 "r2cc": {"calls": s.n_r2cc, "rank": s.r2cc_rank, "X": s.r2cc_X, "Y": s.r2cc_Y,

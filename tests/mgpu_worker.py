@@ -53,7 +53,8 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     rc = comm.sync()
     E = r2inputs.elem_bytes(dtype)
     cfg = comm.cfg
-    ll = comm.status()["last_protocol"] == "LL"      # the alpha-beta choice (f3) shapes the step list
+    proto = comm.status()["last_protocol"]
+    ll = proto in ("LL", "LL128")      # the alpha-beta choice (f3) shapes the step list
     g = Geometry(world, cfg.nchannels, N, E,
                  effective_chunk_bytes(N, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel), ll=ll)
     y = OS.allreduce(xs, g.shard, dtype)
@@ -64,7 +65,7 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     oks = [None] * world
     dist.all_gather_object(oks, bool(ok))
     out = {"N": N, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc, "ok": all(oks),
-           "protocol": "LL" if ll else "SIMPLE"}
+           "protocol": proto}
     if faults:
         got = sorted((e for ev in all_evs for e in ev), key=lambda e: (e["rank"], e["stopped_channel"], e["origin"]))
         res = OP.simulate(xs, g, dtype, strategy=strategy, seed=0, inplace=inplace,
@@ -110,7 +111,8 @@ def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", 
     else:
         T.all_gather(comm, send, recv, sendcount=count)
     rc = comm.sync()
-    ll = comm.status()["last_protocol"] == "LL"
+    proto = comm.status()["last_protocol"]
+    ll = proto in ("LL", "LL128")
     ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), np.asarray(want).view(np.uint8))
     evs = [norm_event(e) for e in comm.events()[ne:]]
     all_evs = [None] * world
@@ -118,7 +120,7 @@ def case_op(comm, rank, world, op, count, dtype, faults=(), strategy="BALANCE", 
     oks = [None] * world
     dist.all_gather_object(oks, bool(ok))
     out = {"op": op, "N": count, "dtype": dtype, "faults": list(faults), "strategy": strategy, "rc": rc,
-           "inplace": inplace, "ok": all(oks), "protocol": "LL" if ll else "SIMPLE"}
+           "inplace": inplace, "ok": all(oks), "protocol": proto}
     if faults:
         cfg = comm.cfg
         g = Geometry(world, cfg.nchannels, count, E, effective_chunk_bytes(
@@ -276,17 +278,25 @@ def main():
             comm.finalize()
         results.append(case_fullsize(rank, world))
         results.append(case_host(rank, world))
-        # the LL protocol (f3) forced, over the real NVLink path
-        cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=16 * 1024, max_bytes=16 << 20,
-                               protocol="LL")
+        # the line protocols (f3) forced, over the real NVLink path: LL (R-6) and LL128 (R-12)
+        for proto in ("LL", "LL128"):
+            cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=16 * 1024, max_bytes=16 << 20,
+                                   protocol=proto)
+            comm = T.comm_from_env(cfg)
+            for dtype, N in (("bfloat16", 100_003), ("float32", 1 << 16), ("int32", 5)):
+                results.append(case(comm, rank, world, N, dtype, seed=N + 1))
+            results.append(case(comm, rank, world, 77_777, "bfloat16", inplace=True, seed=2))
+            for op in ("reduce_scatter", "all_gather"):
+                results.append(case_op(comm, rank, world, op, 33_333, "bfloat16", seed=4))
+            f = dict(kind="LINK", src_rank=world - 1, channel=1, step=1, chunk=1, byte_offset=4096, poison=1)
+            results.append(case(comm, rank, world, 1 << 19, "bfloat16", [f], "BALANCE", seed=19))
+            comm.finalize()
+        # LL128 at the bench's mid size with the bench's 8 x 16 CTAs (config-5 bucket)
+        cfg = R.config_default(nchannels=8, ctas_per_channel=16, max_bytes=32 << 20, protocol="LL128")
         comm = T.comm_from_env(cfg)
-        for dtype, N in (("bfloat16", 100_003), ("float32", 1 << 16), ("int32", 5)):
-            results.append(case(comm, rank, world, N, dtype, seed=N + 1))
-        results.append(case(comm, rank, world, 77_777, "bfloat16", inplace=True, seed=2))
-        for op in ("reduce_scatter", "all_gather"):
-            results.append(case_op(comm, rank, world, op, 33_333, "bfloat16", seed=4))
-        f = dict(kind="LINK", src_rank=world - 1, channel=1, step=1, chunk=1, byte_offset=4096, poison=1)
-        results.append(case(comm, rank, world, 1 << 19, "bfloat16", [f], "BALANCE", seed=19))
+        results.append(case(comm, rank, world, 12_500_000, "bfloat16", seed=25))
+        f = dict(kind="LINK", src_rank=world - 1, channel=5, step=1, chunk=3, byte_offset=8192, poison=1)
+        results.append(case(comm, rank, world, 12_500_000, "bfloat16", [f], "BALANCE", seed=26))
         comm.finalize()
         # re-probe (f4): LINK fault, HEAL (the library is not told), re-admission by re-probing
         cfg = R.config_default(nchannels=4, ctas_per_channel=2, chunk_bytes=32 * 1024, max_bytes=16 << 20,

@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 import r2inputs
 from oracle import balance as OB
 from oracle import ledger as OL
+from oracle import rerank as ORR
 from oracle import triangulation as OT
 from oracle.geometry import Geometry
 from tests.scenario import effective_chunk_bytes
@@ -82,6 +83,30 @@ def test_chain_and_rollback_match_oracle():
     for k in range(0, 10):
         for mask in itertools.product([False, True], repeat=k):
             assert R.rollback(list(mask)) == OL.rollback(list(mask))
+
+
+def test_rerank_matches_oracle():
+    """r2_rerank (Algorithm 1, reading R-13) == oracle/rerank.py on random
+    rail-failure patterns with and without dead standard links (2000 cases,
+    n = 3..16, K = 1..8) and on every pattern of n = 4, K = 2."""
+    import random
+    rng = random.Random(7)
+    cases = []
+    for combo in itertools.product(range(1, 4), repeat=4):
+        cases.append((4, 2, list(combo), [0] * 4))
+    for _ in range(2000):
+        n, K = rng.randint(3, 16), rng.randint(1, 8)
+        full = (1 << K) - 1
+        rails = [rng.choice([full, full, rng.randint(1, full)]) for _ in range(n)]
+        dead = [rng.choice([0, 0, 0, rng.randint(0, full)]) for _ in range(n)] if rng.random() < 0.5 else [0] * n
+        cases.append((n, K, rails, dead))
+    for n, K, rails, dead in cases:
+        order = list(range(n))
+        random.Random(n * 31 + K).shuffle(order)
+        rs = {u: frozenset(c for c in range(K) if rails[u] >> c & 1) for u in range(n)}
+        dl = {(u, (u + 1) % n, c) for u in range(n) for c in range(K) if dead[u] >> c & 1}
+        want = ORR.rerank(order, rs, ORR.link_cap(rs, dl))
+        assert R.rerank(order, rails, dead) == want, (order, rails, dead)
 
 
 def test_geometry_matches_oracle():

@@ -1,5 +1,6 @@
-"""Parity of the LL (low-latency) protocol (reading R-6)
-through the C ABI, simulated-rank mode: AllReduce / ReduceScatter /
+"""Parity of the line protocols -- LL (reading R-6) and
+LL128 (reading R-12), every test run for both -- through the C ABI,
+simulated-rank mode: AllReduce / ReduceScatter /
 AllGather results bit-exact against oracle Layer 1, failover records equal to
 Layer 2 over the LL step list (oracle/geometry.py ll=True), the alpha-beta
 selection picks LL for latency-bound sizes and SIMPLE for bandwidth-bound
@@ -23,6 +24,11 @@ from paper_2512_25059_b200 import r2ccl as R
 pytestmark = pytest.mark.gpu
 
 AR, RS, AG = "allreduce", "reduce_scatter", "all_gather"
+
+
+@pytest.fixture(params=["LL", "LL128"])
+def proto(request):
+    return request.param
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -68,17 +74,17 @@ def xs_for(op, n, count, dtype, seed):
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
 @pytest.mark.parametrize("n", [2, 3, 4, 8])
 @pytest.mark.parametrize("count", [1, 999, 20_001])
-def test_ll_fault_free_parity(op, dtype, n, count):
-    comm = ll_comm(n)
+def test_ll_fault_free_parity(op, dtype, n, count, proto):
+    comm = ll_comm(n, protocol=proto)
     xs = xs_for(op, n, count, dtype, 3000 + n)
     rc, out = run_any(comm, op, xs, count, dtype)
     assert rc == R.SUCCESS
-    assert comm.status()["last_protocol"] == "LL"
+    assert comm.status()["last_protocol"] == proto
     check_any(op, out, xs, count, dtype, geom(comm, op, count, dtype))
 
 
-def test_ll_inplace_allreduce_and_many_calls():
-    comm = ll_comm(4)
+def test_ll_inplace_allreduce_and_many_calls(proto):
+    comm = ll_comm(4, protocol=proto)
     N, dtype = 50_003, "bfloat16"
     xs = r2inputs.inputs(4, N, dtype, seed=8)
     g = geom(comm, AR, N, dtype)
@@ -91,9 +97,9 @@ def test_ll_inplace_allreduce_and_many_calls():
 @pytest.mark.parametrize("op", [AR, RS, AG])
 @pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
 @pytest.mark.parametrize("dtype", ["bfloat16", "int32"])
-def test_ll_link_fault_events_exact(op, strategy, dtype):
+def test_ll_link_fault_events_exact(op, strategy, dtype, proto):
     n, K, W, count = 4, 4, 2, 30_001
-    comm = sim_comm(n, K, W, 4096, strategy=strategy, protocol="LL")
+    comm = sim_comm(n, K, W, 4096, strategy=strategy, protocol=proto)
     f = dict(kind="LINK", src_rank=2, channel=1, step=1, chunk=1, byte_offset=1000, poison=1)
     comm.inject_fault(at_seq=1, **f)
     xs = xs_for(op, n, count, dtype, 5)
@@ -109,11 +115,12 @@ def test_ll_link_fault_events_exact(op, strategy, dtype):
 
 
 @pytest.mark.parametrize("op", [AR, AG])
-def test_ll_brute_force_small(op):
+def test_ll_brute_force_small(op, proto):
     """Every (rank, channel, q) LINK fault on n=3, K=3, m=2 with the LL step
-    list (the unpack step is LOCAL: never a fault point)."""
+    list (the unpack step is LOCAL: never a fault point).  Under LL128 a
+    4-vector chunk is one line, so Balance parts share it (whole-line writes)."""
     n, K, W = 3, 3, 2
-    comm = sim_comm(n, K, W, chunk_bytes=64, strategy="BALANCE", protocol="LL")
+    comm = sim_comm(n, K, W, chunk_bytes=64, strategy="BALANCE", protocol=proto)
     count = (n * K if op == AR else K) * 2 * 16
     xs = xs_for(op, n, count, "int32", 77)
     g = geom(comm, op, count, "int32")
@@ -140,12 +147,12 @@ def test_ll_brute_force_small(op):
 
 
 def test_auto_selects_by_alpha_beta():
-    """AUTO: LL for a latency-bound size, SIMPLE for a bandwidth-bound one;
-    results bit-identical between the protocols."""
+    """AUTO: LL for a latency-bound size, LL128 for a mid size, SIMPLE above
+    the line scratch (ll_max_bytes); results bit-identical between protocols."""
     n = 4
-    comm = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="AUTO")
+    comm = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="AUTO", ll_max_bytes=8 << 20)
     simple = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="SIMPLE")
-    for N, want in ((4096, "LL"), (16 << 20, "SIMPLE")):
+    for N, want in ((4096, "LL"), (2 << 20, "LL128"), (8 << 20, "SIMPLE")):
         xs = r2inputs.inputs(n, N, "bfloat16", seed=N)
         rc, out = run(comm, xs, "bfloat16")
         assert rc == R.SUCCESS and comm.status()["last_protocol"] == want, N
@@ -156,18 +163,18 @@ def test_auto_selects_by_alpha_beta():
         assert same_bits(out[0], y)
 
 
-def test_ll_too_large_is_invalid():
-    comm = sim_comm(2, 2, 1, 4096, max_bytes=1 << 20, protocol="LL", ll_max_bytes=4096)
+def test_ll_too_large_is_invalid(proto):
+    comm = sim_comm(2, 2, 1, 4096, max_bytes=1 << 20, protocol=proto, ll_max_bytes=4096)
     x = torch.zeros((2, 1 << 16), dtype=torch.float32, device="cuda")
     with pytest.raises(Exception):
         comm.allreduce(x.data_ptr(), x.data_ptr(), 1 << 16, R.FLOAT32)
 
 
-def test_ll_no_backup_releases_stream():
+def test_ll_no_backup_releases_stream(proto):
     """A chain exhausted mid-collective under LL: data warps spinning on lines
     that will never arrive are released by the abort; NO_BACKUP reported."""
     n, K, N = 3, 2, 30_000
-    comm = sim_comm(n, K, 1, 8192, strategy="HOT_REPAIR", protocol="LL")
+    comm = sim_comm(n, K, 1, 8192, strategy="HOT_REPAIR", protocol=proto)
     comm.inject_fault(at_seq=1, kind="LINK", src_rank=1, channel=0, step=1, chunk=0, byte_offset=0)
     comm.inject_fault(at_seq=1, kind="LINK", src_rank=1, channel=1, step=2, chunk=0, byte_offset=0, origin_channel=0)
     xs = r2inputs.inputs(n, N, "int32", seed=1)
@@ -177,11 +184,11 @@ def test_ll_no_backup_releases_stream():
     assert comm.status()["last_error"] == R.ERR_NO_BACKUP
 
 
-def test_ll_speculation_with_midcall_fault_many_points():
+def test_ll_speculation_with_midcall_fault_many_points(proto):
     """Healthy static plan (speculative LL publishing) with a fault firing at
     several points of an AllReduce: bit-exact each time."""
     n, K, W, N = 4, 3, 2, 40_000
-    comm = sim_comm(n, K, W, 4096, strategy="BALANCE", protocol="LL")
+    comm = sim_comm(n, K, W, 4096, strategy="BALANCE", protocol=proto)
     xs = r2inputs.inputs(n, N, "bfloat16", seed=12)
     g = geom(comm, AR, N, "bfloat16")
     for t in range(0, g.steps - 1, 2):
@@ -197,11 +204,11 @@ def test_ll_speculation_with_midcall_fault_many_points():
 
 
 @pytest.mark.parametrize("strategy", ["BALANCE", "HOT_REPAIR"])
-def test_ll_inplace_with_fault(strategy):
+def test_ll_inplace_with_fault(strategy, proto):
     """In-place AllReduce under LL with a mid-collective LINK fault in the fused
     final-add step (the staged own shard protects the overwritten input)."""
     n, K, W, N = 4, 3, 2, 40_003
-    comm = sim_comm(n, K, W, 4096, strategy=strategy, protocol="LL")
+    comm = sim_comm(n, K, W, 4096, strategy=strategy, protocol=proto)
     f = dict(kind="LINK", src_rank=1, channel=2, step=n - 1, chunk=1, byte_offset=512, poison=1)
     comm.inject_fault(at_seq=1, **f)
     xs = r2inputs.inputs(n, N, "bfloat16", seed=44)

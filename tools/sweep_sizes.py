@@ -35,8 +35,9 @@ def main():
     ap.add_argument("--dtypes", default="bf16,fp32")
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--sim-ranks", type=int, default=8)
-    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
+    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL", "LL128"])
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--ll-max", type=int, default=128 << 20, help="ll_max_bytes (line-protocol scratch)")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = 512 sim / 256 GPUs, as bench.py)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -55,7 +56,7 @@ def main():
     else:
         dist.init_process_group("gloo")
         comm = T.comm_from_env(R.config_default(nchannels=8, ctas_per_channel=W, max_bytes=maxb, protocol=a.protocol,
-                                                ll_max_bytes=min(maxb, 32 << 20), threads_per_cta=a.threads or 256))
+                                                ll_max_bytes=min(maxb, a.ll_max), threads_per_cta=a.threads or 256))
         os.environ["NCCL_NVLS_ENABLE"] = "0"
         saved = os.dup(1)
         os.dup2(2, 1)
