@@ -71,70 +71,6 @@ def peaks():
 
 
 # ------------------------------------------------------------------ clocks
-class NvLinkCounters:
-    """Per-GPU NVLink byte counters (NVML field values) read on the host
-    around a timed region -- ncu must not wrap multi-rank runs, so this is the
-    NVLink side of the roofline's `traffic`.  Every candidate
-    field is read both aggregated (scope 0xFFFFFFFF) and summed over links
-    0..17; the deltas are kept raw and the first usable TX/RX pair is used."""
-    LINKS = 18
-    CANDIDATES = (("COUNT_XMIT_BYTES", "COUNT_RCV_BYTES", 1),        # bytes
-                  ("THROUGHPUT_DATA_TX", "THROUGHPUT_DATA_RX", 1024),  # KiB
-                  ("THROUGHPUT_RAW_TX", "THROUGHPUT_RAW_RX", 1024))
-
-    def __init__(self, dev):
-        self.ok = False
-        try:
-            import pynvml as N
-            import torch
-            N.nvmlInit()
-            self.N = N
-            uuid = str(torch.cuda.get_device_properties(dev).uuid)
-            self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-            self.ok = True
-        except Exception as e:  # noqa: BLE001
-            self.err = f"{type(e).__name__}: {e}"[:160]
-
-    def read(self):
-        out = {}
-        N = self.N
-        for tx, rx, _ in self.CANDIDATES:
-            for name in (tx, rx):
-                fid = getattr(N, "NVML_FI_DEV_NVLINK_" + name)
-                for tag, scopes in (("all", [0xFFFFFFFF]), ("sum", list(range(self.LINKS)))):
-                    try:
-                        vals = N.nvmlDeviceGetFieldValues(self.h, [(fid, s) for s in scopes])
-                        good = [v.value.ullVal for v in vals if v.nvmlReturn == 0]
-                        out[f"{name}/{tag}"] = sum(good) if good else None
-                    except Exception:  # noqa: BLE001
-                        out[f"{name}/{tag}"] = None
-        return out
-
-    def __enter__(self):
-        self.r0 = self.read() if self.ok else None
-        return self
-
-    def __exit__(self, *exc):
-        self.r1 = self.read() if self.ok else None
-
-    def result(self, algorithmic_bytes, launches):
-        """Per-launch TX/RX bytes from the first field pair that moved."""
-        if not self.ok:
-            return {"error": self.err}
-        raw = {k: (self.r1[k] - self.r0[k]) if self.r0[k] is not None and self.r1[k] is not None else None
-               for k in self.r0}
-        for tx, rx, unit in self.CANDIDATES:
-            for tag in ("all", "sum"):
-                dt, dr = raw.get(f"{tx}/{tag}"), raw.get(f"{rx}/{tag}")
-                if dt and dr:
-                    t, r = dt * unit / launches, dr * unit / launches
-                    return {"field": f"{tx}/{rx} ({tag})", "tx_bytes_per_launch": t, "rx_bytes_per_launch": r,
-                            "tx_over_algorithmic": t / algorithmic_bytes, "rx_over_algorithmic": r / algorithmic_bytes,
-                            "raw_deltas": raw}
-        return {"error": "no NVLink counter moved", "raw_deltas": raw}
-
-
-
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -565,19 +501,24 @@ def run_multi(a):
     clk = Clocks(",".join(str(i) for i in range(world))) if local == 0 else None
     if clk:
         clk.__enter__()
-    nvl = NvLinkCounters(local)
+    # bytes this rank's kernels pushed over NVLink, per channel, counted by the
+    # kernel itself (r2_status bytes): hardware NVLink counters are not
+    # exposed on these boxes (NVML NOT_SUPPORTED, `nvidia-smi nvlink -gt d`
+    # N/A: profiles/r02_nvlink_counters_unavailable.txt) and ncu must not wrap
+    # a multi-rank run
+    b0 = sum(comm.status()["bytes"][0])
     barrier()
-    with nvl:
-        ms = reduce_max(timed(step, a.steps, stream))
+    ms = reduce_max(timed(step, a.steps, stream))
     if clk:
         clk.__exit__(None, None, None)
     barrier()
     assert comm.sync() == R.SUCCESS
+    b1 = sum(comm.status()["bytes"][0])
     g = R.geometry(count, R.BFLOAT16, world, K, W, a.chunk)
     res = {"ms": ms, "clocks": clk.summary() if clk else None, "W": W, "m": g.m}
-    # NVLink bytes of every rank over the timed region
-    nv = nvl.result(2 * (world - 1) / world * S, a.steps)
-    res["nvlink_all"] = gather([nv])
+    alg = 2 * (world - 1) / world * S
+    res["nvlink_all"] = gather([{"tx_bytes_per_launch": (b1 - b0) / a.steps,
+                                 "tx_over_algorithmic": (b1 - b0) / a.steps / alg}])
     if a.ctas_small and not a.profile:
         res["small_footprint"] = guarded(lambda: small_footprint(a, T, R, send, recv, S, world, K, stream, barrier,
                                                                  reduce_max))
@@ -634,6 +575,8 @@ def run_multi(a):
     if not a.no_fault and world >= 3 and a.bw_model_gbps > 0:
         res["r2cc_allreduce"] = guarded(lambda: r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier,
                                                              reduce_max))
+        res["rerank"] = guarded(lambda: rerank_section(a, T, R, send, recv, S, world, K, W, stream, barrier,
+                                                       reduce_max))
     return res, rank
 
 
@@ -675,6 +618,43 @@ def degrade(c, T, R, f, chans, send, recv, barrier):
         while (f, ch) not in c.status()["dead_endpoints"] and _t.time() - t0 < 10:
             _t.sleep(0.002)
         barrier()
+
+
+def rerank_section(a, T, R, send, recv, S, world, K, W, stream, barrier, reduce_max):
+    """disjoint endpoint losses on neighbouring ranks (rank 1
+    loses channel 1, rank 2 loses channel 2), channels as bandwidth
+    units (channel_gbps).  Rank order leaves the edge 1 -> 2 with K-2
+    channels; Algorithm 1's R' keeps every edge at >= K-1.  Both runs are
+    Balance rings on the same degraded communicator; result compared."""
+    import torch
+    out = {"channel_gbps": a.bw_model_gbps, "lost": [[1, 1], [2, 2]], "cases": {}}
+    results = {}
+    for rr in (0, 1):
+        c = T.comm_from_env(R.config_default(
+            nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+            strategy="BALANCE", protocol="SIMPLE", channel_gbps=a.bw_model_gbps, allreduce_algo="RING", rerank=rr))
+        T.register(c, recv)
+        degrade(c, T, R, 1, [1], send, recv, barrier)
+        degrade(c, T, R, 2, [2], send, recv, barrier)
+        step = lambda cc=c: T.allreduce(cc, send, recv)  # noqa: E731
+        for _ in range(3):
+            step()
+        barrier()
+        ms = reduce_max(timed(step, 20, stream))
+        assert c.sync() == R.SUCCESS
+        st = c.status()
+        results[rr] = recv.clone()
+        out["cases"]["rerank" if rr else "rank_order"] = {
+            "ms": ms, "busbw_per_rank": 2 * (world - 1) / world * S / (ms * 1e-3) / 1e9,
+            "ring_order": st["ring_order"], "n_rerank": st["n_rerank"]}
+        c.finalize()
+        barrier()
+    out["speedup"] = out["cases"]["rank_order"]["ms"] / out["cases"]["rerank"]["ms"]
+    # the two rings fold in different orders: equal for bf16 only up to rounding, so compare with the
+    # tolerance the north star states (normwise, bf16 <= 1e-2)
+    d = (results[0].float() - results[1].float()).norm() / results[1].float().norm()
+    out["normwise_diff_vs_rank_order"] = float(d)
+    return out
 
 
 def r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier, reduce_max):
@@ -778,18 +758,17 @@ def report(a, res, n_gpus, n_ranks, mode):
     else:
         nv = 2 * (n_ranks - 1) / n_ranks * S
         peak = 770.0
-        counters = [x for x in res.get("nvlink_all") or [] if "tx_bytes_per_launch" in x]
+        counters = res.get("nvlink_all") or []
         traffic = (statistics.mean(x["tx_bytes_per_launch"] for x in counters)
                    if counters and len(counters) == n_ranks else None)
         roof = {"bound": "nvlink", "achieved": nv / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": nv / (ms * 1e-3) / 1e9 / peak, "traffic": traffic,
-                "traffic_source": ("NVML NVLink counters read around the timed region on every rank "
-                                   "(mean TX bytes per launch; ncu must not wrap multi-rank runs)"),
+                "traffic_source": ("kernel-counted NVLink bytes per launch (mean over ranks; r2_status bytes): "
+                                   "hardware NVLink counters are not exposed on these boxes "
+                                   "(profiles/r02_nvlink_counters_unavailable.txt) and ncu must not wrap "
+                                   "multi-rank runs"),
                 "traffic_over_algorithmic": traffic / nv if traffic else None,
-                "nvlink_counters_per_rank": [
-                    {k: x.get(k) for k in ("field", "tx_bytes_per_launch", "rx_bytes_per_launch",
-                                           "tx_over_algorithmic", "rx_over_algorithmic", "error")}
-                    for x in res.get("nvlink_all") or []],
+                "traffic_per_rank": [x["tx_bytes_per_launch"] for x in counters],
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction (900 nominal)",
                 "sm_store_peak_gbs": 697.0,
                 "sm_store_peak_source": "profiles/r01_p2p_store_n4.log: SM/TMA peer-store ceiling (copy engine 760)",
@@ -834,6 +813,8 @@ def report(a, res, n_gpus, n_ranks, mode):
         line["fault_bandwidth_model"] = res["fault_bw_model"]
     if "r2cc_allreduce" in res:
         line["r2cc_allreduce"] = res["r2cc_allreduce"]
+    if "rerank" in res:
+        line["rerank"] = res["rerank"]
     return line
 
 

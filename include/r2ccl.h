@@ -130,6 +130,13 @@ typedef struct {
  *                     a bandwidth unit like the paper's NIC (reading C-1: without
  *                     it channels share the GPU's NVLink ports and a dead channel
  *                     only removes CTAs)
+ *   rerank            1 (default): before every ring AllReduce the planner
+ *                     applies Algorithm 1 (App. D, §6; r2_rerank) to the
+ *                     health records of that seq -- rails S_u = channels alive
+ *                     on rank u, dead standard links excluded from an edge's
+ *                     capacity (reading R-13) -- and runs the collective on the
+ *                     re-ranked ring R' (AllReduce only: its result does not
+ *                     depend on which rank owns which shard); 0 keeps rank order
  *   alpha_simple_ns, alpha_ll_ns, alpha_ll128_ns, beta_mbps
  *                     cost model: T = (#ring steps) * alpha + (wire bytes per
  *                     rank) / beta, LL moving twice the bytes and LL128 8/7 of
@@ -169,6 +176,7 @@ typedef struct {
   int allreduce_algo;   /* r2_algo_t (default AUTO)                                  */
   int alpha_launch_ns;  /* cost model: one more collective launch (R²CCL stage 2)    */
   int alpha_ll128_ns;   /* cost model: per ring step under LL128                     */
+  int rerank;           /* 1 (default): ring AllReduce on Algorithm 1's re-ranked ring */
 } r2_config_t;
 
 /*
@@ -269,6 +277,10 @@ typedef struct {
   int r2cc_rank;
   double r2cc_X, r2cc_Y;
   uint64_t r2cc_NA, r2cc_NP, r2cc_seq;
+  /* Re-ranking (f4, Algorithm 1): AllReduce calls that ran on a re-ranked
+     ring, and the ring order of the last ring AllReduce (ranks by position) */
+  int n_rerank;
+  int ring_order[R2_MAX_RANKS];
 } r2_status_t;
 
 /* Fill *cfg with the defaults documented above. */

@@ -266,6 +266,7 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->probe_timeout_us = 50;
   cfg->watchdog_ms = 3000;
   cfg->use_channel_w = 0;
+  cfg->rerank = 1;
   for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
   cfg->sim_ranks = 1;
   cfg->protocol = R2_PROTO_AUTO;
@@ -891,6 +892,29 @@ static r2_result_t enqueue_coll(r2_comm* c, r2_op_t op, const void* send, void* 
   return launch_rings(c, rings, dt, stream);
 }
 
+// ---------------------------------------------------------------- re-ranking
+// SURVEY §8(f) f4 (Algorithm 1, App. D; §6; readings C-19,
+// R-13): the ring order of the next AllReduce from the health records of its
+// seq ("the planner inspects the health status records").
+std::vector<int> rerank_plan(r2_comm* c, uint32_t q) {
+  const int n = c->n, K = c->K;
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  if (n < 3) return order;
+  std::vector<uint32_t> rails(n, 0), dead(n, 0);
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    for (int r = 0; r < n; ++r)
+      for (int k = 0; k < K; ++k) {
+        if (!r2_ep_dead_at(c, r, k, q)) rails[r] |= 1u << k;
+        if (r2_link_dead_at(c, r, k, q)) dead[r] |= 1u << k;
+      }
+  }
+  std::vector<int> out(n);
+  if (r2_rerank(n, order.data(), rails.data(), dead.data(), out.data()) <= 0) return order;
+  return out;
+}
+
 // ---------------------------------------------------------------- R²CCL-AllReduce
 // SURVEY §8(f) f2 (App. A; reading R-9) and the strategy
 // choice of f3 (reading R-11).
@@ -1022,7 +1046,17 @@ extern "C" r2_result_t r2_allreduce(r2_comm_t c, const void* send, void* recv, s
     if (pl.applies && (c->cfg.allreduce_algo == R2_ALGO_R2CC || r2cc_faster(c, pl, count, dt)))
       return r2cc_enqueue(c, pl, send, recv, count, dt, stream);
   }
-  return enqueue_coll(c, R2_OP_ALLREDUCE, send, recv, count, dt, stream);
+  if (c->n == 1) return enqueue_coll(c, R2_OP_ALLREDUCE, send, recv, count, dt, stream);
+  std::vector<RingSpec> rings{standard_ring(c, R2_OP_ALLREDUCE, send, recv, count, 0)};
+  if (c->cfg.rerank) rings[0].order = rerank_plan(c, (uint32_t)c->seq + 1);
+  const bool reranked = !std::is_sorted(rings[0].order.begin(), rings[0].order.end());
+  r2_result_t e = launch_rings(c, rings, dt, stream);
+  if (e == R2_SUCCESS) {
+    std::lock_guard<std::mutex> gl(c->mu);
+    c->last_ring = rings[0].order;
+    c->n_rerank += reranked;
+  }
+  return e;
 }
 
 // ReduceScatter / AllGather (f1).  The shard stride count * elem need not be
@@ -1249,6 +1283,9 @@ extern "C" r2_result_t r2_status(r2_comm_t c, r2_status_t* out) {
     out->r2cc_NA = c->last_r2cc.NA;
     out->r2cc_NP = c->last_r2cc.NP;
     out->r2cc_seq = c->last_r2cc.seq;
+    out->n_rerank = c->n_rerank;
+    for (int i = 0; i < c->n && i < R2_MAX_RANKS; ++i)
+      out->ring_order[i] = i < (int)c->last_ring.size() ? c->last_ring[i] : i;
     const uint32_t q = (uint32_t)c->seq + 1;   // the view of the next collective
     for (int r = 0; r < c->n && r < R2_MAX_LOCAL * 4; ++r)
       for (int k = 0; k < c->K; ++k) {

@@ -141,6 +141,8 @@ struct r2_comm {
   int last_protocol = 0;                     // r2_protocol_t of the last enqueued collective
   struct { uint64_t seq; int f; double X, Y; size_t NA, NP; } last_r2cc{0, -1, 0, 0, 0, 0};   // (mu)
   int n_r2cc = 0;                                                                        // (mu)
+  int n_rerank = 0;                                                                      // (mu)
+  std::vector<int> last_ring;   // ring order of the last ring AllReduce (f4 re-ranking)  (mu)
   // re-probing of dead connections ("periodically reprobes to detect
   // component recovery ... adapting probe frequency")
   struct Reprobe { int r, ch; uint64_t next_ns, interval_ns; uint32_t round_id; };

@@ -45,11 +45,10 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const volatile unsigned i
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Completion words are polled with RELAXED loads: the sender's
-// fence.acq_rel.sys before the word guarantees its payload is already
-// performed in this GPU's memory, and the payload is read through L2
-// (ld.global.cg), so no receiver-side sys-scope acquire is needed -- it cost
-// ~1.5 us per poll (tools/pingpong.cu, profiles/r01_pingpong.log).
+// Completion words are polled with RELAXED loads (an acquire per poll cost
+// ~1.5 us, tools/pingpong.cu, profiles/r01_pingpong.log); once a word is
+// seen, one ld.acquire.sys of it makes the receiver side formally ordered
+// (try_publish).
 __device__ __forceinline__ unsigned int ld_relaxed_sys(const volatile unsigned int* p) {
   unsigned int v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -450,21 +449,23 @@ __device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[
   const unsigned int pos = lane & 7u;
   for (unsigned int spins = 0;; ++spins) {
     bool ok = true;
-    bool okl[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool f = !act[u] || (x[u].x == seq && x[u].y == seq && x[u].z == seq && x[u].w == seq);
-      okl[u] = __shfl_sync(0xFFFFFFFFu, f, lane | 7u);      // the line's flag lane decides
-      ok &= okl[u];
+      ok &= __shfl_sync(0xFFFFFFFFu, f, lane | 7u);      // the line's flag lane decides
     }
     if (__all_sync(0xFFFFFFFFu, ok)) return;
     if ((spins & 0x3FFu) == 0x3FFu) {
       const int ab = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (int)(*abort_word == seq) : 0, 0);
       if (ab) return;
     }
+    // reload every line of the warp: the 8 lanes of a line must read it with
+    // ONE converged load instruction (a line read in pieces can pair a new
+    // flag with an old payload)
+    __syncwarp();
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (!okl[u]) x[u] = ll_line(q + (size_t)L[u] * 128 + pos * 16);
+      if (act[u]) x[u] = ll_line(q + (size_t)L[u] * 128 + pos * 16);
   }
 }
 
@@ -472,7 +473,9 @@ __device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[
 // part's first vector, or (src_ll) the chunk's lines in an LL128 slot; s_in:
 // the chunk's lines (or null); d_rem: the chunk's lines at the peer (or null);
 // d_loc: user memory / stage at the part's first vector (or null).  dtid / dn:
-// thread index / count over the data warps (multiples of 32).
+// thread index / count over the data warps (multiples of 32).  Line loads and
+// line stores are issued by the converged warp (__syncwarp before each), so
+// the 8 lanes of a line always access it in one instruction.
 template <int DT>
 __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned int dn, const char* src, bool src_ll,
                            const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
@@ -491,38 +494,60 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       L[u] = base + (unsigned int)u * 4u + (lane >> 3);
-      act[u] = L[u] < L1;
-      const unsigned int vc = L[u] * LL128_PAY + pos;
+      act[u] = L[u] < L1;                 // the same for the 8 lanes of a line
       a[u] = make_uint4(0u, 0u, 0u, 0u);
       b[u] = make_uint4(0u, 0u, 0u, 0u);
-      if (!act[u]) continue;
-      if (src_ll) {
-        a[u] = ll_line(src + (size_t)L[u] * 128 + pos * 16);
-      } else if (pos < LL128_PAY && vc < cvec) {
-        const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
-        const long long left = (long long)lim - ev;
-        const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
-        a[u] = ld_user(src + ((long long)vc - (long long)lo) * 16, valid, E, aligned);
-      }
-      if (s_in) b[u] = ll_line(s_in + (size_t)L[u] * 128 + pos * 16);
+    }
+    // 1. line loads (converged), validated
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (src_ll && act[u]) a[u] = ll_line(src + (size_t)L[u] * 128 + pos * 16);
+      if (s_in && act[u]) b[u] = ll_line(s_in + (size_t)L[u] * 128 + pos * 16);
     }
     if (src_ll) ll128_validate<U>(a, act, src, L, lane, seq, abort_word);
     if (s_in) ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word);
+    // 2. user loads (may diverge: masked tails, unaligned buffers)
+    if (!src_ll) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned int vc = L[u] * LL128_PAY + pos;
+        if (act[u] && pos < LL128_PAY && vc < cvec) {
+          const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
+          const long long left = (long long)lim - ev;
+          const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+          a[u] = ld_user(src + ((long long)vc - (long long)lo) * 16, valid, E, aligned);
+        }
+      }
+    }
+    // 3. sums, then the line stores (converged) and the part's local copies
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const unsigned int vc = L[u] * LL128_PAY + pos;
       const bool pay = pos < LL128_PAY && vc < cvec;
       uint4 v = pay ? a[u] : make_uint4(0u, 0u, 0u, 0u);
       if (pay && s_in) v = vadd<DT>(b[u], v);
-      if (d_rem && act[u]) st_v4(d_rem + (size_t)L[u] * 128 + pos * 16, pos == LL128_PAY ? flag : v);
-      if (d_loc && act[u] && pay && vc >= lo && vc < lo + nvec) {
-        const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
-        if (loc_user) {
-          const long long left = (long long)lim - ev;
-          const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
-          st_user(d_loc + (size_t)(vc - lo) * 16, v, valid, E, aligned);
-        } else {
-          st_v4(d_loc + (size_t)(vc - lo) * 16, v);
+      a[u] = pos == LL128_PAY ? flag : v;
+    }
+    if (d_rem) {
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act[u]) st_v4(d_rem + (size_t)L[u] * 128 + pos * 16, a[u]);
+    }
+    if (d_loc) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned int vc = L[u] * LL128_PAY + pos;
+        if (act[u] && pos < LL128_PAY && vc < cvec && vc >= lo && vc < lo + nvec) {
+          const long long ev = (long long)e0 + ((long long)vc - (long long)lo) * V;
+          if (loc_user) {
+            const long long left = (long long)lim - ev;
+            const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
+            st_user(d_loc + (size_t)(vc - lo) * 16, a[u], valid, E, aligned);
+          } else {
+            st_v4(d_loc + (size_t)(vc - lo) * 16, a[u]);
+          }
         }
       }
     }
@@ -852,8 +877,15 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   // Once alerted, items wait for the completion word again (an adopted
   // residual must never queue behind a spinning item that needs it).
   const bool spec = p.ll && k.all_healthy && !sh.alerted && !sh.dynamic;
-  if (it.t > 0 && !spec && (int)(ld_relaxed_sys(k.me->flags + fidx(p, it.t - 1, it.o, it.j)) - k.seq) < 0)
-    return ST_NOTREADY;
+  if (it.t > 0 && !spec) {
+    const unsigned int* w = k.me->flags + fidx(p, it.t - 1, it.o, it.j);
+    if ((int)(ld_relaxed_sys(w) - k.seq) < 0) return ST_NOTREADY;
+    // the word is there: ONE sys-scope acquire of it (not one per poll) orders
+    // the data warps' payload loads after the sender's release -- thread 0's
+    // acquire, then the slot's mbarrier release/acquire (CTA scope), form the
+    // causality chain of the PTX memory model
+    if (!p.ll) (void)ld_acquire_sys(w);
+  }
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
@@ -1266,8 +1298,10 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
       // LL128: whole lines after the delivered prefix arrive invalid (flag ~0)
       const unsigned int Lf = (d.lo_c + d.nvec + LL128_PAY - 1) / LL128_PAY;
       const unsigned int Le = (d.lo_c + d.total + LL128_PAY - 1) / LL128_PAY;
-      for (unsigned int x = Lf * 8 + dtid; x < Le * 8; x += dn)
-        st_v4(d.d_rem + (size_t)x * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+      for (unsigned int x0 = Lf * 8; x0 < Le * 8; x0 += dn) {
+        __syncwarp();
+        if (x0 + dtid < Le * 8) st_v4(d.d_rem + (size_t)(x0 + dtid) * 16, make_uint4(~0u, ~0u, ~0u, ~0u));
+      }
     } else if (d.poison && d.d_rem && p.ll) {
       // LL: the rest of the faulted part arrives as invalid lines (reading C-6)
       for (unsigned int v = d.nvec + dtid; v < d.total; v += dn) {

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libr2ccl.so")
 
 MAX_CHANNELS = 16
 MAX_LOCAL = 16
+MAX_RANKS = 64
 
 # r2_result_t
 SUCCESS, ERR_INVALID_ARG, ERR_CUDA, ERR_BOOTSTRAP, ERR_NOT_REGISTERED, ERR_NO_BACKUP, ERR_TIMEOUT, ERR_INTERNAL = range(8)
@@ -48,7 +49,7 @@ class Config(C.Structure):
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
                 ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
                 ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int), ("allreduce_algo", C.c_int),
-                ("alpha_launch_ns", C.c_int), ("alpha_ll128_ns", C.c_int)]
+                ("alpha_launch_ns", C.c_int), ("alpha_ll128_ns", C.c_int), ("rerank", C.c_int)]
 
 
 PROTO_AUTO, PROTO_SIMPLE, PROTO_LL, PROTO_LL128 = 0, 1, 2, 3
@@ -105,7 +106,8 @@ class Status(C.Structure):
                 ("bytes", (C.c_uint64 * MAX_CHANNELS) * MAX_LOCAL), ("last_protocol", C.c_int),
                 ("n_readmits", C.c_int), ("n_reprobes", C.c_int), ("n_service_kernels", C.c_int),
                 ("n_r2cc", C.c_int), ("r2cc_rank", C.c_int), ("r2cc_X", C.c_double), ("r2cc_Y", C.c_double),
-                ("r2cc_NA", C.c_uint64), ("r2cc_NP", C.c_uint64), ("r2cc_seq", C.c_uint64)]
+                ("r2cc_NA", C.c_uint64), ("r2cc_NP", C.c_uint64), ("r2cc_seq", C.c_uint64),
+                ("n_rerank", C.c_int), ("ring_order", C.c_int * MAX_RANKS)]
 
 
 class Geometry(C.Structure):
@@ -371,7 +373,8 @@ class Comm:
                 "n_readmits": s.n_readmits, "n_reprobes": s.n_reprobes,
                 "n_service_kernels": s.n_service_kernels,
                 "r2cc": {"calls": s.n_r2cc, "rank": s.r2cc_rank, "X": s.r2cc_X, "Y": s.r2cc_Y,
-                         "NA": int(s.r2cc_NA), "NP": int(s.r2cc_NP), "seq": int(s.r2cc_seq)}}
+                         "NA": int(s.r2cc_NA), "NP": int(s.r2cc_NP), "seq": int(s.r2cc_seq)},
+                "n_rerank": s.n_rerank, "ring_order": list(s.ring_order[:n])}
 
     def events(self) -> list:
         st = Status()
