@@ -133,8 +133,8 @@ typedef struct {
  *   rerank            1 (default): before every ring AllReduce the planner
  *                     applies Algorithm 1 (App. D, §6; r2_rerank) to the
  *                     health records of that seq -- rails S_u = channels alive
- *                     on rank u, dead standard links excluded from an edge's
- *                     capacity (reading R-13) -- and runs the collective on the
+ *                     on rank u; a neighbour pair with no live link left has
+ *                     capacity 0 (reading R-13) -- and runs the collective on the
  *                     re-ranked ring R' (AllReduce only: its result does not
  *                     depend on which rank owns which shard); 0 keeps rank order
  *   alpha_simple_ns, alpha_ll_ns, alpha_ll128_ns, beta_mbps
@@ -456,7 +456,8 @@ void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
  * ring order (a permutation of ranks 0..n-1); rails[u]: bitmask of the
  * channels whose endpoint on rank u is alive (the rail set S_u, reading
  * C-1); dead_links[u] (may be NULL): channels whose standard link u -> u+1
- * mod n is dead (reading R-13: an edge's capacity excludes them).  Writes
+ * mod n is dead (reading R-13: an edge whose links are dead on every common
+ * channel has capacity 0, else |S_u ∩ S_v|).  Writes
  * R' to ring_out[0..n) (caller-owned).  Returns the number of relocations,
  * or -1 on invalid arguments (n outside 1..R2_MAX_RANKS, NULL pointers). */
 int r2_rerank(int n, const int* ring_in, const uint32_t* rails, const uint32_t* dead_links, int* ring_out);

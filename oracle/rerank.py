@@ -9,11 +9,12 @@ connectivity.  This targeted repair modifies only the problematic edges".
 
 On the box (SURVEY C-1) a rail is a channel: S_u = the channels whose
 endpoint on rank u is alive.  The capacity of the ring edge (u, v) is
-|S_u ∩ S_v| exactly as in Algorithm 1; reading R-13 generalises
-it to cap(u, v) = |{c ∈ S_u ∩ S_v : link (u, v, c) alive}| so that a ring
-neighbour pair whose direct links are dead is bridged like a rail mismatch
-(the 2-hop relay through a proxy GPU, at ring level).  With no dead
-link the two are identical.
+|S_u ∩ S_v| exactly as in Algorithm 1; reading R-13 adds one
+case: a neighbour pair with no live link left on any common channel has
+capacity 0 (no direct path), so it is bridged like an empty rail
+intersection -- the 2-hop relay through a proxy GPU at ring level.
+Partly dead links leave the capacity |S_u ∩ S_v| (Balance handles them, as
+for a single NIC failure); with no dead link the two are identical.
 
 Readings (SURVEY C-19, SPEC S:643 vs S:632): the bridge scan visits
 w ∈ R' \\ {u, v} in R' index order from position 0 (this reproduces SPEC's
@@ -42,9 +43,12 @@ def intersect_cap(rails: dict[int, frozenset]) -> Callable[[int, int], int]:
 
 
 def link_cap(rails: dict[int, frozenset], dead_links: set) -> Callable[[int, int], int]:
-    """Reading R-13: channels alive at both endpoints whose link u -> v is
-    alive; dead_links holds (u, v, c)."""
-    return lambda u, v: sum(1 for c in rails[u] & rails[v] if (u, v, c) not in dead_links)
+    """Reading R-13: |S_u ∩ S_v|, or 0 when the link u -> v is dead on every
+    common channel; dead_links holds (u, v, c)."""
+    def cap(u, v):
+        common = rails[u] & rails[v]
+        return len(common) if any((u, v, c) not in dead_links for c in common) else 0
+    return cap
 
 
 def find_candidates(order: Sequence[int], cap: Callable[[int, int], int], B: int) -> list[tuple[int, int]]:

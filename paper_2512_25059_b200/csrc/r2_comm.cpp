@@ -47,7 +47,8 @@ ArenaLayout make_layout(int n, int K, int W, size_t chunk, size_t max_bytes, siz
     const size_t shard = std::max<size_t>(align_up(std::min(ll_max_bytes, max_bytes), q) / n, 16 * K);
     const size_t slice = shard / K;
     const size_t mmax = std::max<size_t>((size_t)W, (slice + chunk - 1) / chunk) + 1;
-    L.ll_slot_bytes = std::max<size_t>(2 * shard, (size_t)K * ((slice + 111) / 112 + mmax) * 128);
+    // 128-byte multiple: every slot (and so every LL128 line) starts 128-byte aligned
+    L.ll_slot_bytes = align_up(std::max<size_t>(2 * shard, (size_t)K * ((slice + 111) / 112 + mmax) * 128), 128);
   }
   const int steps = n > 1 ? 2 * n - 1 : 1;     // + the LL unpack step
   size_t off = 0;
@@ -813,6 +814,18 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
     for (auto& rc : c->readmit_pending) r2_declare_conn_repaired(c, rc.first, rc.second, seq);
     c->readmit_pending.clear();
     if ((!repairs.empty() || readmit) && r2_push_health(c) != 0) return R2_ERR_CUDA;
+    // speculation (line protocols, reading R-6) only on a ring whose every
+    // connection is healthy for this seq: a static Balance plan anywhere puts
+    // parts of one channel into another channel's lane, and a published
+    // speculative item could then wait (through that lane) on a residual
+    // queued behind it after a mid-call fault
+    for (int i = 0; i < S.nrings; ++i) {
+      const RingInfo& ri = li.ring[i];
+      bool all = true;
+      for (int j = 0; j < ri.n && all; ++j)
+        for (int k = 0; k < ri.K && all; ++k) all = r2_conn_ok_to(c, ri.order[j], ri.next_of(ri.order[j]), ri.chans[k], seq);
+      S.ring[i].spec_ok = all;
+    }
     // a ring connection with no healthy channel left: the chain is exhausted
     for (int i = 0; i < S.nrings; ++i) {
       const RingInfo& ri = li.ring[i];

@@ -249,9 +249,9 @@ extern "C" const char* r2_strerror(r2_result_t r) {
 
 // Algorithm 1 (§6): bridge-based repair of a ring order.
 // Rails of rank u = channels whose endpoint on u is alive; the capacity of
-// the ring edge u -> v is the number of channels alive at both whose link
-// u -> v is alive (reading R-13; only standard links u -> u+1 mod n have link
-// state, reading R-10).  Scan order, tie-breaks and skipped pairs: reading
+// the ring edge u -> v is |S_u ∩ S_v|, or 0 when the link u -> v is dead on
+// every common channel (reading R-13; only standard links u -> u+1 mod n have
+// link state, reading R-10).  Scan order, tie-breaks and skipped pairs: reading
 // C-19 / R-13.
 namespace {
 struct RerankCtx {
@@ -259,8 +259,8 @@ struct RerankCtx {
   const uint32_t* rails;
   const uint32_t* dead_links;
   int cap(int u, int v) const {
-    uint32_t m = rails[u] & rails[v];
-    if (dead_links && v == (u + 1) % n) m &= ~dead_links[u];
+    const uint32_t m = rails[u] & rails[v];
+    if (dead_links && v == (u + 1) % n && (m & ~dead_links[u]) == 0) return 0;   // no direct path left
     return __builtin_popcount(m);
   }
 };

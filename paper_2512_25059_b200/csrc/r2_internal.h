@@ -217,7 +217,9 @@ struct LaunchParams {
   unsigned long long N, Np, shard, slice, chunk;   // elements (N: the whole user buffer)
   unsigned long long sstride, slen;      // shard stride in the user buffers / valid elements per shard
   size_t slot_bytes;
-  int ll;                                // LL protocol (r2ccl.h "Protocols")
+  int ll;                                // 0 SIMPLE, 1 LL, 2 LL128 (r2ccl.h "Protocols")
+  int spec_ok;                           // line protocols: every connection of the ring healthy for this
+                                         // seq (speculative publishing allowed, reading R-6)
   unsigned int lane_ps_per_byte;         // channel bandwidth model: pacing per lane (0 = off)
   size_t ll_slot_bytes;
   unsigned long long watchdog_ns;

@@ -249,7 +249,7 @@ struct Cta {
   bool fault_channel;
   bool own_alive;
   unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
-  bool all_healthy;         // conn_mask covers every channel (LL speculation allowed)
+  bool all_healthy;         // conn_mask covers every channel (O(1) own-item walk)
   int t_act;                // Broadcast: this rank's chain position (sends only at that step); else -1
   const RankPtrs* me;        // this rank's / the ring successor's arena (global peers table)
   const RankPtrs* nx;
@@ -505,9 +505,8 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
       if (src_ll && act[u]) a[u] = ll_line(src + (size_t)L[u] * 128 + pos * 16);
       if (s_in && act[u]) b[u] = ll_line(s_in + (size_t)L[u] * 128 + pos * 16);
     }
-    if (src_ll) ll128_validate<U>(a, act, src, L, lane, seq, abort_word);
-    if (s_in) ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word);
-    // 2. user loads (may diverge: masked tails, unaligned buffers)
+    // 2. user loads (independent of the lines: issued before the validation
+    //    waits on them; may diverge -- masked tails, unaligned buffers)
     if (!src_ll) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -520,6 +519,8 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
         }
       }
     }
+    if (src_ll) ll128_validate<U>(a, act, src, L, lane, seq, abort_word);
+    if (s_in) ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word);
     // 3. sums, then the line stores (converged) and the part's local copies
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -876,7 +877,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   // and an own item's inputs never depend on a later item of the same lane.
   // Once alerted, items wait for the completion word again (an adopted
   // residual must never queue behind a spinning item that needs it).
-  const bool spec = p.ll && k.all_healthy && !sh.alerted && !sh.dynamic;
+  const bool spec = p.ll && p.spec_ok && !sh.alerted && !sh.dynamic;
   if (it.t > 0 && !spec) {
     const unsigned int* w = k.me->flags + fidx(p, it.t - 1, it.o, it.j);
     if ((int)(ld_relaxed_sys(w) - k.seq) < 0) return ST_NOTREADY;

@@ -57,7 +57,8 @@ def case(comm, rank, world, N, dtype, faults=(), strategy="BALANCE", inplace=Fal
     ll = proto in ("LL", "LL128")      # the alpha-beta choice (f3) shapes the step list
     g = Geometry(world, cfg.nchannels, N, E,
                  effective_chunk_bytes(N, world, cfg.nchannels, E, cfg.chunk_bytes, cfg.ctas_per_channel), ll=ll)
-    y = OS.allreduce(xs, g.shard, dtype)
+    # the planner may have re-ranked the ring (f4, reading R-13): fold along its order
+    y = OS.allreduce_ring(xs, comm.status()["ring_order"], g.shard, dtype)
     ok = rc == R.SUCCESS and np.array_equal(host(recv, dtype).view(np.uint8), y.view(np.uint8))
     evs = [norm_event(e) for e in comm.events()[ne:]]
     all_evs = [None] * world

@@ -29,7 +29,7 @@ def setup(cuda_required):
     torch.cuda.set_device(0)
 
 
-def kill(comm, kind, f, c, key):
+def kill(comm, kind, f, c, key, ok=(R.SUCCESS,)):
     """A LOCAL (endpoint) or LINK fault mid-collective, triangulated by the
     monitor; the verdict applies from the next collective on."""
     n = comm.n
@@ -37,7 +37,7 @@ def kill(comm, kind, f, c, key):
     comm.inject_fault(at_seq=s, kind=kind, src_rank=f, channel=c, step=0, chunk=0, byte_offset=0)
     xs = r2inputs.inputs(n, 4096, "int32", seed=c)
     T.allreduce(comm, to_dev(xs, "int32"), poisoned(n, 4096, "int32"), count=4096)
-    assert comm.sync() == R.SUCCESS
+    assert comm.sync() in ok
     t0 = time.time()
     while (f, c) not in comm.status()[key]:
         assert time.time() - t0 < 5, "verdict not applied"
@@ -127,15 +127,17 @@ def test_fault_on_reranked_ring(strategy):
 
 
 def test_all_links_of_a_pair_dead_relay_by_rerank():
-    """Reading R-13: every channel's link 1 -> 2 dies (successive LINK faults;
-    the chain of the last one is exhausted only at the end).  Later
-    AllReduces run on a ring that no longer has 1 and 2 as neighbours (the
-    bridge is the 2-hop relay) instead of failing with NO_BACKUP."""
+    """Reading R-13: every channel's link 1 -> 2 dies (successive LINK faults).
+    While one link is left the ring stays (Balance carries the pair); when
+    the last dies (that collective's chain is exhausted: NO_BACKUP), later
+    AllReduces run on a ring in which 1 and 2 are no longer neighbours (the
+    bridge is the 2-hop relay) instead of failing."""
     n, K = 4, 3
     comm = sim_comm(n, K=K, W=1, chunk_bytes=16 * 1024, max_bytes=16 << 20)
     for c in range(K - 1):
         kill(comm, "LINK", 1, c, "dead_links")
-    # one healthy link left: R' already bridges the pair (cap 1 < B_global 3)
+    assert expected_order(comm) == [0, 1, 2, 3]
+    kill(comm, "LINK", 1, K - 1, "dead_links", ok=(R.SUCCESS, R.ERR_NO_BACKUP))
     order = expected_order(comm)
     assert order[(order.index(1) + 1) % n] != 2
     xs = r2inputs.inputs(n, 30_001, "int32", seed=5)

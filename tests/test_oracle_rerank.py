@@ -120,7 +120,8 @@ def test_rerank_brute_force_small():
 
 def test_link_capacity_bridges_dead_links():
     """Reading R-13: all links 1 -> 2 dead (every channel): the pair is
-    bridged like an empty rail intersection; without dead links link_cap ==
+    bridged like an empty rail intersection; partly dead links leave the
+    ring alone (Balance's case); without dead links link_cap ==
     intersect_cap."""
     n, K = 4, 3
     rails = {u: frozenset(range(K)) for u in range(n)}
@@ -129,6 +130,8 @@ def test_link_capacity_bridges_dead_links():
     assert RR.find_candidates([0, 1, 2, 3], cap, 3) == [(1, 2)]
     out = RR.rerank([0, 1, 2, 3], rails, cap)
     assert RR.min_adjacent_cap(out, cap) == 3 and out == [1, 0, 2, 3]
+    part = RR.link_cap(rails, {(1, 2, c) for c in range(K - 1)})
+    assert part(1, 2) == K and RR.rerank([0, 1, 2, 3], rails, part) == [0, 1, 2, 3]
     assert all(RR.link_cap(rails, set())(u, v) == RR.intersect_cap(rails)(u, v)
                for u in range(n) for v in range(n))
 
