@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-coll", action="store_true", help="skip the standalone ReduceScatter / AllGather section")
-    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL"])
+    ap.add_argument("--protocol", default="AUTO", choices=["AUTO", "SIMPLE", "LL", "LL128"])
     ap.add_argument("--bw-model-gbps", type=int, default=80,
                     help="per-channel bandwidth of the channel-as-NIC fault section (0 = skip; r2ccl.h channel_gbps)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")

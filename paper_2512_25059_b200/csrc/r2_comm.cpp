@@ -315,6 +315,8 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
   c->K = cfg.nchannels;
   c->W = cfg.ctas_per_channel;
   c->threads = cfg.threads_per_cta;
+  c->ll_threads = getenv("R2_LL_THREADS") ? atoi(getenv("R2_LL_THREADS")) : 0;
+  if (c->ll_threads != 0 && (c->ll_threads < 64 || c->ll_threads > 512 || c->ll_threads % 32)) c->ll_threads = 0;
   c->trace = getenv("R2_TRACE") ? atoi(getenv("R2_TRACE")) : 0;
   for (int k = 0; k < c->K; ++k) c->weights[k] = cfg.use_channel_w ? (unsigned)std::max(cfg.channel_w[k], 1) : 1u;
   if (oob) {
@@ -338,7 +340,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     return e;
   };
   if (c->n > 1) {
-    c->max_coop = r2_max_coop_ctas(c->threads);
+    c->max_coop = r2_max_coop_ctas(std::max(c->threads, c->ll_threads));
     if (c->nlocal * c->K * c->W > c->max_coop) return fail(R2_ERR_INVALID_ARG);
   }
 
@@ -874,7 +876,8 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
   static uint64_t sum_win = 0;
   if (r2_debug >= 2) sum_win += t_pre - t_win0;
   // worker CTAs of every ring + the service CTA (r2_kernels.cu service_main)
-  int rc = r2_launch_allreduce(S, c->threads, stream);
+  const int threads = S.ring[0].ll && c->ll_threads ? c->ll_threads : c->threads;
+  int rc = r2_launch_allreduce(S, threads, stream);
   if (r2_debug >= 2) {                       // host enqueue cost breakdown (diagnostics)
     static uint64_t n_calls = 0, sum_pre = 0, sum_launch = 0;
     const uint64_t t_post = r2_now_ns();

@@ -137,6 +137,7 @@ struct r2_comm {
   bool sim = false;
   r2_config_t cfg{};
   int K = 8, W = 4, threads = 512;
+  int ll_threads = 0;   // threads per CTA of line-protocol launches (0: threads; R2_LL_THREADS)
   int trace = 0;                             // R2_TRACE=1: record the device timeline (r2_trace)
   int last_protocol = 0;                     // r2_protocol_t of the last enqueued collective
   struct { uint64_t seq; int f; double X, Y; size_t NA, NP; } last_r2cc{0, -1, 0, 0, 0, 0};   // (mu)

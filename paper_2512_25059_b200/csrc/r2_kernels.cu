@@ -235,6 +235,9 @@ struct Shared {
   Slot slot[NSLOT];
   Meta meta[NSLOT];
   PlanEntry ent[R2_MAXK];
+  RankPtrs rp[2];             // this rank's / the ring successor's arena pointers (Cta::me / nx):
+                              // the control lane reads them on every chunk, so they live here
+                              // and not in the device-memory peers table (an L2 round trip each)
 };
 
 struct Cta {
@@ -251,7 +254,7 @@ struct Cta {
   unsigned int conn_mask;   // static plan: outgoing channels healthy for this seq (health records)
   bool all_healthy;         // conn_mask covers every channel (O(1) own-item walk)
   int t_act;                // Broadcast: this rank's chain position (sends only at that step); else -1
-  const RankPtrs* me;        // this rank's / the ring successor's arena (global peers table)
+  const RankPtrs* me;        // this rank's / the ring successor's arena (copies in Shared::rp)
   const RankPtrs* nx;
   Ctrl* ctrl;
   unsigned int total_items;
@@ -1467,8 +1470,8 @@ __device__ void copy_stage(Cta& k, Shared& sh) {
 
 // thread 0, once per CTA on the way out.  The last CTA of the rank resets
 // the per-collective counters (nobody reads them any more in this launch) and
-// tells the service lane (which publishes done_seq once every local rank is
-// out, see service_main).
+// counts its (ring, rank) pair out; the last pair publishes done_seq and the
+// service lane leaves (service_main).
 __device__ void last_out(const Cta& k) {
   const unsigned int per_rank = (unsigned int)(k.p->K * k.p->W);
   TRACE_MAX(k, 62);
@@ -1478,7 +1481,11 @@ __device__ void last_out(const Cta& k) {
     __threadfence();
     atomicExch(&k.me->misc->exited, 0u);
     __threadfence();
-    atomicAdd(k.p->grid_exited, 1u);                  // one (ring, rank) pair done (service_main)
+    // one (ring, rank) pair done (service_main); the last pair of the launch
+    // publishes done_seq (posted host writes: the host only paces its
+    // in-flight window and drops stale re-plans with it)
+    if (atomicAdd(k.p->grid_exited, 1u) == k.p->exit_target - 1)
+      for (int l = 0; l < R2_MAXL && k.p->ctrl[l]; ++l) k.p->ctrl[l]->done_seq = k.seq;   // every local rank
   }
 }
 
@@ -1713,7 +1720,7 @@ __device__ void svc_take(SvcBlock* S, MiscDev* m0, SvcShared& ss, unsigned int l
 }
 
 // Resident flavour (the service CTA of a collective): serve until every local
-// rank's worker CTAs have left, then publish done_seq for all of them.
+// rank's worker CTAs have left (the last of them published done_seq).
 __device__ void service_main(const LaunchParams& p) {
   __shared__ SvcShared ss;
   const unsigned int lane = threadIdx.x & 31u;
@@ -1725,16 +1732,20 @@ __device__ void service_main(const LaunchParams& p) {
     S->alive = R2_SS(p.seq, 1);
   }
   __syncwarp();
-  unsigned long long t_head = 0;
+  unsigned long long t_head = gtimer();
   unsigned int head_seen = 0, tail_seen = 0;
+  // the host's head word costs a PCIe round trip (~1 us): it is loaded every
+  // ~2 us and its value used only at the NEXT load, so the lane never stalls
+  // on it (the exit check below stays prompt when the last worker leaves)
+  unsigned int head_inflight = S->head;
   for (;;) {
-    // the host's head word costs a PCIe round trip: read it every ~2 us
     int take = 0;
     if (lane == 0) {
       const unsigned long long now = gtimer();
       if (now - t_head >= 2000ull) {
         t_head = now;
-        head_seen = S->head;
+        head_seen = head_inflight;
+        head_inflight = S->head;
         tail_seen = *(volatile unsigned int*)&m0->svc_tail;
       }
       take = head_seen != tail_seen;
@@ -1742,7 +1753,11 @@ __device__ void service_main(const LaunchParams& p) {
     take = __shfl_sync(0xFFFFFFFFu, take, 0);
     if (take) {
       svc_take(S, m0, ss, lane);
-      if (lane == 0) t_head = 0;                      // look again right away
+      if (lane == 0) {                                // look again right away
+        head_seen = head_inflight = S->head;
+        tail_seen = *(volatile unsigned int*)&m0->svc_tail;
+        t_head = gtimer();
+      }
     }
     if (ss.nactive) svc_probes(S, ss, lane);
     int out = 0;
@@ -1750,14 +1765,11 @@ __device__ void service_main(const LaunchParams& p) {
       out = ss.nactive == 0 && ld_relaxed_sys((const volatile unsigned int*)p.grid_exited) == p.exit_target;
     out = __shfl_sync(0xFFFFFFFFu, out, 0);
     if (out) break;
-    __nanosleep(100);
+    __nanosleep(64);
   }
   if (lane == 0) {
     *p.grid_exited = 0;                               // nobody else touches it in this launch
-    __threadfence();
-    S->alive = R2_SS(p.seq, 0);
-    for (int l = 0; l < p.nlocal; ++l) p.ctrl[l]->done_seq = p.seq;
-    __threadfence_system();
+    S->alive = R2_SS(p.seq, 0);                       // posted: the monitor only uses it as a hint
   }
 }
 
@@ -1810,8 +1822,10 @@ __device__ __forceinline__ void worker_main(const LaunchSet& S, unsigned int b) 
   k.nthr = blockDim.x;
   k.seq = p.seq;
   k.par = (int)(p.seq & 1u);
-  k.me = &p.peers[k.l * p.ng + k.r];
-  k.nx = &p.peers[k.l * p.ng + k.r1];
+  if (k.tid < 2) sh.rp[k.tid] = p.peers[k.l * p.ng + (k.tid == 0 ? k.r : k.r1)];
+  __syncthreads();
+  k.me = &sh.rp[0];
+  k.nx = &sh.rp[1];
   k.ctrl = p.ctrl[k.l];
   // chain collectives: this rank's position in the chain from the root
   k.t_act = (p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2) ? ((k.pos - p.root) % p.n + p.n) % p.n : -1;
