@@ -340,7 +340,7 @@ extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t
     return e;
   };
   if (c->n > 1) {
-    c->max_coop = r2_max_coop_ctas(std::max(c->threads, c->ll_threads));
+    c->max_coop = r2_max_coop_ctas(std::max(std::max(c->threads, c->ll_threads), 512));
     if (c->nlocal * c->K * c->W > c->max_coop) return fail(R2_ERR_INVALID_ARG);
   }
 
@@ -662,6 +662,9 @@ r2_result_t prep_ring(r2_comm* c, const RingSpec& rs, r2_dtype_t dt, uint32_t se
   p.ll_slot_bytes = c->lay.ll_slot_bytes;
   if (c->cfg.channel_gbps > 0)          // lane rate = channel rate / W
     p.lane_ps_per_byte = (unsigned int)((1000ull * c->W + c->cfg.channel_gbps / 2) / c->cfg.channel_gbps);
+  p.cvec_full = (unsigned int)(g.chunk / g.V);
+  p.cvec_last = g.m ? (unsigned int)((g.slice - (uint64_t)(g.m - 1) * g.chunk) / g.V) : 0u;
+  p.lc128 = (p.cvec_full + 6) / 7;
   p.sstride = g.stride;
   p.slen = op == R2_OP_ALLREDUCE ? g.shard : count;
   const size_t shard_bytes = count * (size_t)E;
@@ -876,7 +879,10 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
   static uint64_t sum_win = 0;
   if (r2_debug >= 2) sum_win += t_pre - t_win0;
   // worker CTAs of every ring + the service CTA (r2_kernels.cu service_main)
-  const int threads = S.ring[0].ll && c->ll_threads ? c->ll_threads : c->threads;
+  // LL128 launches run 512 threads per CTA (15 data warps: twice the lines in
+  // flight; measured 32 MiB 146 -> 128 us, 64 MiB 253 -> 220 us at N=4,
+  // profiles/r02_summary.md); R2_LL_THREADS overrides both line protocols
+  const int threads = S.ring[0].ll && c->ll_threads ? c->ll_threads : S.ring[0].ll == 2 ? 512 : c->threads;
   int rc = r2_launch_allreduce(S, threads, stream);
   if (r2_debug >= 2) {                       // host enqueue cost breakdown (diagnostics)
     static uint64_t n_calls = 0, sum_pre = 0, sum_launch = 0;

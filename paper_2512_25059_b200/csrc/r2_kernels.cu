@@ -960,12 +960,9 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     // each chunk owns ceil(chunk vectors / 7) whole lines of the slot; the
     // slot pointers address the chunk's first line, the user pointers the
     // part's first vector (move_ll128)
-    const unsigned long long cvec_full = p.chunk / V;
     const unsigned long long lo =
-        p.ll == 2 ? ((unsigned long long)it.o * p.m + it.j) * ((cvec_full + LL128_PAY - 1) / LL128_PAY) * 128ull
-                  : off * E * 2;
-    const unsigned long long c0 = (unsigned long long)it.j * p.chunk;
-    d.cvec = (unsigned int)((p.slice - c0 < p.chunk ? p.slice - c0 : p.chunk) / V);
+        p.ll == 2 ? ((unsigned long long)it.o * p.m + it.j) * p.lc128 * 128ull : off * E * 2;
+    d.cvec = it.j == p.m - 1 ? p.cvec_last : p.cvec_full;
     d.lo_c = it.lo;
     d.rs = 1;                                         // d_rem is library scratch
     if (ta <= n - 2) {                                // reduce-scatter hop
@@ -1806,8 +1803,18 @@ __device__ __forceinline__ void worker_main(const LaunchSet& S, unsigned int b) 
   const LaunchParams& p = S.ring[RI];
   const int per_rank = p.K * p.W;
   __shared__ Shared sh;
+  // the launch parameters in shared memory: every later access goes through
+  // Cta::p, a generic pointer, which into the parameter space is a slow
+  // generic load -- the control lane reads dozens of fields per chunk
+  __shared__ __align__(16) LaunchParams sp;
+  {
+    static_assert(sizeof(LaunchParams) % 4 == 0, "LaunchParams copy");
+    const unsigned int* src = reinterpret_cast<const unsigned int*>(&p);
+    unsigned int* dst = reinterpret_cast<unsigned int*>(&sp);
+    for (unsigned int i = threadIdx.x; i < sizeof(LaunchParams) / 4; i += blockDim.x) dst[i] = src[i];
+  }
   Cta k;
-  k.p = &p;
+  k.p = &sp;
   k.l = p.part_l[b / per_rank];
   k.c = (int)(b % per_rank) / p.W;
   k.w = (int)(b % per_rank) % p.W;
