@@ -272,16 +272,17 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->sim_ranks = 1;
   cfg->protocol = R2_PROTO_AUTO;
   cfg->ll_max_bytes = (size_t)128 << 20;  // covers the LL128 / SIMPLE crossovers (reading R-12)
-  // fitted to the forced-protocol sweeps at n = 2 and 4 (profiles/r01_protocols_n{2,4}.jsonl):
-  // T(n=2) / T(n=4) = c + steps * alpha, crossovers 5 MB (n=2) and 12 MB (n=4)
-  cfg->alpha_simple_ns = 7150;     // per ring step, SIMPLE (fence + completion word + publish)
+  // fitted to the forced-protocol sweeps at n = 2 and 4 (profiles/r02_protocols_n{2,4}.jsonl):
+  // they reproduce the measured crossovers LL -> LL128 at 2 MB (n=2) / 3 MB (n=4)
+  // and LL128 -> SIMPLE at ~21-25 MB (n=2) / ~60 MB (n=4)
+  cfg->alpha_simple_ns = 6400;     // per ring step, SIMPLE (fence + completion word + publish)
   cfg->alpha_ll_ns = 2050;         // per ring step, LL (one line flight)
-  cfg->beta_mbps = 650000;         // per-GPU NVLink store rate at large sizes
+  cfg->beta_mbps = 700000;         // per-GPU NVLink store rate at large sizes
   cfg->reprobe_us = 2000;
   cfg->reprobe_max_us = 200000;
   cfg->allreduce_algo = R2_ALGO_AUTO;
   cfg->alpha_launch_ns = 6000;     // one cooperative launch + prologue (profiles/r01_host_overhead_n4.log)
-  cfg->alpha_ll128_ns = 2300;      // per ring step, LL128 (one 128-byte line flight + the warp's flag check)
+  cfg->alpha_ll128_ns = 2850;      // per ring step, LL128 (one 128-byte line flight + the warp's flag check)
 }
 
 extern "C" r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob, const r2_config_t* cfg_in,

@@ -27,6 +27,7 @@
 // of every residual chunk on every healthy channel) and deliver them to the
 // canonical addresses with the canonical flags.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stdint.h>
 
 #include "../../include/r2ccl.h"
@@ -1799,8 +1800,7 @@ __global__ void r2_service_kernel(SvcBlock* S, MiscDev* m0) {
 // constant-bank load at a fixed offset (a run-time ring index made them
 // indexed and cost registers: spills in the data path).
 template <int RI>
-__device__ __forceinline__ void worker_main(const LaunchSet& S, unsigned int b) {
-  const LaunchParams& p = S.ring[RI];
+__device__ __forceinline__ void worker_main(const LaunchParams& p, unsigned int b) {
   const int per_rank = p.K * p.W;
   __shared__ Shared sh;
   // the launch parameters in shared memory: every later access goes through
@@ -1917,15 +1917,25 @@ __device__ __forceinline__ void worker_main(const LaunchSet& S, unsigned int b) 
 __global__ void __launch_bounds__(512, 1) r2_allreduce_kernel(const __grid_constant__ LaunchSet S) {
   unsigned int b = blockIdx.x;
   if (b < (unsigned)S.nctas[0]) {
-    worker_main<0>(S, b);
+    worker_main<0>(S.ring[0], b);
     return;
   }
   b -= (unsigned)S.nctas[0];
   if (S.nrings > 1 && b < (unsigned)S.nctas[1]) {
-    worker_main<1>(S, b);
+    worker_main<1>(S.ring[1], b);
     return;
   }
   if (threadIdx.x < 32) service_main(S.ring[0]);        // the service CTA (last in the grid)
+}
+
+// The single-ring flavour (every launch but R²CCL-AllReduce's stage 1): half
+// the parameter block to push per launch (measured on the small-call floor)
+__global__ void __launch_bounds__(512, 1) r2_ring_kernel(const __grid_constant__ LaunchParams P, int nctas) {
+  if (blockIdx.x < (unsigned)nctas) {
+    worker_main<0>(P, blockIdx.x);
+    return;
+  }
+  if (threadIdx.x < 32) service_main(P);
 }
 
 // ------------------------------------------------------------ probe kernel
@@ -1965,11 +1975,19 @@ __global__ void r2_probe_kernel(const __grid_constant__ ProbeParams p) {
 }  // namespace
 
 int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream) {
-  void* args[] = {(void*)&s};
   int nctas = 1;                                         // + the service CTA
   for (int i = 0; i < s.nrings; ++i) nctas += s.nctas[i];
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
-                                              (cudaStream_t)stream);
+  cudaError_t e;
+  if (s.nrings == 1) {
+    int nw = s.nctas[0];
+    void* args[] = {(void*)&s.ring[0], (void*)&nw};
+    e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
+                                    (cudaStream_t)stream);
+  } else {
+    void* args[] = {(void*)&s};
+    e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
+                                    (cudaStream_t)stream);
+  }
   return (int)e;
 }
 
@@ -1994,6 +2012,8 @@ int r2_warmup(const ProbeParams& p, void* stream) {
   cudaFuncAttributes a;
   cudaError_t e = cudaFuncGetAttributes(&a, r2_allreduce_kernel);
   if (e != cudaSuccess) return (int)e;
+  e = cudaFuncGetAttributes(&a, r2_ring_kernel);
+  if (e != cudaSuccess) return (int)e;
   e = cudaFuncGetAttributes(&a, r2_probe_kernel);
   if (e != cudaSuccess) return (int)e;
   e = cudaFuncGetAttributes(&a, r2_service_kernel);
@@ -2011,6 +2031,8 @@ int r2_max_coop_ctas(int threads) {
   int dev = 0, nsm = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per1 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, r2_allreduce_kernel, threads, 0);
-  return (nsm - 2) * per;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, r2_ring_kernel, threads, 0);
+  return (nsm - 2) * std::min(per, per1);
 }

@@ -150,9 +150,9 @@ def test_auto_selects_by_alpha_beta():
     """AUTO: LL for a latency-bound size, LL128 for a mid size, SIMPLE above
     the line scratch (ll_max_bytes); results bit-identical between protocols."""
     n = 4
-    comm = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="AUTO", ll_max_bytes=8 << 20)
+    comm = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="AUTO", ll_max_bytes=16 << 20)
     simple = sim_comm(n, 4, 2, 64 * 1024, max_bytes=64 << 20, protocol="SIMPLE")
-    for N, want in ((4096, "LL"), (2 << 20, "LL128"), (8 << 20, "SIMPLE")):
+    for N, want in ((4096, "LL"), (4 << 20, "LL128"), (16 << 20, "SIMPLE")):
         xs = r2inputs.inputs(n, N, "bfloat16", seed=N)
         rc, out = run(comm, xs, "bfloat16")
         assert rc == R.SUCCESS and comm.status()["last_protocol"] == want, N
