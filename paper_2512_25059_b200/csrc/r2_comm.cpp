@@ -771,6 +771,10 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
   for (int i = 0; i < S.nrings; ++i) total += S.nctas[i];
   if (total > c->max_coop) return R2_ERR_INVALID_ARG;
   for (int i = 0; i < S.nrings; ++i) S.ring[i].exit_target = exit_target;
+  // diagnostics only: a single-ring launch without the service CTA (failover
+  // then has no resident service lane; used to time the small-call floor)
+  static const int no_svc = getenv("R2_NO_SERVICE_CTA") ? atoi(getenv("R2_NO_SERVICE_CTA")) : 0;
+  if (no_svc && S.nrings == 1) S.ring[0].no_svc = 1;
 
   // faults armed for this seq; REPAIRs take effect before it (stand-in for
   // re-probe); HEALs only repair the emulated fabric (found by re-probing)
@@ -1034,13 +1038,17 @@ r2_result_t r2cc_enqueue(r2_comm* c, const R2ccPlan& pl, const void* send, void*
   pr.allow_ll = false;
   pr.row_elems = count;
   st1.push_back(pr);
-  r2_result_t e = launch_rings(c, st1, dt, stream);
+  // diagnostics only (tools/r2cc_stages.py): R2_R2CC_ONLY_STAGE=1/2 launches
+  // one stage alone to time it -- the result is then incomplete
+  static const int only = getenv("R2_R2CC_ONLY_STAGE") ? atoi(getenv("R2_R2CC_ONLY_STAGE")) : 0;
+  r2_result_t e = R2_SUCCESS;
+  if (only != 2) e = launch_rings(c, st1, dt, stream);
   if (e != R2_SUCCESS) return e;
   std::vector<RingSpec> st2{standard_ring(c, R2_OP_R2CC_STAGE2, (const char*)send + shiftb, (char*)recv + shiftb,
                                           pl.NP, pl.f)};
   st2[0].row_elems = count;
   st2[0].allow_ll = false;
-  e = launch_rings(c, st2, dt, stream);
+  if (only != 1) e = launch_rings(c, st2, dt, stream);
   if (e != R2_SUCCESS) return e;
   std::lock_guard<std::mutex> gl(c->mu);
   c->last_r2cc.seq = c->seq;

@@ -236,6 +236,8 @@ struct Shared {
   Slot slot[NSLOT];
   Meta meta[NSLOT];
   PlanEntry ent[R2_MAXK];
+  unsigned long long sbase[2 * R2_MAXR];   // per op-step: first element of the shard this rank sends
+  unsigned long long slim[2 * R2_MAXR];    //   and one past its last valid element
   RankPtrs rp[2];             // this rank's / the ring successor's arena pointers (Cta::me / nx):
                               // the control lane reads them on every chunk, so they live here
                               // and not in the device-memory peers table (an L2 round trip each)
@@ -272,6 +274,16 @@ __device__ __forceinline__ char* scratch_slot(const RankPtrs& rp, const LaunchPa
   return rp.scratch + ((size_t)par * (p.n - 1) + slot) * p.slot_bytes;
 }
 
+// back-off of the data warps' line polls (ns); R2_SPIN_NS=0 at build time disables it
+#ifndef R2_SPIN_NS
+#define R2_SPIN_NS 0
+#endif
+#if R2_SPIN_NS > 0
+#define R2_SPIN_PAUSE() __nanosleep(R2_SPIN_NS)
+#else
+#define R2_SPIN_PAUSE() ((void)0)
+#endif
+
 // ------------------------------------------------------------ LL protocol
 // One 16-byte vector {w0, w1, w2, w3} travels as two 16-byte lines
 // {w0, seq, w1, seq}, {w2, seq, w3, seq} (r2ccl.h "Protocols"): a line is valid
@@ -303,6 +315,9 @@ __device__ __forceinline__ uint4 ll_load(const char* q, unsigned int seq, const 
   unsigned int spins = 0;
   while (a.y != seq || a.w != seq || b.y != seq || b.w != seq) {
     if ((++spins & 0x3FFu) == 0 && *abort_word == seq) break;
+    // back off: a warp re-polling at full rate keeps the SM's load queue full,
+    // and the control lane's own loads / stores then wait behind the polls
+    R2_SPIN_PAUSE();
     if (a.y != seq || a.w != seq) a = ll_line(q);
     if (b.y != seq || b.w != seq) b = ll_line(q + 16);
   }
@@ -466,6 +481,7 @@ __device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[
     // reload every line of the warp: the 8 lanes of a line must read it with
     // ONE converged load instruction (a line read in pieces can pair a new
     // flag with an old payload)
+    R2_SPIN_PAUSE();
     __syncwarp();
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -732,7 +748,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         out.o = k.c;
         out.j = j;
         out.lo = 0;
-        out.hi = (unsigned int)((j == m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
+        out.hi = j == m - 1 ? p.cvec_last : p.cvec_full;
         out.parts = 1;
         out.epoch = 0;
         out.own = true;
@@ -797,8 +813,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         // is in flight (freeze), so the receiver's flags are stable evidence
         if (dyn && (int)(ld_relaxed_sys((t == p.local_step ? k.me->flags : k.nx->flags) + fidx(p, t, o, j)) - k.seq) >= 0)
           continue;
-        const unsigned int Vj =
-            (unsigned int)((j == p.m - 1 ? (p.slice - (unsigned long long)j * p.chunk) : p.chunk) / p.V);
+        const unsigned int Vj = j == p.m - 1 ? p.cvec_last : p.cvec_full;
         unsigned int lo = 0, hi = Vj, parts = 1;
         if (!own && mode == PLAN_BAL) {
           bal_part(Vj, mask, p.weights, p.K, k.c, lo, hi, parts);
@@ -907,10 +922,10 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
 
   const int E = p.elem_bytes, V = p.V;
   const bool chain = p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2;
-  const int s_ = chain ? 0 : (ta <= n - 2) ? ((k.pos - 1 - ta) % n + n) % n : ((k.pos - (ta - n + 1)) % n + n) % n;
+  // shard of this step (computed once per CTA: sh.sbase / sh.slim, worker_main)
   const unsigned long long off =
       (unsigned long long)it.o * p.slice + (unsigned long long)it.j * p.chunk + (unsigned long long)it.lo * V;
-  const unsigned long long sbase = (unsigned long long)s_ * p.sstride;
+  const unsigned long long sbase = sh.sbase[t];
   const unsigned long long e0 = sbase + off;
   const unsigned int u = sh.pub % NSLOT;
   Slot& d = sh.slot[u];
@@ -920,7 +935,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   d.total = it.hi - it.lo;
   d.poison = fire && poison;
   d.e0 = e0;
-  d.lim = sbase + p.slen < p.N ? sbase + p.slen : p.N;
+  d.lim = sh.slim[t];
   d.rs = ta <= n - 2;
   d.src_ll = 0;
   if (p.op == R2_OP_R2CC_STAGE2) {
@@ -1381,12 +1396,19 @@ __device__ int drain(Cta& k, Shared& sh) {
     post_state(k, sh, CTA_DRAINING, 0);
     sh.wait_t0 = 0;
   }
+  bool first = true;
   for (;;) {
     if (k.tid == 0) {
-      int st = poll_control(k, sh);
+      // first pass: the rank's delivered count first -- when it is complete
+      // (the common case) the control words need no look (two dependent
+      // global loads); every later pass polls them (a freeze must be
+      // acknowledged while this CTA waits for incoming words)
+      const unsigned int dl0 = ld_relaxed_sys((volatile unsigned int*)&k.me->misc->delivered);
+      int st = first && dl0 >= k.total_items ? ST_OK : poll_control(k, sh);
+      first = false;
       int cand = 0;
       if (st == ST_OK) {
-        const unsigned int dl = ld_relaxed_sys((volatile unsigned int*)&k.me->misc->delivered);
+        const unsigned int dl = dl0 >= k.total_items ? dl0 : ld_relaxed_sys((volatile unsigned int*)&k.me->misc->delivered);
         cand = dl >= k.total_items;
         if (!cand) {
           if (watchdog(k, sh)) {
@@ -1482,8 +1504,10 @@ __device__ void last_out(const Cta& k) {
     // one (ring, rank) pair done (service_main); the last pair of the launch
     // publishes done_seq (posted host writes: the host only paces its
     // in-flight window and drops stale re-plans with it)
-    if (atomicAdd(k.p->grid_exited, 1u) == k.p->exit_target - 1)
+    if (atomicAdd(k.p->grid_exited, 1u) == k.p->exit_target - 1) {
       for (int l = 0; l < R2_MAXL && k.p->ctrl[l]; ++l) k.p->ctrl[l]->done_seq = k.seq;   // every local rank
+      if (k.p->no_svc) *k.p->grid_exited = 0;       // diagnostics launch without a service CTA
+    }
   }
 }
 
@@ -1830,6 +1854,17 @@ __device__ __forceinline__ void worker_main(const LaunchParams& p, unsigned int 
   k.seq = p.seq;
   k.par = (int)(p.seq & 1u);
   if (k.tid < 2) sh.rp[k.tid] = p.peers[k.l * p.ng + (k.tid == 0 ? k.r : k.r1)];
+  // per op-step shard tables (the control lane's per-chunk arithmetic without
+  // integer divisions; SURVEY §8 header: RS sends shard (pos-1-t) mod n, AG
+  // shard (pos-(t-n+1)) mod n, chains one shard)
+  for (int t = k.tid; t < p.steps; t += k.nthr) {
+    const int n = p.n, ta = t + p.t0;
+    const bool chain = p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2;
+    const int s_ = chain ? 0 : (ta <= n - 2) ? ((k.pos - 1 - ta) % n + n) % n : ((k.pos - (ta - n + 1)) % n + n) % n;
+    const unsigned long long sb = (unsigned long long)s_ * p.sstride;
+    sh.sbase[t] = sb;
+    sh.slim[t] = sb + p.slen < p.N ? sb + p.slen : p.N;
+  }
   __syncthreads();
   k.me = &sh.rp[0];
   k.nx = &sh.rp[1];
@@ -1935,7 +1970,7 @@ __global__ void __launch_bounds__(512, 1) r2_ring_kernel(const __grid_constant__
     worker_main<0>(P, blockIdx.x);
     return;
   }
-  if (threadIdx.x < 32) service_main(P);
+  if (threadIdx.x < 32 && !P.no_svc) service_main(P);
 }
 
 // ------------------------------------------------------------ probe kernel
@@ -1980,6 +2015,7 @@ int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream) {
   cudaError_t e;
   if (s.nrings == 1) {
     int nw = s.nctas[0];
+    if (s.ring[0].no_svc) nctas = nw;
     void* args[] = {(void*)&s.ring[0], (void*)&nw};
     e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
                                     (cudaStream_t)stream);

@@ -1,0 +1,9 @@
+R=$PWD
+for v in new nospin; do d=.; [ $v = nospin ] && d=ab/nospin; (cd $d && timeout 120 python tools/trace_sim.py 2>&1 | tail -2 | sed "s/^/$v /"); done
+run() { python tools/sweep_sizes.py --sim-ranks 4 --ctas 4 --min-log2 10 --max-log2 11 --dtypes bf16 2>/dev/null | python -c "
+import json,sys; print('$1', [(json.loads(l)['bytes'], round(json.loads(l)['r2_ms']*1e3,1)) for l in sys.stdin])"; }
+run new; (cd ab/nospin && run nospin)
+for v in new nospin; do d=.; [ $v = nospin ] && d=ab/nospin
+(cd $d && timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29532 tools/sweep_sizes.py --max-log2 27 --dtypes bf16 --no-nccl 2>/dev/null | python -c "
+import json,sys; print('$v N=4', [(json.loads(l)['bytes'], json.loads(l)['protocol'], round(json.loads(l)['r2_ms']*1e3,1)) for l in sys.stdin])")
+done

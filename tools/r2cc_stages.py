@@ -51,8 +51,25 @@ def main():
         e1.synchronize()
         assert comm.sync() == R.SUCCESS
         st = comm.status()
+        # device timeline of the LAST launch of one more call (R2_TRACE=1): for
+        # R²CCL-AllReduce that is stage 2, the tailored broadcast
+        tr = None
+        if os.environ.get("R2_TRACE") == "1":
+            import ctypes as C
+            buf = (C.c_uint64 * 64)()
+            R.lib().r2_trace(comm._h, 0, buf)            # arm
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            T.allreduce(comm, x, y)
+            f1.record()
+            f1.synchronize()
+            R.lib().r2_trace(comm._h, 0, buf)
+            b = buf[0]
+            tr = (f0.elapsed_time(f1), (buf[62] - b) / 1e6, (buf[1] - b) / 1e6)
         print(f"{algo}: {e0.elapsed_time(e1) / iters:.3f} ms/call  r2cc calls {st['r2cc']['calls']} "
-              f"Y {st['r2cc']['Y']:.3f} NA/NP {st['r2cc']['NA']}/{st['r2cc']['NP']}", flush=True)
+              f"Y {st['r2cc']['Y']:.3f} NA/NP {st['r2cc']['NA']}/{st['r2cc']['NP']}"
+              + (f"  | one call {tr[0]:.3f} ms, last launch first-CTA-start -> last exit {tr[1]:.3f} ms" if tr else ""),
+              flush=True)
         comm.finalize()
 
 
