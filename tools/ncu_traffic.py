@@ -26,11 +26,12 @@ def main(rep, out, how):
         return float(row[i].replace(",", "")) * UNITS[units[i]]
 
     for row in rows[2:]:
-        if "r2_allreduce_kernel" not in row[head.index("Kernel Name")]:
+        name = row[head.index("Kernel Name")]
+        if "r2_allreduce_kernel" not in name and "r2_ring_kernel" not in name:
             continue
         rd, wr = val(row, "dram__bytes_read.sum"), val(row, "dram__bytes_write.sum")
         d = {"workload": "8 simulated ranks x 256 MiB bf16, K=8, W=2, 512 KiB chunks (bench.py N=1 default)",
-             "kernel": "r2_allreduce_kernel",
+             "kernel": name.split("(")[0].split("::")[-1],
              "dram_bytes_read_per_launch": int(rd), "dram_bytes_write_per_launch": int(wr),
              "dram_bytes_per_launch": int(rd + wr),
              "ncu_duration_ms": val(row, "gpu__time_duration.sum"),

@@ -70,6 +70,23 @@ def main():
               f"Y {st['r2cc']['Y']:.3f} NA/NP {st['r2cc']['NA']}/{st['r2cc']['NP']}"
               + (f"  | one call {tr[0]:.3f} ms, last launch first-CTA-start -> last exit {tr[1]:.3f} ms" if tr else ""),
               flush=True)
+        if algo == "RING" and os.environ.get("BCAST"):
+            # the same degraded communicator: a plain Broadcast chain from rank 1
+            # over the stage-2 payload (R²CCL's Y share of the buffer)
+            NP = int(N * float(os.environ.get("BCAST"))) // 8 * 8
+            xb = x[:, :NP].contiguous()
+            yb = torch.empty_like(xb)
+            for _ in range(2):
+                T.broadcast(comm, xb, yb, root=1)
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            for _ in range(iters):
+                T.broadcast(comm, xb, yb, root=1)
+            g1.record()
+            g1.synchronize()
+            assert comm.sync() == R.SUCCESS
+            print(f"BROADCAST root 1, {NP} elements: {g0.elapsed_time(g1) / iters:.3f} ms/call", flush=True)
         comm.finalize()
 
 
