@@ -36,8 +36,6 @@ extern "C" {
 #define R2_MAX_CHANNELS 16   /* K upper bound                                   */
 #define R2_MAX_LOCAL 16      /* simulated ranks per process upper bound         */
 #define R2_MAX_RANKS 64      /* ranks of a communicator upper bound             */
-#define R2_LANE_CHUNKS 4     /* chunks per lane per ring step (r2_geometry)     */
-#define R2_LANE_CHUNK_MIN 4096  /* ... but chunks not below this (or slice/W)   */
 
 typedef enum {
   R2_SUCCESS = 0,
@@ -465,10 +463,8 @@ void r2_rollback(const uint8_t* completed, int npos, int* resume, int* floor);
 int r2_rerank(int n, const int* ring_in, const uint32_t* rails, const uint32_t* dead_links, int* ring_out);
 
 /* Geometry of one collective (SURVEY §8 header, reading C-3).
- * Chunk = chunk_bytes, capped at max(ceil(slice bytes / (W * R2_LANE_CHUNKS)),
- * min(ceil(slice bytes / W), R2_LANE_CHUNK_MIN)) rounded up to 16 bytes:
- * every one of a channel's W lanes gets R2_LANE_CHUNKS chunks per ring step
- * (a pipeline across steps) once a lane's share is large enough.
+ * Chunk = chunk_bytes, capped at ceil(slice bytes / W) rounded up to 16
+ * bytes: every one of a channel's W lanes gets a chunk per ring step.
  * AllReduce: N = count, shards of Np/n at stride shard.
  * Broadcast (f1): N = count, one shard of roundup(count, K*V) = Np, steps
  * n-1 (rank r sends only at its chain position (r - root) mod n), chunks

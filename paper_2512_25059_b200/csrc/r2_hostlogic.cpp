@@ -96,18 +96,11 @@ extern "C" r2_result_t r2_geometry_op(r2_op_t op, uint64_t count, r2_dtype_t dt,
   }
   const uint64_t slice = Np_cap / ((uint64_t)(chain ? 1 : n) * K);
   const uint64_t slice_bytes = slice * E;
-  // reading C-3 (round 2): R2_LANE_CHUNKS chunks per lane per step, so that a
-  // lane streams chunk j+1 of a step while chunk j's successor step waits for
-  // its completion word (one chunk per lane per step made every ring step a
-  // store-and-forward: its fence + completion + publish latency was paid
-  // 2n-2 times per collective)
-  // (not below min(slice / W, 4 KiB): latency-bound sizes keep one chunk per lane)
-  const uint64_t lanes = (uint64_t)W * R2_LANE_CHUNKS;
-  const uint64_t per_lane = (slice_bytes + W - 1) / W;
-  uint64_t per_worker = (slice_bytes + lanes - 1) / lanes;
-  const uint64_t floor_b = per_lane < R2_LANE_CHUNK_MIN ? per_lane : R2_LANE_CHUNK_MIN;
-  if (per_worker < floor_b) per_worker = floor_b;
-  per_worker = (per_worker + 15) / 16 * 16;
+  // reading C-3: capped at ceil(slice / W) -- one chunk per lane per step.
+  // (Four chunks per lane per step, to pipeline across ring steps, was
+  // measured slower at 4-64 MiB: the control lane's per-chunk cost (~1.7 us
+  // per publish) outweighs the overlap -- profiles/r02_lane_chunks.txt)
+  uint64_t per_worker = ((slice_bytes + W - 1) / W + 15) / 16 * 16;
   // a Broadcast chain pipelines per chunk (fill = (n-2) chunk hops): 128 KiB cap (reading R-8)
   const uint64_t cap = chain && chunk_bytes > (128u << 10) ? (128u << 10) : chunk_bytes;
   uint64_t chunkb = cap < per_worker ? cap : per_worker;

@@ -9,10 +9,8 @@ include/r2ccl.h r2_geometry_op), restated here so that a test can name the
 scenario a configured communicator runs; tests/test_abi.py checks that the
 library's r2_geometry_op uses exactly this chunk.
 
-* C-3: the configured chunk, capped at max(ceil(slice / (W * LANE_CHUNKS)),
-  min(ceil(slice / W), LANE_CHUNK_MIN)) rounded up to a 16-byte vector, so
-  that every one of the W lanes of a channel gets LANE_CHUNKS chunks per step
-  once its share is large enough (r2ccl.h R2_LANE_CHUNKS, R2_LANE_CHUNK_MIN).
+* C-3: the configured chunk, capped at ceil(slice / W) rounded up to a 16-byte
+  vector, so that every one of the W lanes of a channel gets a chunk per step.
 * R-8: Broadcast chunks are further capped at 128 KiB (a chain's pipeline
   fill is n-2 chunk hops).
 """
@@ -21,8 +19,6 @@ from __future__ import annotations
 from oracle.geometry import ALLREDUCE, BROADCAST, ceil_div
 
 BCAST_CHUNK_CAP = 128 * 1024
-LANE_CHUNKS = 4
-LANE_CHUNK_MIN = 4096
 
 
 def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: int, W: int = 1,
@@ -34,8 +30,7 @@ def effective_chunk_bytes(N: int, n: int, K: int, elem_bytes: int, chunk_bytes: 
         slice_bytes = Np // (n * K) * elem_bytes
     else:
         slice_bytes = ceil_div(max(N, 1), K * V) * V * elem_bytes
-    per_worker = max(ceil_div(slice_bytes, W * LANE_CHUNKS), min(ceil_div(slice_bytes, W), LANE_CHUNK_MIN))
-    per_worker = ceil_div(per_worker, 16) * 16
+    per_worker = ceil_div(ceil_div(slice_bytes, W), 16) * 16
     if op == BROADCAST:
         chunk_bytes = min(chunk_bytes, BCAST_CHUNK_CAP)
     return max(16, min(chunk_bytes, per_worker))
