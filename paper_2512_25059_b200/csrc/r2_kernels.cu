@@ -274,6 +274,17 @@ __device__ __forceinline__ char* scratch_slot(const RankPtrs& rp, const LaunchPa
   return rp.scratch + ((size_t)par * (p.n - 1) + slot) * p.slot_bytes;
 }
 
+// The launch parameters, the Cta's arena pointers and Shared live in shared
+// memory but reach the control-lane functions through generic pointers; the
+// assumption lets the compiler emit shared-space loads (LDS) for them.
+#define R2_ASSUME_SHARED(k, sh)                     \
+  do {                                              \
+    __builtin_assume(__isShared((k).p));            \
+    __builtin_assume(__isShared((k).me));           \
+    __builtin_assume(__isShared((k).nx));           \
+    __builtin_assume(__isShared(&(sh)));            \
+  } while (0)
+
 // back-off of the data warps' line polls (ns); R2_SPIN_NS=0 at build time disables it
 #ifndef R2_SPIN_NS
 #define R2_SPIN_NS 0
@@ -580,6 +591,7 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
 // (set on every rank by a firing fault) and, once alerted, the host-mapped
 // control block (abort, stop mask, plan epoch).
 __device__ int poll_control(const Cta& k, Shared& sh) {
+  R2_ASSUME_SHARED(k, sh);
   sh.t_prev_poll = sh.t_poll;
   sh.t_poll = gtimer();
   sh.npoll++;
@@ -722,6 +734,7 @@ struct ItemRef {
 };
 
 __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out) {
+  R2_ASSUME_SHARED(k, sh);
   const LaunchParams& p = *k.p;
   if (k.all_healthy && !sh.dynamic && !sh.freeze) {
     // healthy static plan: the lane's own chunks only, (t, c, j = w, w+W, ...)
@@ -847,6 +860,7 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
 // Returns ST_OK (published; *fired if it carries an armed fault),
 // ST_NOTREADY, or a terminal status (cause in sh.cause).
 __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try, bool* fired) {
+  R2_ASSUME_SHARED(k, sh);
   const LaunchParams& p = *k.p;
   const int n = p.n;
   int fire = 0;
@@ -1134,10 +1148,18 @@ __device__ void apply_plan(const Cta& k, Shared& sh) {
 // is retired before returning, then an END slot releases the data warps.
 // Returns the status (also in sh.pipe_status).
 __device__ int control_run(Cta& k, Shared& sh) {
+  R2_ASSUME_SHARED(k, sh);
   const LaunchParams& p = *k.p;
   Iter it{0, 0, k.w};
   ItemRef cur;
+  // R2_TRACE=3 (diagnostics): SM cycles the control lane of CTA 0 spends in
+  // try_publish / iter_next / retiring, into trace slots 50..56
+  const bool prof = p.trace == 3 && k.cta_in_rank == 0 && k.l == 0;
+  long long c_pub = 0, c_it = 0, c_ret = 0, n_pub = 0, n_it = 0, n_ret = 0;
+  const long long c_start = clock64();
+  long long c0 = clock64();
   bool have = iter_next(k, sh, it, cur);
+  if (prof) c_it += clock64() - c0, n_it++;
   bool first_try = true;
   int pending = ST_OK;
   unsigned int idle = 0;
@@ -1154,7 +1176,9 @@ __device__ int control_run(Cta& k, Shared& sh) {
     bool replanned = false;
     while (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
       bool fired = false;
+      if (prof) c0 = clock64();
       int st = try_publish(k, sh, cur, first_try, &fired);
+      if (prof) c_pub += clock64() - c0, n_pub++;
       first_try = false;
       if (st == ST_REPLAN) {
         apply_plan(k, sh);
@@ -1178,7 +1202,9 @@ __device__ int control_run(Cta& k, Shared& sh) {
           sh.cause = STOP_FAULT_FIRED;
           have = false;
         } else {
+          if (prof) c0 = clock64();
           have = iter_next(k, sh, it, cur);
+          if (prof) c_it += clock64() - c0, n_it++;
         }
       } else {
         if (st != ST_NOTREADY) {
@@ -1197,6 +1223,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
       ++nd;
     }
     if (nd) {
+      if (prof) c0 = clock64(), n_ret += nd;
       bool any = false;
       for (unsigned int i = 0; i < nd; ++i) any |= sh.meta[(sh.fin + i) % NSLOT].kind != META_END;
       if (any && !p.ll) fence_sys();   // LL lines validate themselves: no fence
@@ -1215,6 +1242,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
           if (sh.fin + i < 8) k.me->misc->trace[16 + sh.fin + i] = gtimer();   // retire i
       sh.fin += nd;
       progress = true;
+      if (prof) c_ret += clock64() - c0;
     }
     // 1b. acknowledge a freeze once no adopted chunk is in flight
     if (ack_epoch && sh.fin >= last_adopt_pub) {
@@ -1233,6 +1261,13 @@ __device__ int control_run(Cta& k, Shared& sh) {
       sh.pipe_status = pending;
       sh.stop_key = fired_key != ~0ull ? fired_key : k.own_next_key;
       TRACE_MAX(k, 60);
+      if (prof) {
+        unsigned long long* tr = k.me->misc->trace;
+        tr[50] = (unsigned long long)c_pub, tr[51] = (unsigned long long)n_pub;
+        tr[52] = (unsigned long long)c_it, tr[53] = (unsigned long long)n_it;
+        tr[54] = (unsigned long long)c_ret, tr[55] = (unsigned long long)n_ret;
+        tr[56] = (unsigned long long)(clock64() - c_start);
+      }
       mbar_arrive(&sh.full[u]);
       sh.pub++;
       return pending;

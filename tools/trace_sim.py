@@ -18,9 +18,10 @@ def main():
     B.build()
     torch.cuda.set_device(0)
     n = int(os.environ.get("SIM", 4))
-    comm = R.Comm(0, 1, 0, None, R.config_default(sim_ranks=n, nchannels=8, ctas_per_channel=4, protocol="LL",
-                                                  max_bytes=1 << 20))
-    x = torch.randn((n, 512), device="cuda").to(torch.bfloat16)
+    comm = R.Comm(0, 1, 0, None, R.config_default(sim_ranks=n, nchannels=8, ctas_per_channel=4,
+                                                  protocol=os.environ.get("PROTO", "LL"),
+                                                  max_bytes=64 << 20))
+    x = torch.randn((n, int(os.environ.get("ELEMS", 512))), device="cuda").to(torch.bfloat16)
     y = torch.empty_like(x)
     buf = (C.c_uint64 * 64)()
     steps = 2 * n - 1
@@ -37,6 +38,10 @@ def main():
               + " ".join(f"{rel(buf[32 + t]):.1f}" for t in range(steps)) + " | step last-retire: "
               + " ".join(f"{rel(buf[4 + t]):.1f}" for t in range(steps))
               + f" | ctl-end {rel(buf[60]):.1f} drain {rel(buf[61]):.1f} exit {rel(buf[62]):.1f}", flush=True)
+        if os.environ.get("R2_TRACE") == "3":
+            cyc = lambda c, k: f"{c / max(k, 1):.0f} cyc x {k}"  # noqa: E731
+            print(f"   control lane of CTA 0: try_publish {cyc(buf[50], buf[51])}, iter_next {cyc(buf[52], buf[53])}, "
+                  f"retire {cyc(buf[54], buf[55])} per chunk, control_run total {buf[56]} cyc", flush=True)
     comm.finalize()
 
 
