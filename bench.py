@@ -569,6 +569,9 @@ def run_multi(a):
             mk, lambda c: T.allreduce(c, send, recv), ms, world, K, g.m, strat, lambda: recv, ref,
             fault_rank=3 % world, stream=stream, barrier=barrier, reduce_max=reduce_max, gather=gather))
             for strat in ("BALANCE", "HOT_REPAIR")]
+    if not a.no_fault and world >= 2:
+        res["bucket_25MB"] = guarded(lambda: bucket_section(a, T, R, mk, send, recv, world, K, W, stream, barrier,
+                                                           reduce_max, gather, pg if not a.no_nccl else None))
     if not a.no_fault and world >= 2 and a.bw_model_gbps > 0:
         res["fault_bw_model"] = guarded(lambda: bw_model_section(
             a, T, R, mk, send, recv, ref, S, world, K, W, g.m, stream, barrier, reduce_max, gather))
@@ -578,6 +581,62 @@ def run_multi(a):
         res["rerank"] = guarded(lambda: rerank_section(a, T, R, send, recv, S, world, K, W, stream, barrier,
                                                        reduce_max))
     return res, rank
+
+
+def bucket_section(a, T, R, mk, send, recv, world, K, W, stream, barrier, reduce_max, gather, pg):
+    """BASELINE configs[4]'s bucket: 25,000,000 B bf16 per rank -- the healthy
+    time (AUTO protocol) next to NCCL's, then one LINK fault mid-collective and
+    the degraded steady state under Balance, unpaced and with channels paced
+    as bandwidth units (VERDICT r1 #3: Balance at 25 MB vs the (K-1)/K bound)."""
+    import torch
+    cb = 12_500_000
+    S_b = cb * 2
+    sb, rb = send[:cb], recv[:cb]
+    out = {"bytes_per_rank": S_b}
+    c = mk("BALANCE")
+    step = lambda cc=c: T.allreduce(cc, sb, rb)  # noqa: E731
+    for _ in range(3):
+        step()
+    barrier()
+    ms = reduce_max(timed(step, 50, stream))
+    assert c.sync() == R.SUCCESS
+    out["protocol"] = c.status()["last_protocol"]
+    out["ms"] = ms
+    out["busbw_per_rank"] = 2 * (world - 1) / world * S_b / (ms * 1e-3) / 1e9
+    ref = rb.clone()
+    c.finalize()
+    if pg is not None:
+        import torch.distributed as dist
+        buf = sb.clone()
+        for _ in range(3):
+            dist.all_reduce(buf, group=pg)
+        barrier()
+        msn = reduce_max(timed(lambda: dist.all_reduce(buf, group=pg), 50, stream))
+        out["nccl_ms"] = msn
+    g = R.geometry(cb, R.BFLOAT16, world, K, W, a.chunk)
+    out["fault_unpaced"] = fault_scenario(mk, lambda cc: T.allreduce(cc, sb, rb), ms, S_b, world, K, g.m, "BALANCE",
+                                          lambda: rb, ref, fault_rank=3 % world, b=4096, stream=stream,
+                                          barrier=barrier, reduce_max=reduce_max, gather=gather)
+    if a.bw_model_gbps > 0:
+        def mkp(strategy):
+            cc = T.comm_from_env(R.config_default(
+                nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=a.bytes,
+                strategy=strategy, protocol=a.protocol, channel_gbps=a.bw_model_gbps))
+            T.register(cc, recv)
+            return cc
+        c = mkp("BALANCE")
+        step = lambda cc=c: T.allreduce(cc, sb, rb)  # noqa: E731
+        for _ in range(3):
+            step()
+        barrier()
+        ms_p = reduce_max(timed(step, 50, stream))
+        assert c.sync() == R.SUCCESS
+        c.finalize()
+        out["paced_healthy_ms"] = ms_p
+        out["fault_paced"] = fault_scenario(mkp, lambda cc: T.allreduce(cc, sb, rb), ms_p, S_b, world, K, g.m,
+                                            "BALANCE", lambda: rb, ref, fault_rank=3 % world, b=4096, stream=stream,
+                                            barrier=barrier, reduce_max=reduce_max, gather=gather)
+    return out
 
 
 def small_footprint(a, T, R, send, recv, S, world, K, stream, barrier, reduce_max):
@@ -815,6 +874,8 @@ def report(a, res, n_gpus, n_ranks, mode):
         line["r2cc_allreduce"] = res["r2cc_allreduce"]
     if "rerank" in res:
         line["rerank"] = res["rerank"]
+    if "bucket_25MB" in res:
+        line["bucket_25MB"] = res["bucket_25MB"]
     return line
 
 
