@@ -824,18 +824,13 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
     for (auto& rc : c->readmit_pending) r2_declare_conn_repaired(c, rc.first, rc.second, seq);
     c->readmit_pending.clear();
     if ((!repairs.empty() || readmit) && r2_push_health(c) != 0) return R2_ERR_CUDA;
-    // speculation (line protocols, reading R-6) only on a ring whose every
-    // connection is healthy for this seq: a static Balance plan anywhere puts
-    // parts of one channel into another channel's lane, and a published
-    // speculative item could then wait (through that lane) on a residual
-    // queued behind it after a mid-call fault
-    for (int i = 0; i < S.nrings; ++i) {
-      const RingInfo& ri = li.ring[i];
-      bool all = true;
-      for (int j = 0; j < ri.n && all; ++j)
-        for (int k = 0; k < ri.K && all; ++k) all = r2_conn_ok_to(c, ri.order[j], ri.next_of(ri.order[j]), ri.chans[k], seq);
-      S.ring[i].spec_ok = all;
-    }
+    // speculation (line protocols, reading R-6) on every ring, static degraded
+    // plans included: a mid-call plan change makes the lanes abandon their
+    // spinning items before they take on a residual (r2_kernels.cu
+    // control_run), which breaks the cycle a static Balance plan could
+    // otherwise close (parts of one channel in another channel's lane)
+    static const int no_spec = getenv("R2_NO_SPECULATION") ? atoi(getenv("R2_NO_SPECULATION")) : 0;
+    for (int i = 0; i < S.nrings; ++i) S.ring[i].spec_ok = !no_spec;
     // a ring connection with no healthy channel left: the chain is exhausted
     for (int i = 0; i < S.nrings; ++i) {
       const RingInfo& ri = li.ring[i];

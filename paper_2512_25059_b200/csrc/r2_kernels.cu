@@ -238,6 +238,9 @@ struct Shared {
   PlanEntry ent[R2_MAXK];
   unsigned long long sbase[2 * R2_MAXR];   // per op-step: first element of the shard this rank sends
   unsigned long long slim[2 * R2_MAXR];    //   and one past its last valid element
+  int abandon;                // control lane -> data warps: give up spinning line items
+  int reissue;                // own items may have been abandoned: re-yield those without a completion
+  int slot_ab[NSLOT];         // data warps -> control lane: the slot's item was abandoned
   RankPtrs rp[2];             // this rank's / the ring successor's arena pointers (Cta::me / nx):
                               // the control lane reads them on every chunk, so they live here
                               // and not in the device-memory peers table (an L2 round trip each)
@@ -321,11 +324,18 @@ __device__ __forceinline__ uint4 ll_line(const char* q) {
 // The control lane publishes an LL item only after the sender's completion
 // word for its input (written after the sender issued every line), so the
 // lines are in flight and the spin is short; the abort word bounds it anyway.
-__device__ __forceinline__ uint4 ll_load(const char* q, unsigned int seq, const volatile unsigned int* abort_word) {
+// `bail` (Shared::abandon): the control lane asks the data warps to give up
+// spinning items (a new plan needs the lane, reading R-6); *gave is set then.
+__device__ __forceinline__ uint4 ll_load(const char* q, unsigned int seq, const volatile unsigned int* abort_word,
+                                         const volatile int* bail, bool* gave) {
   uint4 a = ll_line(q), b = ll_line(q + 16);
   unsigned int spins = 0;
   while (a.y != seq || a.w != seq || b.y != seq || b.w != seq) {
-    if ((++spins & 0x3FFu) == 0 && *abort_word == seq) break;
+    if ((++spins & 0x3Fu) == 0 && *bail) {
+      *gave = true;
+      break;
+    }
+    if ((spins & 0x3FFu) == 0 && *abort_word == seq) break;
     // back off: a warp re-polling at full rate keeps the SM's load queue full,
     // and the control lane's own loads / stores then wait behind the polls
     R2_SPIN_PAUSE();
@@ -440,23 +450,27 @@ __device__ void move(const LaunchParams& p, unsigned int tid, unsigned int nthr,
 // an LL slot at the peer, d_loc user memory / stage.  Padding vectors travel
 // as zeros so that the receiver can validate every line.
 template <int DT>
-__device__ void move_ll(const LaunchParams& p, unsigned int tid, unsigned int nthr, const char* src, bool src_ll,
+__device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nthr, const char* src, bool src_ll,
                         const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
                         unsigned int nvec, unsigned long long lim, bool aligned, unsigned int seq,
-                        const volatile unsigned int* abort_word) {
+                        const volatile unsigned int* abort_word, const volatile int* bail) {
   const int E = p.elem_bytes, V = p.V;
-  for (unsigned int v = tid; v < nvec; v += nthr) {
+  bool gave = false;
+  for (unsigned int v = tid; v < nvec && !gave; v += nthr) {
     const long long ev = (long long)(e0 + (unsigned long long)v * V);
     const long long left = (long long)lim - ev;
     const int valid = left <= 0 ? 0 : (left >= V ? V : (int)left);
-    uint4 a = src_ll ? ll_load(src + (size_t)v * 32, seq, abort_word) : ld_user(src + (size_t)v * 16, valid, E, aligned);
-    if (s_in) a = vadd<DT>(ll_load(s_in + (size_t)v * 32, seq, abort_word), a);
+    uint4 a = src_ll ? ll_load(src + (size_t)v * 32, seq, abort_word, bail, &gave)
+                     : ld_user(src + (size_t)v * 16, valid, E, aligned);
+    if (s_in) a = vadd<DT>(ll_load(s_in + (size_t)v * 32, seq, abort_word, bail, &gave), a);
+    if (gave) break;                       // an abandoned item writes nothing more
     if (d_rem) ll_store(d_rem + (size_t)v * 32, a, seq);
     if (d_loc) {
       if (loc_user) st_user(d_loc + (size_t)v * 16, a, valid, E, aligned);
       else st_v4(d_loc + (size_t)v * 16, a);
     }
   }
+  return gave;
 }
 
 // ------------------------------------------------------------ LL128 protocol
@@ -473,9 +487,9 @@ __device__ void move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 // inputs, so two parts sharing a boundary line write identical bytes).
 #define LL128_PAY 7
 template <int U>
-__device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
+__device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
                                                const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
-                                               const volatile unsigned int* abort_word) {
+                                               const volatile unsigned int* abort_word, const volatile int* bail) {
   const unsigned int pos = lane & 7u;
   for (unsigned int spins = 0;; ++spins) {
     bool ok = true;
@@ -484,10 +498,14 @@ __device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[
       const bool f = !act[u] || (x[u].x == seq && x[u].y == seq && x[u].z == seq && x[u].w == seq);
       ok &= __shfl_sync(0xFFFFFFFFu, f, lane | 7u);      // the line's flag lane decides
     }
-    if (__all_sync(0xFFFFFFFFu, ok)) return;
+    if (__all_sync(0xFFFFFFFFu, ok)) return true;
+    if ((spins & 0x3Fu) == 0x3Fu) {
+      const int gv = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (int)(*bail != 0) : 0, 0);
+      if (gv) return false;                              // abandoned (Shared::abandon)
+    }
     if ((spins & 0x3FFu) == 0x3FFu) {
       const int ab = __shfl_sync(0xFFFFFFFFu, lane == 0 ? (int)(*abort_word == seq) : 0, 0);
-      if (ab) return;
+      if (ab) return true;
     }
     // reload every line of the warp: the 8 lanes of a line must read it with
     // ONE converged load instruction (a line read in pieces can pair a new
@@ -508,10 +526,11 @@ __device__ __forceinline__ void ll128_validate(uint4 (&x)[U], const bool (&act)[
 // line stores are issued by the converged warp (__syncwarp before each), so
 // the 8 lanes of a line always access it in one instruction.
 template <int DT>
-__device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned int dn, const char* src, bool src_ll,
+__device__ bool move_ll128(const LaunchParams& p, unsigned int dtid, unsigned int dn, const char* src, bool src_ll,
                            const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
                            unsigned int lo, unsigned int nvec, unsigned int cvec, unsigned long long lim,
-                           bool aligned, unsigned int seq, const volatile unsigned int* abort_word) {
+                           bool aligned, unsigned int seq, const volatile unsigned int* abort_word,
+                           const volatile int* bail) {
   constexpr int U = 4;                    // line groups per warp per iteration (memory-level parallelism)
   const int E = p.elem_bytes, V = p.V;
   const unsigned int lane = dtid & 31u, wid = dtid >> 5, nw = dn >> 5;
@@ -550,8 +569,8 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
         }
       }
     }
-    if (src_ll) ll128_validate<U>(a, act, src, L, lane, seq, abort_word);
-    if (s_in) ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word);
+    if (src_ll && !ll128_validate<U>(a, act, src, L, lane, seq, abort_word, bail)) return true;
+    if (s_in && !ll128_validate<U>(b, act, s_in, L, lane, seq, abort_word, bail)) return true;
     // 3. sums, then the line stores (converged) and the part's local copies
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -584,6 +603,7 @@ __device__ void move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
       }
     }
   }
+  return false;
 }
 
 // ------------------------------------------------------------ control polls
@@ -821,6 +841,11 @@ __device__ bool iter_next(const Cta& k, const Shared& sh, Iter& it, ItemRef& out
         const int j = it.j;
         const unsigned long long key = keyof(t, o, j);
         if (own && key < k.own_next_key) continue;
+        // after an abandonment own items from the abandoned key on come back:
+        // those already completed are skipped (never completed twice)
+        if (own && sh.reissue &&
+            (int)(ld_relaxed_sys((t == p.local_step ? k.me->flags : k.nx->flags) + fidx(p, t, o, j)) - k.seq) >= 0)
+          continue;
         // re-placed chunks: exactly those without a completion (reading C-7);
         // the origin's own lanes have quiesced and no part of an older plan
         // is in flight (freeze), so the receiver's flags are stable evidence
@@ -944,6 +969,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   const unsigned int u = sh.pub % NSLOT;
   Slot& d = sh.slot[u];
   Meta& m = sh.meta[u];
+  sh.slot_ab[u] = 0;
   d.status = SLOT_GO;
   d.nvec = fire ? fire_nvec : (it.hi - it.lo);
   d.total = it.hi - it.lo;
@@ -1167,6 +1193,27 @@ __device__ int control_run(Cta& k, Shared& sh) {
   unsigned long long fired_key = ~0ull;   // own chunk that carried a fired fault
   unsigned int last_adopt_pub = 0;        // 1 + slot index of the newest published adopted chunk
   unsigned int ack_epoch = 0;             // freeze epoch still to acknowledge
+  // a new plan while line items are in flight: published speculative items may
+  // be spinning on inputs that now depend on this lane's residual, so they
+  // are abandoned first (Shared::abandon), then the plan is applied and the
+  // abandoned items re-issued (reading R-6)
+  bool defer_plan = false;
+  unsigned long long ab_min = ~0ull;      // smallest abandoned own key
+  auto replan_now = [&]() {
+    apply_plan(k, sh);
+    if (sh.freeze) ack_epoch = sh.seen_epoch;
+    it = Iter{0, 0, k.w};                 // rescan: own chunks skip by key, re-placed ones by flag
+    have = iter_next(k, sh, it, cur);
+    first_try = true;
+  };
+  auto on_replan = [&]() {
+    if (p.ll && sh.pub != sh.fin) {
+      sh.abandon = 1;
+      defer_plan = true;
+    } else {
+      replan_now();
+    }
+  };
   for (;;) {
     bool progress = false;
     // 1. publish as many chunks as possible (slot free, input arrived) BEFORE
@@ -1174,19 +1221,15 @@ __device__ int control_run(Cta& k, Shared& sh) {
     //    chunks' stores have landed, and the data warps must not idle meanwhile
     //    (publishing after the fence cost one chunk transfer per chunk)
     bool replanned = false;
-    while (pending == ST_OK && have && sh.pub - sh.fin < NSLOT) {
+    while (pending == ST_OK && have && !defer_plan && sh.pub - sh.fin < NSLOT) {
       bool fired = false;
       if (prof) c0 = clock64();
       int st = try_publish(k, sh, cur, first_try, &fired);
       if (prof) c_pub += clock64() - c0, n_pub++;
       first_try = false;
       if (st == ST_REPLAN) {
-        apply_plan(k, sh);
-        if (sh.freeze) ack_epoch = sh.seen_epoch;
-        it = Iter{0, 0, k.w};             // rescan: own chunks skip by key, re-placed ones by flag
-        have = iter_next(k, sh, it, cur);
-        first_try = true;
-        replanned = true;
+        on_replan();
+        replanned = !defer_plan;
         break;
       }
       if (st == ST_OK) {
@@ -1229,7 +1272,14 @@ __device__ int control_run(Cta& k, Shared& sh) {
       if (any && !p.ll) fence_sys();   // LL lines validate themselves: no fence
       for (unsigned int i = 0; i < nd; ++i) {
         const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
-        if (m.kind == META_ITEM) {
+        if (m.kind == META_ITEM && sh.slot_ab[(sh.fin + i) % NSLOT]) {
+          // abandoned: no completion; re-issued after the new plan
+          if (m.own) {
+            const unsigned long long key = keyof(m.t, m.o, m.j);
+            ab_min = key < ab_min ? key : ab_min;
+            sh.reissue = 1;
+          }
+        } else if (m.kind == META_ITEM) {
           complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes, m.local != 0);
           if (m.own && m.t < 28) TRACE_MAX(k, 4 + m.t);
         } else if (m.kind == META_FIRE) {
@@ -1243,6 +1293,15 @@ __device__ int control_run(Cta& k, Shared& sh) {
       sh.fin += nd;
       progress = true;
       if (prof) c_ret += clock64() - c0;
+    }
+    // 1a. the deferred plan, once every line item in flight came back
+    if (defer_plan && sh.fin == sh.pub) {
+      sh.abandon = 0;
+      if (ab_min < k.own_next_key) k.own_next_key = ab_min;
+      ab_min = ~0ull;
+      defer_plan = false;
+      replan_now();
+      continue;
     }
     // 1b. acknowledge a freeze once no adopted chunk is in flight
     if (ack_epoch && sh.fin >= last_adopt_pub) {
@@ -1277,14 +1336,10 @@ __device__ int control_run(Cta& k, Shared& sh) {
     if (progress) {
       idle = 0;
       t_idle = 0;
-    } else if ((++idle & 31u) == 0 && pending == ST_OK) {
+    } else if ((++idle & 31u) == 0 && pending == ST_OK && !defer_plan) {
       int st = poll_control(k, sh);
       if (st == ST_REPLAN) {
-        apply_plan(k, sh);
-        if (sh.freeze) ack_epoch = sh.seen_epoch;
-        it = Iter{0, 0, k.w};
-        have = iter_next(k, sh, it, cur);
-        first_try = true;
+        on_replan();
         continue;
       }
       if (st == ST_OK && have && conn_phys_dead(k)) {
@@ -1337,12 +1392,13 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
       if (lane == 0) mbar_arrive(&sh.empty[u]);
       return;
     }
+    bool gave = false;
     if (p.ll == 2)
-      move_ll128<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.lo_c,
-                     d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort);
+      gave = move_ll128<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0,
+                            d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort, &sh.abandon);
     else if (p.ll)
-      move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
-                  d.lim, d.aligned != 0, k.seq, k.me->abort);
+      gave = move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
+                         d.lim, d.aligned != 0, k.seq, k.me->abort, &sh.abandon);
     else
       move<DT>(p, dtid, dn, d.src, d.s_in, d.d_rem, d.rem_user, d.d_loc, d.loc_user, d.e0, d.nvec, d.lim,
                d.aligned != 0);
@@ -1370,6 +1426,7 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
         else st_user(d.d_rem + (size_t)v * 16, make_uint4(~0u, ~0u, ~0u, ~0u), valid, p.elem_bytes, d.aligned != 0);
       }
     }
+    if (__any_sync(0xFFFFFFFFu, gave) && lane == 0) sh.slot_ab[u] = 1;   // before this warp's arrival
     __syncwarp();
     if (p.trace == 2 && k.cta_in_rank == 0 && k.tid == 32 && dcount <= 8)
       k.me->misc->trace[48 + dcount - 1] = gtimer();   // warp 1 done with item dcount-1
@@ -1952,6 +2009,9 @@ __device__ __forceinline__ void worker_main(const LaunchParams& p, unsigned int 
       mbar_init(&sh.empty[s], (k.nthr >> 5) - 1);         // one arrival per data warp
     }
     sh.seen_epoch = 0;
+    sh.abandon = 0;
+    sh.reissue = 0;
+    for (int s2 = 0; s2 < NSLOT; ++s2) sh.slot_ab[s2] = 0;
     sh.dynamic = 0;
     sh.freeze = 0;
     sh.nent = 0;

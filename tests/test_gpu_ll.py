@@ -218,3 +218,32 @@ def test_ll_inplace_with_fault(strategy, proto):
     check_result(out, xs, g, "bfloat16")
     res = OP.simulate(xs, g, "bfloat16", faults=oracle_faults([f]), strategy=strategy, seed=1, inplace=True)
     assert [norm_event(e) for e in comm.events()] == [norm_event(e) for e in res.events]
+
+
+@pytest.mark.parametrize("step", [0, 2, 4])
+def test_speculation_on_degraded_ring_with_midcall_fault(proto, step):
+    """A statically degraded ring (rank 1 lost channel 1: Balance parts of one
+    channel in other channels' lanes) speculates; a LOCAL fault at rank 2 in
+    the middle of the call re-plans lanes that hold spinning items -- they are
+    abandoned and re-issued (reading R-6), never a watchdog abort."""
+    import time
+    n, K, W, N = 4, 4, 2, 60_003
+    comm = sim_comm(n, K, W, 4096, strategy="BALANCE", protocol=proto, rerank=0)
+    s = comm.status()["seq"] + 1
+    comm.inject_fault(at_seq=s, kind="LOCAL", src_rank=1, channel=1, step=0, chunk=0, byte_offset=0)
+    xs0 = r2inputs.inputs(n, 4096, "int32", seed=1)
+    rc, _ = run(comm, xs0, "int32")
+    assert rc == R.SUCCESS
+    t0 = time.time()
+    while (1, 1) not in comm.status()["dead_endpoints"]:
+        assert time.time() - t0 < 5
+        time.sleep(0.002)
+    xs = r2inputs.inputs(n, N, "bfloat16", seed=50 + step)
+    g = geom(comm, AR, N, "bfloat16")
+    s = comm.status()["seq"] + 1
+    comm.inject_fault(at_seq=s, kind="LOCAL", src_rank=2, channel=2, step=step, chunk=0, byte_offset=512, poison=1)
+    rc, out = run(comm, xs, "bfloat16")
+    assert rc == R.SUCCESS
+    assert comm.status()["last_protocol"] == proto
+    check_result(out, xs, g, "bfloat16")
+    comm.finalize()
