@@ -967,8 +967,11 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   const unsigned long long sbase = sh.sbase[t];
   const unsigned long long e0 = sbase + off;
   const unsigned int u = sh.pub % NSLOT;
-  Slot& d = sh.slot[u];
-  Meta& m = sh.meta[u];
+  // built in registers and stored to the slot at the end: a field-by-field
+  // store into shared memory, which also holds the launch parameters, made the
+  // compiler re-issue every later parameter load behind each store
+  Slot d{};
+  Meta m{};
   sh.slot_ab[u] = 0;
   d.status = SLOT_GO;
   d.nvec = fire ? fire_nvec : (it.hi - it.lo);
@@ -1109,6 +1112,8 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   m.nbytes = (it.hi - it.lo) * 16u;
   m.own = it.own;
   m.fault = fire - 1;
+  sh.slot[u] = d;
+  sh.meta[u] = m;
   mbar_arrive(&sh.full[u]);
   if (p.trace == 2 && k.cta_in_rank == 0 && sh.pub < 8) k.me->misc->trace[24 + sh.pub] = gtimer();  // publish i
   sh.pub++;
