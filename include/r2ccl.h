@@ -309,7 +309,10 @@ r2_result_t r2_init(int rank, int world, int cuda_dev, const r2_oob_t* oob,
  */
 r2_result_t r2_register_multi(r2_comm_t comm, void* dptr, size_t bytes, uint64_t* reg_out);
 
-/* r2_deregister -- collective.  Unmaps a registration on every rank. */
+/* r2_deregister -- collective.  Unmaps a registration on every rank (the
+ * inverse of r2_register_multi's multi-NIC registration, P:27 / P:741; SPEC
+ * register_multi S:225-233).  reg: the id r2_register_multi returned.  Errors:
+ * R2_ERR_NOT_REGISTERED for an unknown id, R2_ERR_BOOTSTRAP if the OOB fails. */
 r2_result_t r2_deregister(r2_comm_t comm, uint64_t reg);
 
 /*
@@ -404,7 +407,12 @@ r2_result_t r2_inject_fault(r2_comm_t comm, const r2_fault_t* f);
  */
 r2_result_t r2_probe(r2_comm_t comm, int rank_local, int peer, int channel, r2_verdict_t* out);
 
-/* r2_status -- thread-safe snapshot (waits for nothing). */
+/* r2_status -- thread-safe snapshot (waits for nothing): the observable
+ * state of the method -- health records ("inspects the health status
+ * records"), failover records (P:31-36 rollback, P:27 chain, P:73 Balance),
+ * per-channel bytes, protocol / R²CCL / ring-order choices -- the
+ * counterpart of SPEC's Report.  *out is caller-owned; fields
+ * are a consistent snapshot under the communicator's lock. */
 r2_result_t r2_status(r2_comm_t comm, r2_status_t* out);
 
 /* r2_get_event -- idx-th failover record (0 <= idx < n_events). */
@@ -426,7 +434,11 @@ r2_result_t r2_sync(r2_comm_t comm);
  */
 r2_result_t r2_trace(r2_comm_t comm, int rank_local, uint64_t out[64]);
 
-/* r2_finalize -- collective.  Stops the monitor, unmaps peers, frees all. */
+/* r2_finalize -- collective.  Stops the monitor, unmaps peers, frees all
+ * (the end of the communicator the bootstrap of P:657 created).  Must not be
+ * called with a collective of this communicator in flight on any stream
+ * (synchronise first); after it, comm is invalid.  Errors: R2_ERR_CUDA if a
+ * device resource cannot be released (the rest is still freed). */
 r2_result_t r2_finalize(r2_comm_t comm);
 
 const char* r2_strerror(r2_result_t r);

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/r2ccl.h"
 #include "r2_internal.h"
@@ -2113,12 +2114,18 @@ int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream) {
   int nctas = 1;                                         // + the service CTA
   for (int i = 0; i < s.nrings; ++i) nctas += s.nctas[i];
   cudaError_t e;
+  // diagnostics (R2_PLAIN_LAUNCH=1): a plain launch instead of a cooperative
+  // one, to measure what the co-residency guarantee costs per call
+  static const int plain = getenv("R2_PLAIN_LAUNCH") ? atoi(getenv("R2_PLAIN_LAUNCH")) : 0;
   if (s.nrings == 1) {
     int nw = s.nctas[0];
     if (s.ring[0].no_svc) nctas = nw;
     void* args[] = {(void*)&s.ring[0], (void*)&nw};
-    e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
-                                    (cudaStream_t)stream);
+    if (plain)
+      e = cudaLaunchKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0, (cudaStream_t)stream);
+    else
+      e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
+                                      (cudaStream_t)stream);
   } else {
     void* args[] = {(void*)&s};
     e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
