@@ -771,10 +771,6 @@ r2_result_t launch_rings(r2_comm* c, std::vector<RingSpec>& rings, r2_dtype_t dt
   for (int i = 0; i < S.nrings; ++i) total += S.nctas[i];
   if (total > c->max_coop) return R2_ERR_INVALID_ARG;
   for (int i = 0; i < S.nrings; ++i) S.ring[i].exit_target = exit_target;
-  // diagnostics only: a single-ring launch without the service CTA (failover
-  // then has no resident service lane; used to time the small-call floor)
-  static const int no_svc = getenv("R2_NO_SERVICE_CTA") ? atoi(getenv("R2_NO_SERVICE_CTA")) : 0;
-  if (no_svc && S.nrings == 1) S.ring[0].no_svc = 1;
 
   // faults armed for this seq; REPAIRs take effect before it (stand-in for
   // re-probe); HEALs only repair the emulated fabric (found by re-probing)

@@ -220,7 +220,6 @@ struct LaunchParams {
   int ll;                                // 0 SIMPLE, 1 LL, 2 LL128 (r2ccl.h "Protocols")
   unsigned int cvec_full, cvec_last, lc128;   // vectors per chunk / in a slice's last chunk; LL128 lines
                                              // per chunk (host-computed: no 64-bit divisions per chunk)
-  int no_svc;                            // diagnostics (R2_NO_SERVICE_CTA): no service CTA in the grid
   int spec_ok;                           // line protocols: speculative publishing allowed (reading R-6;
                                          // R2_NO_SPECULATION=1 turns it off for diagnostics)
   unsigned int lane_ps_per_byte;         // channel bandwidth model: pacing per lane (0 = off)

@@ -1604,7 +1604,6 @@ __device__ void last_out(const Cta& k) {
     // in-flight window and drops stale re-plans with it)
     if (atomicAdd(k.p->grid_exited, 1u) == k.p->exit_target - 1) {
       for (int l = 0; l < R2_MAXL && k.p->ctrl[l]; ++l) k.p->ctrl[l]->done_seq = k.seq;   // every local rank
-      if (k.p->no_svc) *k.p->grid_exited = 0;       // diagnostics launch without a service CTA
     }
   }
 }
@@ -2071,7 +2070,7 @@ __global__ void __launch_bounds__(512, 1) r2_ring_kernel(const __grid_constant__
     worker_main<0>(P, blockIdx.x);
     return;
   }
-  if (threadIdx.x < 32 && !P.no_svc) service_main(P);
+  if (threadIdx.x < 32) service_main(P);
 }
 
 // ------------------------------------------------------------ probe kernel
@@ -2114,18 +2113,13 @@ int r2_launch_allreduce(const LaunchSet& s, int threads, void* stream) {
   int nctas = 1;                                         // + the service CTA
   for (int i = 0; i < s.nrings; ++i) nctas += s.nctas[i];
   cudaError_t e;
-  // diagnostics (R2_PLAIN_LAUNCH=1): a plain launch instead of a cooperative
-  // one, to measure what the co-residency guarantee costs per call
-  static const int plain = getenv("R2_PLAIN_LAUNCH") ? atoi(getenv("R2_PLAIN_LAUNCH")) : 0;
+  // (a plain launch instead of the cooperative one measured the same per-call
+  // time: the co-residency guarantee costs nothing here)
   if (s.nrings == 1) {
     int nw = s.nctas[0];
-    if (s.ring[0].no_svc) nctas = nw;
     void* args[] = {(void*)&s.ring[0], (void*)&nw};
-    if (plain)
-      e = cudaLaunchKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0, (cudaStream_t)stream);
-    else
-      e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
-                                      (cudaStream_t)stream);
+    e = cudaLaunchCooperativeKernel((const void*)r2_ring_kernel, dim3(nctas), dim3(threads), args, 0,
+                                    (cudaStream_t)stream);
   } else {
     void* args[] = {(void*)&s};
     e = cudaLaunchCooperativeKernel((const void*)r2_allreduce_kernel, dim3(nctas), dim3(threads), args, 0,
