@@ -67,3 +67,40 @@ def test_bench_configuration_sampled_parity_and_fault(protocol):
     ev = comm.events()
     assert len(ev) == 1 and ev[0]["verdict"] == "LINK" and ev[0]["resume"] == 3 * geo.m + 4
     comm.finalize()
+
+
+def test_ll128_bucket_size_sampled_parity_and_fault():
+    """The LL128 protocol at BASELINE configs[4]'s bucket size (25,000,000 B
+    bf16 per rank, 8 simulated ranks, K = 8 x W = 2): 4096 sampled outputs per
+    rank against the oracle fold, then a LINK fault mid-collective (rank 3,
+    channel 5, step 3, chunk 1, 4 KiB into it) recovered bit-identical."""
+    count = 12_500_000
+    send = torch.empty((K_RANKS, count), dtype=torch.bfloat16, device="cuda")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    send.copy_(torch.randn(send.shape, generator=g, device="cuda", dtype=torch.float32).to(torch.bfloat16))
+    recv = torch.empty_like(send)
+    comm = sim_comm(K_RANKS, 8, 2, 512 * 1024, max_bytes=2 * count, protocol="LL128")
+    geo = R.geometry(count, R.BFLOAT16, K_RANKS, 8, 2, 512 * 1024)
+    T.allreduce(comm, send, recv)
+    assert comm.sync() == R.SUCCESS
+    assert comm.status()["last_protocol"] == "LL128"
+    rng = np.random.default_rng(9)
+    idx = np.unique(rng.integers(0, count, size=4096))
+    it = torch.from_numpy(idx).cuda()
+    xs = send[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
+    got = recv[:, it].view(torch.int16).cpu().numpy().view(np.uint16)
+    for col, i in enumerate(idx):
+        want = OS.ring_fold([xs[r, col:col + 1] for r in range(K_RANKS)], int(i) // geo.shard, "bfloat16")[0]
+        assert np.all(got[:, col] == want), int(i)
+    healthy = recv.clone()
+    seq = comm.status()["seq"] + 1
+    comm.inject_fault(at_seq=seq, kind="LINK", src_rank=3, channel=5, step=3, chunk=min(1, geo.m - 1),
+                      byte_offset=4096, poison=1)
+    recv.view(torch.uint8).fill_(0xFF)
+    T.allreduce(comm, send, recv)
+    assert comm.sync() == R.SUCCESS
+    assert torch.equal(recv, healthy)
+    ev = comm.events()
+    assert len(ev) == 1 and ev[0]["verdict"] == "LINK"
+    comm.finalize()
