@@ -727,7 +727,7 @@ def r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier, reduce_ma
     out = {"channel_gbps": a.bw_model_gbps, "degraded_rank": f, "threshold_X": world / (3 * world - 2), "cases": []}
     for d in (K // 2, 3 * K // 4):
         row = {"dead_channels": d, "X": d / K}
-        for algo in ("RING", "R2CC"):
+        for algo in ("RING", "R2CC", "AUTO"):
             c = T.comm_from_env(R.config_default(
                 nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
                 strategy="BALANCE", protocol="SIMPLE", channel_gbps=a.bw_model_gbps, allreduce_algo=algo))
@@ -745,6 +745,8 @@ def r2cc_section(a, T, R, send, recv, S, world, K, W, stream, barrier, reduce_ma
             if algo == "R2CC":
                 row["Y"] = st["r2cc"]["Y"]
                 row["NA_NP"] = [st["r2cc"]["NA"], st["r2cc"]["NP"]]
+            if algo == "AUTO":       # the alpha-beta choice (reading R-11)
+                row["auto_chose"] = "R2CC" if st["r2cc"]["calls"] > 0 else "RING"
             c.finalize()
             barrier()
         row["r2cc_speedup_over_ring"] = row["ring"]["ms"] / row["r2cc"]["ms"]

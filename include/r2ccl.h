@@ -137,6 +137,12 @@ typedef struct {
  *                     capacity 0 (reading R-13) -- and runs the collective on the
  *                     re-ranked ring R' (AllReduce only: its result does not
  *                     depend on which rank owns which shard); 0 keeps rank order
+ *   r2cc_stage1_eff_pct, r2cc_stage2_eff_pct
+ *                     the AUTO algorithm choice divides R²CCL-AllReduce's stage
+ *                     bandwidth terms by these measured efficiencies
+ *                     (defaults 75 / 50: stage 1 0.79 ms vs 0.59 modelled, the
+ *                     tailored broadcast 0.89 vs 0.44; reading R-11); 100 / 100
+ *                     is the paper's model as written
  *   alpha_simple_ns, alpha_ll_ns, alpha_ll128_ns, beta_mbps
  *                     cost model: T = (#ring steps) * alpha + (wire bytes per
  *                     rank) / beta, LL moving twice the bytes and LL128 8/7 of
@@ -177,6 +183,8 @@ typedef struct {
   int alpha_launch_ns;  /* cost model: one more collective launch (R²CCL stage 2)    */
   int alpha_ll128_ns;   /* cost model: per ring step under LL128                     */
   int rerank;           /* 1 (default): ring AllReduce on Algorithm 1's re-ranked ring */
+  int r2cc_stage1_eff_pct, r2cc_stage2_eff_pct;  /* cost model: measured efficiency of
+                           R²CCL-AllReduce's stages vs their bandwidth terms (75, 50) */
 } r2_config_t;
 
 /*

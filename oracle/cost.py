@@ -95,19 +95,22 @@ def r2cc_split(N: int, V: int, Y: float) -> tuple[int, int]:
     return NA, N - NA
 
 
-def algo_times(n: int, X: float, Y: float, S: float, alpha: float, B: float, launch: float):
+def algo_times(n: int, X: float, Y: float, S: float, alpha: float, B: float, launch: float,
+               eff1: float = 1.0, eff2: float = 1.0):
     """Reading R-11 (the alpha-beta strategy choice of SURVEY §8(f) f3):
     per-call time of the ring on the degraded communicator and of
     R²CCL-AllReduce, each = (ring steps) x alpha + the paper's bandwidth terms
     (P:121-130 with g = 1, B = per-GPU rate): the ring is throttled to
     (1 - X) B at the degraded rank; R²CCL-AllReduce pays max(T1, T2) + T3 plus
-    the n steps and the launch of its stage 2.  Returns (t_ring, t_r2cc)."""
+    the n steps and the launch of its stage 2.  eff1 / eff2: the fraction of
+    its bandwidth model stage 1 / stage 2 achieve (1 = the paper's model; the
+    library's defaults are measured, reading R-11).  Returns (t_ring, t_r2cc)."""
     t_ring = (2 * n - 2) * alpha + ring_allreduce_time(n, 1, S, (1 - X) * B)
     if Y <= 0:
         return t_ring, float("inf")
     T1, T2, T3 = stage_times(Y, n, 1, X, S, B)
     # the partial ring has n - 1 members: P:123's (n-1)g ring factor
-    return t_ring, (2 * n - 2) * alpha + max(T1, T2) + n * alpha + T3 + launch
+    return t_ring, (2 * n - 2) * alpha + max(T1, T2) / eff1 + n * alpha + T3 / eff2 + launch
 
 
 def bottleneck_load(Y: float, D: float = 1.0) -> float:

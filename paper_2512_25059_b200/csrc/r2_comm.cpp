@@ -268,6 +268,8 @@ extern "C" void r2_config_default(r2_config_t* cfg) {
   cfg->watchdog_ms = 3000;
   cfg->use_channel_w = 0;
   cfg->rerank = 1;
+  cfg->r2cc_stage1_eff_pct = 75;   // measured stage efficiencies (profiles/r02_summary.md, R²CCL stages)
+  cfg->r2cc_stage2_eff_pct = 50;
   for (int i = 0; i < R2_MAX_CHANNELS; ++i) cfg->channel_w[i] = 1;
   cfg->sim_ranks = 1;
   cfg->protocol = R2_PROTO_AUTO;
@@ -1003,7 +1005,10 @@ bool r2cc_faster(const r2_comm* c, const R2ccPlan& pl, size_t count, r2_dtype_t 
   const double T1 = 2.0 * (n - 1) / n * (1 - Y) * S / ((1 - X) * B);
   const double T2 = 2.0 * (n - 2) / (n - 1) * Y * S / (X * B);
   const double T3 = Y * S / (X * B);
-  const double t_r2cc = (2 * n - 2) * a + std::max(T1, T2) + n * a + T3 + c->cfg.alpha_launch_ns;
+  // stage efficiencies: the fraction of its bandwidth model each stage reaches
+  // on this implementation (reading R-11; measured, tools/r2cc_stages.py)
+  const double e1 = std::max(c->cfg.r2cc_stage1_eff_pct, 1) / 100.0, e2 = std::max(c->cfg.r2cc_stage2_eff_pct, 1) / 100.0;
+  const double t_r2cc = (2 * n - 2) * a + std::max(T1, T2) / e1 + n * a + T3 / e2 + c->cfg.alpha_launch_ns;
   return t_r2cc < t_ring;
 }
 

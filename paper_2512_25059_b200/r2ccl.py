@@ -49,7 +49,8 @@ class Config(C.Structure):
                 ("protocol", C.c_int), ("ll_max_bytes", C.c_size_t), ("alpha_simple_ns", C.c_int),
                 ("alpha_ll_ns", C.c_int), ("beta_mbps", C.c_int), ("reprobe_us", C.c_int),
                 ("reprobe_max_us", C.c_int), ("channel_gbps", C.c_int), ("allreduce_algo", C.c_int),
-                ("alpha_launch_ns", C.c_int), ("alpha_ll128_ns", C.c_int), ("rerank", C.c_int)]
+                ("alpha_launch_ns", C.c_int), ("alpha_ll128_ns", C.c_int), ("rerank", C.c_int),
+                ("r2cc_stage1_eff_pct", C.c_int), ("r2cc_stage2_eff_pct", C.c_int)]
 
 
 PROTO_AUTO, PROTO_SIMPLE, PROTO_LL, PROTO_LL128 = 0, 1, 2, 3

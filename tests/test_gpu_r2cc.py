@@ -146,7 +146,8 @@ def test_auto_choice_matches_the_cost_model():
         xs = r2inputs.inputs(n, N, "float32", seed=N)
         X, Y, NA, NP, y = expected(comm, xs, "float32", f, dead, K)
         t_ring, t_r2 = OC.algo_times(n, X, NP / N, N * 4.0, float(cfg.alpha_simple_ns), cfg.beta_mbps / 1000.0,
-                                     float(cfg.alpha_launch_ns))
+                                     float(cfg.alpha_launch_ns), cfg.r2cc_stage1_eff_pct / 100.0,
+                                     cfg.r2cc_stage2_eff_pct / 100.0)
         calls0 = comm.status()["r2cc"]["calls"]
         rc, out = run_ar(comm, xs, "float32")
         assert rc == R.SUCCESS
