@@ -702,8 +702,12 @@ __device__ void fire_fault(const Cta& k, const FaultDev& f, int t, int o, int j)
 
 // control lane: item delivered -> completion word (+ Balance counter).  The
 // caller has issued the release fence (one for every chunk retired together).
+// dl_acc / by_acc: the rank's delivered-items and this channel's byte
+// counters, accumulated over a retire batch by the caller (one atomic each
+// per batch instead of two per chunk)
 __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, unsigned int parts,
-                              unsigned int epoch, bool own, unsigned int nbytes, bool local) {
+                              unsigned int epoch, bool own, unsigned int nbytes, bool local, unsigned int& dl_acc,
+                              unsigned long long& by_acc) {
   const LaunchParams& p = *k.p;
   bool last = true;
   const size_t fi = fidx(p, t, o, j);
@@ -726,9 +730,9 @@ __device__ void complete_item(const Cta& k, Shared& sh, int t, int o, int j, uns
     // the completion word lives with its consumer: the receiver, or this rank
     // itself for a LOCAL item (ReduceScatter's final add, reading R-5)
     st_relaxed_sys((local ? k.me->flags : k.nx->flags) + fi, k.seq);
-    atomicAdd(&k.me->misc->delivered, 1u);
+    dl_acc++;
   }
-  if (!local) atomicAdd(&k.me->bytes[k.cg], (unsigned long long)nbytes);
+  if (!local) by_acc += nbytes;
   if (!own && sh.first_adopt == 0) {
     // failover latency endpoint: first retransmitted chunk's flag
     sh.first_adopt = gtimer();
@@ -1276,6 +1280,8 @@ __device__ int control_run(Cta& k, Shared& sh) {
       bool any = false;
       for (unsigned int i = 0; i < nd; ++i) any |= sh.meta[(sh.fin + i) % NSLOT].kind != META_END;
       if (any && !p.ll) fence_sys();   // LL lines validate themselves: no fence
+      unsigned int dl_acc = 0;
+      unsigned long long by_acc = 0;
       for (unsigned int i = 0; i < nd; ++i) {
         const Meta& m = sh.meta[(sh.fin + i) % NSLOT];
         if (m.kind == META_ITEM && sh.slot_ab[(sh.fin + i) % NSLOT]) {
@@ -1286,13 +1292,15 @@ __device__ int control_run(Cta& k, Shared& sh) {
             sh.reissue = 1;
           }
         } else if (m.kind == META_ITEM) {
-          complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes, m.local != 0);
+          complete_item(k, sh, m.t, m.o, m.j, m.parts, m.epoch, m.own, m.nbytes, m.local != 0, dl_acc, by_acc);
           if (m.own && m.t < 28) TRACE_MAX(k, 4 + m.t);
         } else if (m.kind == META_FIRE) {
           atomicAdd(&k.me->bytes[k.cg], (unsigned long long)sh.slot[(sh.fin + i) % NSLOT].nvec * 16ull);
           fire_fault(k, p.faults[m.fault], m.t, m.o, m.j);
         }
       }
+      if (dl_acc) atomicAdd(&k.me->misc->delivered, dl_acc);
+      if (by_acc) atomicAdd(&k.me->bytes[k.cg], by_acc);
       if (p.trace == 2 && k.cta_in_rank == 0)
         for (unsigned int i = 0; i < nd; ++i)
           if (sh.fin + i < 8) k.me->misc->trace[16 + sh.fin + i] = gtimer();   // retire i
