@@ -487,6 +487,9 @@ __device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 // WHOLE by that part (vectors outside the part are recomputed from the same
 // inputs, so two parts sharing a boundary line write identical bytes).
 #define LL128_PAY 7
+#ifndef R2_LL128_U
+#define R2_LL128_U 4
+#endif
 template <int U>
 __device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
                                                const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
@@ -532,7 +535,7 @@ __device__ bool move_ll128(const LaunchParams& p, unsigned int dtid, unsigned in
                            unsigned int lo, unsigned int nvec, unsigned int cvec, unsigned long long lim,
                            bool aligned, unsigned int seq, const volatile unsigned int* abort_word,
                            const volatile int* bail) {
-  constexpr int U = 4;                    // line groups per warp per iteration (memory-level parallelism)
+  constexpr int U = R2_LL128_U;           // line groups per warp per iteration (memory-level parallelism)
   const int E = p.elem_bytes, V = p.V;
   const unsigned int lane = dtid & 31u, wid = dtid >> 5, nw = dn >> 5;
   const unsigned int pos = lane & 7u;
