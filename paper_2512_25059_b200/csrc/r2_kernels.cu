@@ -487,9 +487,11 @@ __device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 // WHOLE by that part (vectors outside the part are recomputed from the same
 // inputs, so two parts sharing a boundary line write identical bytes).
 #define LL128_PAY 7
-#ifndef R2_LL128_U
-#define R2_LL128_U 4
-#endif
+// line groups per warp per iteration: 2 for items of up to R2_LL128_SMALL
+// lines, 4 above (U = 2 measured 8 % faster at 16 MiB and 3 % slower at
+// 64-128 MiB than U = 4 at N=4; U = 8 slower everywhere:
+// profiles/r02_ll128_unroll.txt)
+#define R2_LL128_SMALL 512
 template <int U>
 __device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
                                                const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
@@ -529,13 +531,12 @@ __device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[
 // thread index / count over the data warps (multiples of 32).  Line loads and
 // line stores are issued by the converged warp (__syncwarp before each), so
 // the 8 lanes of a line always access it in one instruction.
-template <int DT>
+template <int DT, int U>
 __device__ bool move_ll128(const LaunchParams& p, unsigned int dtid, unsigned int dn, const char* src, bool src_ll,
                            const char* s_in, char* d_rem, char* d_loc, bool loc_user, unsigned long long e0,
                            unsigned int lo, unsigned int nvec, unsigned int cvec, unsigned long long lim,
                            bool aligned, unsigned int seq, const volatile unsigned int* abort_word,
                            const volatile int* bail) {
-  constexpr int U = R2_LL128_U;           // line groups per warp per iteration (memory-level parallelism)
   const int E = p.elem_bytes, V = p.V;
   const unsigned int lane = dtid & 31u, wid = dtid >> 5, nw = dn >> 5;
   const unsigned int pos = lane & 7u;
@@ -1411,8 +1412,13 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     }
     bool gave = false;
     if (p.ll == 2)
-      gave = move_ll128<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0,
-                            d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort, &sh.abandon);
+      gave = d.cvec <= R2_LL128_SMALL * LL128_PAY
+                 ? move_ll128<DT, 2>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
+                                     d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
+                                     &sh.abandon)
+                 : move_ll128<DT, 4>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
+                                     d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
+                                     &sh.abandon);
     else if (p.ll)
       gave = move_ll<DT>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0, d.e0, d.nvec,
                          d.lim, d.aligned != 0, k.seq, k.me->abort, &sh.abandon);
