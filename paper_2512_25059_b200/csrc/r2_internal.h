@@ -200,9 +200,9 @@ struct LaunchParams {
   int n, K, W, m, steps, nlocal, first_rank;   // nlocal: participating local ranks of this ring
   int ng, Kg;                            // communicator ranks / channels
   int ring_id;                           // 0 / 1: which region set (RankPtrs table)
-  int ring[R2_MAXR];                     // global rank at ring position
-  int chan[R2_MAXK];                     // global channel of ring-local channel
-  int part_l[R2_MAXL];                   // process-local index of participant i (sim mode: its global rank)
+  unsigned char ring[R2_MAXR];           // global rank at ring position
+  unsigned char chan[R2_MAXK];           // global channel of ring-local channel
+  unsigned char part_l[R2_MAXL];         // process-local index of participant i (sim mode: its global rank)
   unsigned long long peer_recv_off;      // bytes added to a downstream rank's registered recv (ring region)
   unsigned int* grid_exited;             // local rank 0's ring-0 misc: (ring, rank) pairs done
   unsigned int exit_target;              // (ring, local rank) pairs of the whole launch
