@@ -491,7 +491,12 @@ __device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 // lines, 4 above (U = 2 measured 8 % faster at 16 MiB and 3 % slower at
 // 64-128 MiB than U = 4 at N=4; U = 8 slower everywhere:
 // profiles/r02_ll128_unroll.txt)
+#ifndef R2_LL128_SMALL
 #define R2_LL128_SMALL 512
+#endif
+#ifndef R2_LL128_ULARGE
+#define R2_LL128_ULARGE 4
+#endif
 template <int U>
 __device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
                                                const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
@@ -1416,7 +1421,8 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
                  ? move_ll128<DT, 2>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
                                      d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
                                      &sh.abandon)
-                 : move_ll128<DT, 4>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
+                 : move_ll128<DT, R2_LL128_ULARGE>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc,
+                                                   d.loc_user != 0,
                                      d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
                                      &sh.abandon);
     else if (p.ll)
