@@ -488,11 +488,11 @@ __device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 // inputs, so two parts sharing a boundary line write identical bytes).
 #define LL128_PAY 7
 // line groups per warp per iteration: 2 for items of up to R2_LL128_SMALL
-// lines, 4 above (U = 2 measured 8 % faster at 16 MiB and 3 % slower at
-// 64-128 MiB than U = 4 at N=4; U = 8 slower everywhere:
+// lines, 4 above (U = 2 measured 8 % faster at 16 MiB, 4 % at 32 MiB and 3 %
+// slower at 64-128 MiB than U = 4 at N=4; U = 3 and U = 8 slower:
 // profiles/r02_ll128_unroll.txt)
 #ifndef R2_LL128_SMALL
-#define R2_LL128_SMALL 512
+#define R2_LL128_SMALL 1024
 #endif
 #ifndef R2_LL128_ULARGE
 #define R2_LL128_ULARGE 4
