@@ -497,6 +497,9 @@ __device__ bool move_ll(const LaunchParams& p, unsigned int tid, unsigned int nt
 #ifndef R2_LL128_ULARGE
 #define R2_LL128_ULARGE 4
 #endif
+#ifndef R2_LL128_TINY
+#define R2_LL128_TINY 256        // chunks of up to this many lines: one line group per iteration
+#endif
 template <int U>
 __device__ __forceinline__ bool ll128_validate(uint4 (&x)[U], const bool (&act)[U], const char* q,
                                                const unsigned int (&L)[U], unsigned int lane, unsigned int seq,
@@ -1417,7 +1420,11 @@ __device__ void data_run(const Cta& k, Shared& sh, unsigned int& dcount) {
     }
     bool gave = false;
     if (p.ll == 2)
-      gave = d.cvec <= R2_LL128_SMALL * LL128_PAY
+      gave = d.cvec <= R2_LL128_TINY * LL128_PAY
+                 ? move_ll128<DT, 1>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
+                                     d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
+                                     &sh.abandon)
+             : d.cvec <= R2_LL128_SMALL * LL128_PAY
                  ? move_ll128<DT, 2>(p, dtid, dn, d.src, d.src_ll != 0, d.s_in, d.d_rem, d.d_loc, d.loc_user != 0,
                                      d.e0, d.lo_c, d.nvec, d.cvec, d.lim, d.aligned != 0, k.seq, k.me->abort,
                                      &sh.abandon)
