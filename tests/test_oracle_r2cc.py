@@ -192,3 +192,31 @@ def test_strategy_choice_latency_bound():
     small = C.algo_times(n, X, Y, 64e3, 7150.0, 650.0, 6000.0)
     big = C.algo_times(n, X, Y, 256e6, 7150.0, 650.0, 6000.0)
     assert small[0] < small[1] and big[1] < big[0]
+
+
+def test_stage_efficiencies_shift_the_choice_toward_the_ring():
+    """Reading R-11's calibration: dividing the stage terms by efficiencies
+    below 1 only ever makes R²CCL-AllReduce slower (never changes the ring's
+    time), so the set of X where it is chosen shrinks monotonically; with
+    efficiencies 1 it is App. A's choice.  With the library's defaults
+    (0.75, 0.50) the ring is chosen at X = 0.5 for n = 4 (measured: R²CCL
+    0.68x the ring there) and R²CCL at X = 0.75 (measured 1.0x)."""
+    for n in (3, 4, 8):
+        chosen = {}
+        for e1, e2 in ((1.0, 1.0), (0.9, 0.8), (0.75, 0.5), (0.5, 0.3)):
+            chosen[(e1, e2)] = set()
+            for X in np.linspace(0.01, 0.99, 99):
+                Y = C.optimal_partition(n, 1, X)
+                t_ring, t_r2 = C.algo_times(n, X, Y, 1.0, 0.0, 1.0, 0.0, e1, e2)
+                t_ring1, _ = C.algo_times(n, X, Y, 1.0, 0.0, 1.0, 0.0)
+                assert t_ring == t_ring1
+                if t_r2 < t_ring:
+                    chosen[(e1, e2)].add(round(X, 4))
+        keys = list(chosen)
+        for a, b in zip(keys, keys[1:]):
+            assert chosen[b] <= chosen[a], (n, a, b)
+    n = 4
+    for X, want_r2 in ((0.5, False), (0.75, True)):
+        Y = C.optimal_partition(n, 1, X)
+        t_ring, t_r2 = C.algo_times(n, X, Y, 1.0, 0.0, 1.0, 0.0, 0.75, 0.5)
+        assert (t_r2 < t_ring) == want_r2, X
