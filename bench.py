@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--threads", type=int, default=0,
                     help="threads per CTA (0 = auto: 512 for the HBM-bound simulated ranks, 256 on GPUs -- "
                          "profiles/r01_sweep_threads_n4.log)")
-    ap.add_argument("--chunk", type=int, default=512 * 1024)
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="chunk bytes (0 = auto: 512 KiB for the simulated ranks, 1 MiB on GPUs -- "
+                         "profiles/r02_chunk_n24.txt)")
     ap.add_argument("--no-fault", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -357,6 +359,7 @@ def run_sim(a):
     torch.cuda.set_device(0)
     k, K, S = a.sim_ranks, a.channels, a.bytes
     W = a.ctas or max(1, min(4, 148 // (k * K)))
+    a.chunk = a.chunk or 512 * 1024
     count = S // 2
     mk = lambda strategy: R.Comm(0, 1, 0, None, R.config_default(
         sim_ranks=k, nchannels=K, ctas_per_channel=W, threads_per_cta=a.threads, chunk_bytes=a.chunk,
@@ -428,6 +431,7 @@ def run_multi(a):
     B.build()
     K, S = a.channels, a.bytes
     W = a.ctas or 16          # 8 x 16 = 128 CTAs/GPU: best of the W sweep (profiles/r01_summary.md)
+    a.chunk = a.chunk or 1024 * 1024   # one chunk per lane and step at N = 2 (profiles/r02_chunk_n24.txt)
     count = S // 2
     send = torch.empty(count, dtype=torch.bfloat16, device="cuda")
     recv = torch.empty_like(send)
