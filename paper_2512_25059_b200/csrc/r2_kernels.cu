@@ -183,7 +183,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned int pa
 // slot has a `full` (control -> data) and an `empty` (data -> control)
 // mbarrier.  The control warp retires finished chunks in order with ONE
 // fence.acq_rel.sys for all chunks finished since its last retire.
-#define NSLOT 4
+// 8 slots: the control lane publishes a whole small collective's items
+// before its first retire (vs 4 slots: 1.5 us less per small LL call at
+// N=4, 64 MiB 4-8 % faster, N=2 unchanged; profiles/r02_nslot.txt)
+#ifndef R2_NSLOT
+#define R2_NSLOT 8
+#endif
+#define NSLOT R2_NSLOT
 enum { SLOT_GO = 0, SLOT_END = 1 };
 enum { META_ITEM = 0, META_FIRE = 1, META_END = 2 };
 
@@ -230,6 +236,7 @@ struct Shared {
   unsigned long long wait_t0;
   unsigned long long t_poll, t_prev_poll;   // diagnostics
   unsigned long long t_ctl;                 // last control / fabric check of try_publish
+  unsigned long long ph[6];                 // R2_TRACE=3: SM cycles per try_publish phase
   unsigned long long pace_next;             // channel bandwidth model: earliest next send
   unsigned int npoll;
   unsigned long long full[NSLOT];
@@ -908,6 +915,14 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   int fire = 0;
   unsigned int fire_nvec = 0;
   int poison = 0;
+  const bool prof = p.trace == 3 && k.cta_in_rank == 0 && k.l == 0;
+  long long q0 = prof ? clock64() : 0;
+#define R2_PH(i)                \
+  if (prof) {                   \
+    const long long q = clock64(); \
+    sh.ph[i] += q - q0;         \
+    q0 = q;                     \
+  }
   const unsigned long long key = keyof(it.t, it.o, it.j);
   for (int i = 0; i < p.nfaults; ++i) {
     const FaultDev& f = p.faults[i];
@@ -926,6 +941,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
       poison = f.poison;
     }
   }
+  R2_PH(0);
   // control words and the emulated fabric state: at most once per ~10 us
   // (40k SM cycles; each check is a handful of global loads, ~2.5 us per
   // publish when done every time -- it was the latency floor of small LL
@@ -952,6 +968,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   // and an own item's inputs never depend on a later item of the same lane.
   // Once alerted, items wait for the completion word again (an adopted
   // residual must never queue behind a spinning item that needs it).
+  R2_PH(1);
   const bool spec = p.ll && p.spec_ok && !sh.alerted && !sh.dynamic;
   if (it.t > 0 && !spec) {
     const unsigned int* w = k.me->flags + fidx(p, it.t - 1, it.o, it.j);
@@ -962,6 +979,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     // causality chain of the PTX memory model
     if (!p.ll) (void)ld_acquire_sys(w);
   }
+  R2_PH(2);
   const int t = it.t;
   const int ta = t + p.t0;                            // the AllReduce step this op-step is
   const bool local = t == p.local_step;
@@ -976,6 +994,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     sh.pace_next = (now > sh.pace_next ? now : sh.pace_next) + wire * p.lane_ps_per_byte / 1000ull;
   }
 
+  R2_PH(3);
   const int E = p.elem_bytes, V = p.V;
   const bool chain = p.op == R2_OP_BROADCAST || p.op == R2_OP_R2CC_STAGE2;
   // shard of this step (computed once per CTA: sh.sbase / sh.slim, worker_main)
@@ -1129,6 +1148,7 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
   m.nbytes = (it.hi - it.lo) * 16u;
   m.own = it.own;
   m.fault = fire - 1;
+  R2_PH(4);
   sh.slot[u] = d;
   sh.meta[u] = m;
   mbar_arrive(&sh.full[u]);
@@ -1140,6 +1160,8 @@ __device__ int try_publish(Cta& k, Shared& sh, const ItemRef& it, bool first_try
     TRACE_MIN(k, 2);
   }
   *fired = fire != 0;
+  R2_PH(5);
+#undef R2_PH
   return ST_OK;
 }
 
@@ -1352,6 +1374,7 @@ __device__ int control_run(Cta& k, Shared& sh) {
         tr[52] = (unsigned long long)c_it, tr[53] = (unsigned long long)n_it;
         tr[54] = (unsigned long long)c_ret, tr[55] = (unsigned long long)n_ret;
         tr[56] = (unsigned long long)(clock64() - c_start);
+        for (int i = 0; i < 6; ++i) tr[40 + i] = sh.ph[i];
       }
       mbar_arrive(&sh.full[u]);
       sh.pub++;
@@ -2056,6 +2079,7 @@ __device__ __forceinline__ void worker_main(const LaunchParams& p, unsigned int 
     sh.wait_t0 = 0;
     sh.t_poll = sh.t_prev_poll = 0;
     sh.t_ctl = (unsigned long long)clock64();   // the plan was read just now: first check after the interval
+    for (int i = 0; i < 6; ++i) sh.ph[i] = 0;
     sh.pace_next = 0;
     sh.npoll = 0;
     CtaRec& rec = k.ctrl->cta[k.cta_in_rank];

@@ -1,7 +1,7 @@
 # Round-2 evidence (4-GPU box): tests, smoke (plain + ncu), bench N=1/2/4, ncu of the N=1 kernel,
 # size sweeps N=2/4, config 5 at N=4, reference arm
 set -x
-O=gpurun_out/fin8; mkdir -p $O
+O=gpurun_out/fin9; mkdir -p $O
 nvidia-smi > $O/nvidia-smi.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -3 $O/pytest_gpu.log
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?"; tail -1 $O/smoke.log
@@ -21,7 +21,7 @@ python - <<'PY'
 import json
 for n in (1, 2, 4):
     try:
-        d = json.load(open(f"gpurun_out/fin8/bench_n{n}.json")); r = d["roofline"]
+        d = json.load(open(f"gpurun_out/fin9/bench_n{n}.json")); r = d["roofline"]
         print(n, d["ms_per_step"], round(d["value"], 1), round(r["frac"], 3), r.get("traffic_over_algorithmic"), (d.get("e2e") or {}).get("value"),
               (d.get("small_footprint") or {}).get("busbw_per_rank"), (d.get("nccl_same_box") or {}).get("busbw_per_gpu"))
     except Exception as e: print(n, e)

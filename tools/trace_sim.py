@@ -42,6 +42,10 @@ def main():
             cyc = lambda c, k: f"{c / max(k, 1):.0f} cyc x {k}"  # noqa: E731
             print(f"   control lane of CTA 0: try_publish {cyc(buf[50], buf[51])}, iter_next {cyc(buf[52], buf[53])}, "
                   f"retire {cyc(buf[54], buf[55])} per chunk, control_run total {buf[56]} cyc", flush=True)
+            k = max(buf[51], 1)
+            print("   try_publish phases (cyc per publish): faults %.0f, control check %.0f, input word %.0f, "
+                  "recv/pace %.0f, slot build %.0f, store+arrive %.0f" % tuple(buf[40 + i] / k for i in range(6)),
+                  flush=True)
     comm.finalize()
 
 
