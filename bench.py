@@ -1,7 +1,7 @@
 """bench.py -- R²CCL hot path on B200: fault-tolerant ring allreduce.
 
 Workload (BASELINE.json configs[2]): 256 MiB bf16
-per rank, K = 8 channels, 512 KiB chunks.
+per rank, K = 8 channels, 512 KiB chunks (1 MiB on GPUs, --chunk).
   N = 1  (default): 8 simulated ranks on one B200 in one cooperative kernel
          (the "1 GPU local reduce" configuration; all traffic is HBM).
   N > 1 (torchrun): one process per GPU, CUDA-IPC peer stores over NVLink 5.
@@ -650,7 +650,9 @@ def small_footprint(a, T, R, send, recv, S, world, K, stream, barrier, reduce_ma
     import torch
     want = recv.clone()
     c = T.comm_from_env(R.config_default(
-        nchannels=K, ctas_per_channel=a.ctas_small, threads_per_cta=a.threads, chunk_bytes=a.chunk, max_bytes=S,
+        # 512 KiB chunks: with 4 CTAs per channel a lane then carries 4 chunks per step, whose
+        # retires overlap the next chunk's transfer (1 MiB: 537 / 592 GB/s at N=2 / 4 vs 556-582 / 619-636)
+        nchannels=K, ctas_per_channel=a.ctas_small, threads_per_cta=a.threads, chunk_bytes=512 * 1024, max_bytes=S,
         strategy="BALANCE", protocol=a.protocol))
     T.register(c, recv)
     step = lambda: T.allreduce(c, send, recv)  # noqa: E731

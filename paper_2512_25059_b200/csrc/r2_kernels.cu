@@ -184,8 +184,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned int pa
 // mbarrier.  The control warp retires finished chunks in order with ONE
 // fence.acq_rel.sys for all chunks finished since its last retire.
 // 8 slots: the control lane publishes a whole small collective's items
-// before its first retire (vs 4 slots: 1.5 us less per small LL call at
-// N=4, 64 MiB 4-8 % faster, N=2 unchanged; profiles/r02_nslot.txt)
+// before its first retire (same-box A/B vs 4 slots: N=4 LL calls 32.4 ->
+// 31.1 us; N=2 and >= 4 MiB within run-to-run noise; profiles/r02_nslot.txt)
 #ifndef R2_NSLOT
 #define R2_NSLOT 8
 #endif
