@@ -651,7 +651,7 @@ def small_footprint(a, T, R, send, recv, S, world, K, stream, barrier, reduce_ma
     want = recv.clone()
     c = T.comm_from_env(R.config_default(
         # 512 KiB chunks: with 4 CTAs per channel a lane then carries 4 chunks per step, whose
-        # retires overlap the next chunk's transfer (1 MiB: 537 / 592 GB/s at N=2 / 4 vs 556-582 / 619-636)
+        # retires overlap the next chunk's transfer (N=2: 1 MiB 537 GB/s, 512 KiB 566; profiles/r02_summary.md)
         nchannels=K, ctas_per_channel=a.ctas_small, threads_per_cta=a.threads, chunk_bytes=512 * 1024, max_bytes=S,
         strategy="BALANCE", protocol=a.protocol))
     T.register(c, recv)
